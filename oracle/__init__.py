@@ -1,0 +1,110 @@
+"""fp64 CPU oracle of the batched NDF range query (Deng et al., arXiv 2109.14807).
+
+TEST INFRASTRUCTURE ONLY: only tests/, __graft_entry__.smoke() and bench.py's
+cpu_baseline / ``--impl reference`` legs may import this package.  It shares no
+code with the CUDA path (``paper_2109_14807_b200``) and never imports it.
+
+Two independent implementations:
+  * ``query_batch``  -- oracle.c, the plain definition written out in fp64
+    (Eq. 6 per neighbour; trilinear blend; clamp);
+  * ``brute.py``     -- numpy brute force for tiny inputs: reconstruct the
+    tensor D-hat of Eq. 5 and sum it over the rectangle.
+Both take the RAW factors (C, X, Y, Z) -- not the CUDA path's store image.
+
+Parity pins (tests/test_oracle_pins.py) tie both to what the paper and the
+mathematics fix; DESIGN.md §4 lists them.  No function here is "parity unpinned".
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "oracle.c")
+_LIB_PATH = os.path.join(_HERE, "_liboracle.so")
+_lib = None
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("s0", ctypes.c_int32), ("L", ctypes.c_int32),
+                ("A", ctypes.c_int32), ("R", ctypes.c_int32), ("wrap", ctypes.c_int32)]
+
+
+def build_lib(force: bool = False) -> str:
+    """gcc -O2 -fopenmp (no -ffast-math, no hand SIMD)."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".{os.getpid()}.tmp"
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-shared", "-fPIC", "-Wall", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        build_lib()
+        L = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.c_void_p
+        L.oracle_query_batch.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, P, ctypes.c_int64, ctypes.c_int, P,
+                                         ctypes.c_int]
+        L.oracle_neighbours_batch.argtypes = [ctypes.POINTER(Desc), P, ctypes.c_int64, P, P]
+        L.oracle_max_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def max_threads() -> int:
+    return lib().oracle_max_threads()
+
+
+def _ptr(a):
+    return None if a is None else ctypes.c_void_p(a.ctypes.data)
+
+
+def make_desc(N, s0, L, A, R, wrap=True) -> Desc:
+    return Desc(N=N, s0=s0, L=L, A=A, R=R, wrap=1 if wrap else 0)
+
+
+def desc_of(cfg) -> Desc:
+    return make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap)
+
+
+def query_batch(desc: Desc, C, X, Y, Z, records: np.ndarray, mean: bool = True, zmap=None,
+                threads: int = 0) -> np.ndarray:
+    """fp64 results for 16-byte records (u, v, size, rect)."""
+    assert desc.R <= 4096
+    C = np.ascontiguousarray(C, np.float32)
+    X = np.ascontiguousarray(X, np.float32)
+    Y = np.ascontiguousarray(Y, np.float32)
+    Z = np.ascontiguousarray(Z, np.float32)
+    assert C.shape == (desc.R,) and X.shape == (desc.A, desc.R) and Y.shape == (desc.A, desc.R)
+    assert Z.ndim == 2 and Z.shape[1] == desc.R
+    recs = np.ascontiguousarray(records)
+    assert recs.dtype.itemsize == 16
+    if zmap is not None:
+        zmap = np.ascontiguousarray(zmap, np.int64)
+    out = np.empty(recs.shape[0], np.float64)
+    lib().oracle_query_batch(ctypes.byref(desc), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(zmap), _ptr(recs),
+                             recs.shape[0], 1 if mean else 0, _ptr(out), threads)
+    return out
+
+
+def neighbours(desc: Desc, records: np.ndarray):
+    """(rows int64 [n,8], weights float64 [n,8]) -- steps 1-2 of the oracle."""
+    recs = np.ascontiguousarray(records)
+    n = recs.shape[0]
+    rows = np.empty((n, 8), np.int64)
+    w = np.empty((n, 8), np.float64)
+    lib().oracle_neighbours_batch(ctypes.byref(desc), _ptr(recs), n, _ptr(rows), _ptr(w))
+    return rows, w
+
+
+def sparse_z(rows_needed: np.ndarray, P: int, row_fn):
+    """Build (Zsub, zmap) holding only the given rows; row_fn(sorted_rows) -> [k, R]."""
+    u = np.unique(rows_needed[rows_needed >= 0])
+    zmap = np.full(P, -1, np.int64)
+    zmap[u] = np.arange(u.shape[0])
+    return np.ascontiguousarray(row_fn(u), np.float32), zmap

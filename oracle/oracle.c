@@ -1,0 +1,190 @@
+/*
+ * oracle.c -- plain fp64 CPU oracle of the batched NDF range query.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline / --impl reference legs may load this library.  It
+ * shares no code with the CUDA path (paper_2109_14807_b200/) and includes none
+ * of its headers: the 16-byte query record and the descriptor are restated
+ * here from the paper's statement of the query.
+ *
+ * What it computes (P:n = line n of /root/reference/PAPER.md), per record
+ * (u, v, S, [x1,x2] x [y1,y2]):
+ *   1. footprint level (Sec. 4.1, "trilinear interpolation between different
+ *      samples in the same level and between different levels", P:276, P:327;
+ *      clamp above the top level):
+ *        l* = clamp(log2(S/s0), 0, L-1), l0 = min(floor(l*), L-2), t = l* - l0
+ *   2. the 4 spatial neighbours on each of levels l0 (weight 1-t), l0+1
+ *      (weight t): centres at ((i+1/2)s_l, (j+1/2)s_l) on a grid of stride
+ *      s_l = s0 2^l, f = u/s_l - 1/2, i0 = floor(f), a = f - i0,
+ *      bilinear weights (1-a)(1-b), a(1-b), (1-a)b, ab; indices wrap modulo
+ *      n_l for tileable maps, clamp to [0, n_l-1] otherwise;
+ *   3. per neighbour z_k, Eq. 6 as a SUM over the rectangle:
+ *        D_k = sum_r C_r (sum_{x=x1..x2} X_r(x)) (sum_{y=y1..y2} Y_r(y)) Z_r(z_k)
+ *      -- the 1-D segment sums are written out directly (the plain definition
+ *      of X-bar times the segment length M, P:345 and Appendix), not
+ *      through a prefix table;
+ *   4. SUM = sum_k w_k D_k ("Eqn. 5 will simply be called multiple times",
+ *      P:327); MEAN = SUM / ((x2-x1+1)(y2-y1+1)) (Eq. 6 is an average).
+ * Everything is accumulated in double from the fp32 factor inputs.
+ *
+ * Invalid records (non-finite or |u|,|v| > 2^22, S <= 0, x1 > x2, x2 >= A,
+ * y1 > y2, y2 >= A) produce NaN (SPEC "invalid range").
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stddef.h>
+#include <omp.h>
+
+#define EXPORT __attribute__((visibility("default")))
+
+typedef struct {
+    int32_t N;    /* map side (texels), power of two              */
+    int32_t s0;   /* base stride, power of two dividing N         */
+    int32_t L;    /* number of levels, 2 <= L <= log2(N/s0) + 1   */
+    int32_t A;    /* angular grid side                            */
+    int32_t R;    /* rank                                         */
+    int32_t wrap; /* 1: periodic neighbours, 0: clamp to edge     */
+} oracle_desc;
+
+typedef struct { float u, v, size; uint32_t rect; } oracle_rec; /* 16 B */
+
+/* Step 1. */
+static void oracle_level(const oracle_desc* d, double S, int* l0, double* t) {
+    double ls = log2(S / (double)d->s0);
+    if (ls < 0.0) ls = 0.0;                 /* below the base level: clamp */
+    if (ls > d->L - 1) ls = d->L - 1;       /* above the top level: "directly clamp" */
+    int f = (int)floor(ls);
+    if (f > d->L - 2) f = d->L - 2;
+    *l0 = f;
+    *t = ls - f;
+}
+
+/* Step 2: neighbour indices and bilinear fraction along one axis. */
+static void oracle_axis(const oracle_desc* d, int l, double u, int64_t* i0, int64_t* i1, double* a) {
+    int64_t s = (int64_t)d->s0 << l, n = d->N / s;
+    double f = u / (double)s - 0.5;
+    double fl = floor(f);
+    *a = f - fl;
+    int64_t i = (int64_t)fl, j = i + 1;
+    if (d->wrap) {
+        i = ((i % n) + n) % n;
+        j = ((j % n) + n) % n;
+    } else {
+        i = i < 0 ? 0 : (i > n - 1 ? n - 1 : i);
+        j = j < 0 ? 0 : (j > n - 1 ? n - 1 : j);
+    }
+    *i0 = i;
+    *i1 = j;
+}
+
+static int64_t oracle_level_offset(const oracle_desc* d, int l) {
+    int64_t off = 0;
+    for (int m = 0; m < l; ++m) {
+        int64_t n = d->N / ((int64_t)d->s0 << m);
+        off += n * n;
+    }
+    return off;
+}
+
+/* Step 3: Eq. 6 sum over the rectangle for one positional index z. */
+static double oracle_range_sum(const oracle_desc* d, const float* C, const double* xs, const double* ys,
+                               const float* zrow) {
+    double acc = 0.0;
+    for (int r = 0; r < d->R; ++r) acc += (double)C[r] * xs[r] * ys[r] * (double)zrow[r];
+    return acc;
+}
+
+static int oracle_valid(const oracle_desc* d, const oracle_rec* q, int* x1, int* x2, int* y1, int* y2) {
+    *x1 = (int)(q->rect & 255u);
+    *x2 = (int)((q->rect >> 8) & 255u);
+    *y1 = (int)((q->rect >> 16) & 255u);
+    *y2 = (int)((q->rect >> 24) & 255u);
+    if (!isfinite(q->u) || !isfinite(q->v) || !isfinite(q->size)) return 0;
+    if (fabs((double)q->u) > 4194304.0 || fabs((double)q->v) > 4194304.0) return 0;
+    if (!(q->size > 0.0f)) return 0;
+    if (*x1 > *x2 || *x2 >= d->A || *y1 > *y2 || *y2 >= d->A) return 0;
+    return 1;
+}
+
+/* One query.  zmap (optional) maps a global row index z to its row in Z
+ * (sparse storage of only the rows a sample touches); NULL = dense [P][R]. */
+static double oracle_query_one(const oracle_desc* d, const float* C, const float* X, const float* Y, const float* Z,
+                               const int64_t* zmap, const oracle_rec* q, int mean, double* xs, double* ys) {
+    int x1, x2, y1, y2;
+    if (!oracle_valid(d, q, &x1, &x2, &y1, &y2)) return NAN;
+    const int R = d->R;
+    /* 1-D segment sums, the numerators of X-bar and Y-bar. */
+    for (int r = 0; r < R; ++r) { xs[r] = 0.0; ys[r] = 0.0; }
+    for (int x = x1; x <= x2; ++x)
+        for (int r = 0; r < R; ++r) xs[r] += (double)X[(int64_t)x * R + r];
+    for (int y = y1; y <= y2; ++y)
+        for (int r = 0; r < R; ++r) ys[r] += (double)Y[(int64_t)y * R + r];
+
+    int l0;
+    double t;
+    oracle_level(d, (double)q->size, &l0, &t);
+    double sum = 0.0;
+    for (int dl = 0; dl < 2; ++dl) {
+        int l = l0 + dl;
+        double wl = dl ? t : 1.0 - t;
+        int64_t n = d->N / ((int64_t)d->s0 << l), off = oracle_level_offset(d, l);
+        int64_t i0, i1, j0, j1;
+        double a, b;
+        oracle_axis(d, l, (double)q->u, &i0, &i1, &a);
+        oracle_axis(d, l, (double)q->v, &j0, &j1, &b);
+        const int64_t zk[4] = {off + j0 * n + i0, off + j0 * n + i1, off + j1 * n + i0, off + j1 * n + i1};
+        const double wk[4] = {(1 - a) * (1 - b), a * (1 - b), (1 - a) * b, a * b};
+        for (int k = 0; k < 4; ++k) {
+            int64_t z = zmap ? zmap[zk[k]] : zk[k];
+            if (z < 0) return NAN; /* a row the sparse sample did not provide */
+            sum += wl * wk[k] * oracle_range_sum(d, C, xs, ys, Z + z * (int64_t)R);
+        }
+    }
+    if (mean) sum /= (double)(x2 - x1 + 1) * (double)(y2 - y1 + 1);
+    return sum;
+}
+
+EXPORT void oracle_query_batch(const oracle_desc* d, const float* C, const float* X, const float* Y, const float* Z,
+                               const int64_t* zmap, const oracle_rec* q, int64_t n, int mean, double* out,
+                               int nthreads) {
+    if (nthreads <= 0) nthreads = omp_get_max_threads();
+#pragma omp parallel num_threads(nthreads)
+    {
+        double xs[4096], ys[4096]; /* R <= 4096 */
+#pragma omp for schedule(static)
+        for (int64_t i = 0; i < n; ++i) out[i] = oracle_query_one(d, C, X, Y, Z, zmap, &q[i], mean, xs, ys);
+    }
+}
+
+/* The 8 (row, weight) pairs of one record, for tests that need the touched
+ * rows (sparse Z samples) -- same steps 1-2 as above. Returns 0 if invalid. */
+EXPORT int oracle_neighbours(const oracle_desc* d, const oracle_rec* q, int64_t* rows, double* w) {
+    int x1, x2, y1, y2;
+    if (!oracle_valid(d, q, &x1, &x2, &y1, &y2)) return 0;
+    int l0;
+    double t;
+    oracle_level(d, (double)q->size, &l0, &t);
+    for (int dl = 0; dl < 2; ++dl) {
+        int l = l0 + dl;
+        double wl = dl ? t : 1.0 - t;
+        int64_t n = d->N / ((int64_t)d->s0 << l), off = oracle_level_offset(d, l);
+        int64_t i0, i1, j0, j1;
+        double a, b;
+        oracle_axis(d, l, (double)q->u, &i0, &i1, &a);
+        oracle_axis(d, l, (double)q->v, &j0, &j1, &b);
+        rows[4 * dl + 0] = off + j0 * n + i0; w[4 * dl + 0] = wl * (1 - a) * (1 - b);
+        rows[4 * dl + 1] = off + j0 * n + i1; w[4 * dl + 1] = wl * a * (1 - b);
+        rows[4 * dl + 2] = off + j1 * n + i0; w[4 * dl + 2] = wl * (1 - a) * b;
+        rows[4 * dl + 3] = off + j1 * n + i1; w[4 * dl + 3] = wl * a * b;
+    }
+    return 1;
+}
+
+EXPORT void oracle_neighbours_batch(const oracle_desc* d, const oracle_rec* q, int64_t n, int64_t* rows, double* w) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        if (!oracle_neighbours(d, &q[i], rows + 8 * i, w + 8 * i))
+            for (int k = 0; k < 8; ++k) { rows[8 * i + k] = -1; w[8 * i + k] = NAN; }
+}
+
+EXPORT int oracle_max_threads(void) { return omp_get_max_threads(); }
