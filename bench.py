@@ -1,0 +1,366 @@
+#!/usr/bin/env python
+"""bench.py -- batched NDF range queries/s on B200 (BASELINE.json "metric").
+
+One step = one pndf_query_batch over this rank's shard of the workload's query
+batch: binning (row a1) + the query kernel (rows a2-a6), inputs resident in HBM.
+Default workload: BASELINE.json configs[4] ("Scaling": 4096^2 flake map, A=R=256,
+10^9 queries sharded over the ranks; factors replicated) -- the config the
+metric's "1/2/4/8 B200" numbers are quoted on, and it fits one GPU.
+
+Launch: python bench.py [--gpus N --steps K --warmup W]; for N > 1 under
+torchrun (one process per GPU, NCCL only for the max-time / checksum reductions
+after the timed region -- the path has no exchange step).
+``--impl reference`` times the fp64 CPU oracle on a bounded sample instead.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402  (seeded inputs; no query arithmetic)
+
+METRIC = "NDF range queries/sec at 1/2/4/8 B200 and % of gather (HBM/L2) roofline"
+UNIT = "queries/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--queries", type=int, default=0, help="override the config's total query count")
+    ap.add_argument("--bin", default="auto", choices=["auto", "on", "off"])
+    ap.add_argument("--lanes", type=int, default=0)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
+    return ap.parse_args()
+
+
+def workload_name(cfg) -> str:
+    return (f"config{cfg.idx}-{cfg.name}: {cfg.N}^2 {cfg.map_kind} map, A={cfg.A}, R={cfg.R}, "
+            f"L={cfg.L} levels (P={cfg.P} rows), {cfg.n_queries:.0e} queries")
+
+
+def bytes_per_query(R: int) -> int:
+    """record 16 B + result 4 B + 8 Z rows + 4 prefix rows of R fp32 = 20 + 48 R."""
+    return 20 + 48 * R
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        return json.load(open(p)), "measured"
+    return {"hbm_gbs": 6650.0}, "fallback"
+
+
+def ncu_traffic(cfg_idx: int):
+    """dram bytes per query-kernel launch from the committed ncu --set full summary, if any."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    return d.get(f"config{cfg_idx}")
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, bus_id: str | None):
+        self.bus_id = bus_id
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            cmd = ["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "200"]
+            if self.bus_id:
+                cmd += ["-i", self.bus_id]
+            self.proc = subprocess.Popen(cmd, stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if not self.proc:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = [r.split(", ") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = max(smax, float(r[2]))
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip() == "Active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def bus_id_of(dev) -> str | None:
+    try:
+        import torch
+        p = torch.cuda.get_device_properties(dev)
+        return f"{p.pci_domain_id:08X}:{p.pci_bus_id:02X}:{p.pci_device_id:02X}.0"
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- inputs --
+def host_inputs(cfg):
+    """Map -> angular bins -> factors (C, X, Y on host; Z stays None for exact-rank configs)."""
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    del nxy
+    if cfg.factor_kind == "als":
+        f = synth.build_factors(cfg, None, bins)
+    else:
+        f = synth.build_factors(cfg, None, bins, with_z=False)
+    return bins, f
+
+
+def z_rows_for(cfg, f, rows):
+    if f.Z is not None:
+        return f.Z[rows]
+    return synth.build_z_rows(cfg, f.info["atom_map"], rows)
+
+
+def oracle_sample_rate(cfg, f, recs, threads=0):
+    """Time the fp64 oracle (as it stands) on recs; Z rows it needs are gathered before timing."""
+    import oracle
+    d = oracle.desc_of(cfg)
+    rows, _ = oracle.neighbours(d, recs)
+    Zs, zmap = oracle.sparse_z(rows, cfg.P, lambda u: z_rows_for(cfg, f, u))
+    t0 = time.perf_counter()
+    out = oracle.query_batch(d, f.C, f.X, f.Y, Zs, recs, mean=True, zmap=zmap, threads=threads)
+    dt = time.perf_counter() - t0
+    return recs.shape[0] / dt, dt, out
+
+
+def cpu_baseline(cfg, f, bins, shard0: int, seconds: float):
+    """Oracle on a bounded sample of the same workload (first m queries of the stream), all host cores."""
+    import oracle
+    probe = synth.gen_queries(cfg, bins, shard0, shard0 + 2000)
+    r0, _, _ = oracle_sample_rate(cfg, f, probe)
+    m = int(max(2000, min(cfg.n_queries, r0 * seconds)))
+    recs = synth.gen_queries(cfg, bins, shard0, shard0 + m)
+    rate, dt, _ = oracle_sample_rate(cfg, f, recs)
+    return {"value": rate, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": f"queries [{shard0}, {shard0 + m}) of the {cfg.n_queries:.0e}-query stream ({dt:.1f} s, "
+                      f"fp64, OpenMP over queries, Z rows pre-gathered)"}
+
+
+# --------------------------------------------------------------- ref arm --
+def run_reference(args, cfg, rank, world):
+    if rank != 0:
+        return 0
+    import oracle
+    bins, f = host_inputs(cfg)
+    n_total = args.queries or cfg.n_queries
+    probe = synth.gen_queries(cfg, bins, 0, 2000)
+    r0, _, _ = oracle_sample_rate(cfg, f, probe)
+    per_step = max(2000, int(r0 * min(20.0, 150.0 / max(1, args.steps + args.warmup))))
+    per_step = min(per_step, n_total)
+    times = []
+    for s in range(args.warmup + args.steps):
+        a = (s * per_step) % max(1, n_total - per_step + 1)
+        recs = synth.gen_queries(cfg, bins, a, a + per_step)
+        rate, dt, _ = oracle_sample_rate(cfg, f, recs)
+        if s >= args.warmup:
+            times.append(dt)
+    t = float(np.mean(times))
+    value = per_step / t
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "sample_queries_per_step": per_step},
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                             "sample": f"{per_step} queries per step from the config's stream"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# --------------------------------------------------------------- our arm --
+def run_ours(args, cfg, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2109_14807_b200 import pndf
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n_total = args.queries or cfg.n_queries
+    i0, i1 = rank * n_total // world, (rank + 1) * n_total // world
+    n = i1 - i0
+
+    # ---- store (untimed): map on host, exact-rank Z built on this GPU (synth CUDA twin)
+    t_setup = time.perf_counter()
+    bins, f = host_inputs(cfg)
+    if f.Z is None:
+        Z = synth.build_z_exact_cuda(cfg, f.info["atom_map"], local_rank)
+    else:
+        Z = f.Z
+    desc = pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap)
+    store = pndf.load_factors(desc, f.C, f.X, f.Y, Z, device=local_rank)
+    del Z
+    torch.cuda.empty_cache()
+    if args.lanes:
+        store.set_lanes(args.lanes)
+
+    # ---- this rank's query shard: pinned host copy (for e2e) + resident device copy
+    h_q = torch.empty((n, 4), dtype=torch.int32, pin_memory=True)
+    synth.gen_queries(cfg, bins, i0, i1, out=h_q.numpy().view(synth.QREC).reshape(-1))
+    d_q = h_q.to(dev, non_blocking=False)
+    d_out = torch.empty(n, dtype=torch.float32, device=dev)
+    opts = {"auto": pndf.BIN_AUTO, "on": pndf.BIN_ON, "off": pndf.BIN_OFF}[args.bin]
+    setup_s = time.perf_counter() - t_setup
+
+    # ---- warm-up
+    for _ in range(args.warmup):
+        store.query_batch(d_q, d_out, opts)
+        store.sync()
+    store.reset_stats()
+    launches0 = store.stats()["kernel_launches"]
+
+    # ---- timed region: K steps, CUDA events on the launching stream, barrier + sync both sides
+    clocks = ClockSampler(bus_id_of(dev))
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        store.query_batch(d_q, d_out, opts | pndf.TIMING)
+        store.sync()
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_rank = ev0.elapsed_time(ev1) / args.steps
+    st = store.stats()
+    launches = st["kernel_launches"] - launches0
+    q_ms = st["query_ms"] / max(1, st["timed_batches"])
+    b_ms = st["bin_ms"] / max(1, st["timed_batches"])
+
+    checksum = float(d_out.double().sum().item())
+    t = torch.tensor([ms_rank, q_ms, b_ms, checksum], dtype=torch.float64, device=dev)
+    if world > 1:
+        tmax = t[:3].clone()
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+        tsum = t[3:].clone()
+        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
+        ms_step, q_ms_max, b_ms_max = tmax.tolist()
+        checksum = tsum.item()
+    else:
+        ms_step, q_ms_max, b_ms_max = ms_rank, q_ms, b_ms
+    value = n_total / (ms_step * 1e-3)
+
+    # ---- end to end through the public API with HOST buffers (H2D + kernels + D2H inside)
+    e2e = None
+    if not args.no_e2e:
+        h_out = torch.empty(n, dtype=torch.float32, pin_memory=True)
+        store.query_batch_host(h_q, h_out, opts)  # warm the host pipeline buffers
+        times = []
+        for _ in range(max(1, args.e2e_steps)):
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            store.query_batch_host(h_q, h_out, opts)
+            times.append(time.perf_counter() - t0)
+        te = torch.tensor([float(np.mean(times))], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": n_total / te.item(), "unit": UNIT, "h2d_bytes_per_step": int(h_q.numel() * 4),
+               "d2h_bytes_per_step": int(h_out.numel() * 4),
+               "bitwise_equal_to_device_path": bool(torch.equal(h_out.to(dev), d_out))}
+
+    if rank != 0:
+        store.free()
+        return 0
+
+    peaks, peak_src = measured_peaks()
+    Bq = bytes_per_query(cfg.R)
+    achieved = Bq * n / (q_ms * 1e-3) / 1e9  # GB/s of the query kernel on rank 0
+    traffic = ncu_traffic(cfg.idx)
+    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+            "kernel": "pndf::query_kernel", "kernel_ms": q_ms, "bytes_per_query": Bq,
+            "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs, copy benchmark)"
+            if peak_src == "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)",
+            "binning_ms": b_ms, "query_share_of_step": q_ms / ms_rank if ms_rank else None}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, f, bins, i0, args.cpu_seconds)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(cfg), "queries_total": n_total, "queries_per_rank": n,
+                       "parallelism": f"query-sharded x{world}, factors replicated",
+                       "binning": args.bin, "binned": bool(st["last_binned"]),
+                       "lanes_per_query": st["lanes_per_query"], "rank_padded": st["rank_padded"],
+                       "l2": "inputs larger than L2 (Zc %.1f GB, records %.1f GB vs 126 MB L2); no flush" % (
+                           st["zc_bytes"] / 1e9, n * 16 / 1e9),
+                       "setup_s": round(setup_s, 1)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk, "checksum": checksum}
+    print(json.dumps(line), flush=True)
+    store.free()
+    return 0
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg = synth.CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg, rank, world)
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+    try:
+        return run_ours(args, cfg, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

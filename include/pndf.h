@@ -1,0 +1,153 @@
+/*
+ * pndf.h -- C ABI of the B200-native batched NDF range query
+ * (Deng et al., "Constant-Cost Spatio-Angular Prefiltering of Glinty
+ * Appearance Using Tensor Decomposition", arXiv 2109.14807).
+ *
+ * P:n below is line n of the paper's LaTeX; S:n of SPEC.md.
+ *
+ * What a query computes.  The method precomputes an NDF image for every
+ * footprint centre of a mip-like pyramid -- level l has stride s0*2^l and
+ * footprint sigma_p = 1.5 s/sqrt(12) -- and compresses the stack
+ * with a rank-R CP decomposition  D-hat = sum_r C_r X_r (x) Y_r (x) Z_r  (Eq. 5,
+ * P:298-303).  A query (footprint centre u,v; footprint size S; inclusive
+ * angular rectangle [x1,x2] x [y1,y2] on the A x A projected-normal grid)
+ * returns the trilinearly interpolated (4 spatial neighbours x 2 levels,
+ * P:276) range MEAN of Eq. 6:
+ *     sum_k w_k sum_r C_r Xbar_r([x1,x2]) Ybar_r([y1,y2]) Z_r(z_k)
+ * or, with PNDF_SUM, the same without the 1/((x2-x1+1)(y2-y1+1)) factor.
+ * The 1-D segment sums come from prefix sums, "strictly, 2 memory look-ups"
+ * per factor.  Above the top level the size clamps; below
+ * the base it clamps to level 0.  DESIGN.md §2 states every reading.
+ *
+ * All calls return pndf_status (0 = OK, < 0 = error) and are thread-safe for
+ * distinct store handles.  One in-flight batch per store handle.
+ */
+#ifndef PNDF_H
+#define PNDF_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PNDF_ABI_VERSION 1u
+
+typedef enum {
+    PNDF_OK = 0,
+    PNDF_EINVAL = -1,  /* bad argument (null pointer, bad descriptor, negative or non-finite factor, bad opts) */
+    PNDF_ENOMEM = -2,  /* device or host allocation failed */
+    PNDF_ECUDA = -3,   /* a CUDA runtime call failed (pndf_last_cuda_error() names it) */
+    PNDF_EFORMAT = -4, /* ABI version mismatch */
+    PNDF_EQUERY = -5   /* sticky, device-side: >= 1 record of a batch was invalid (its result is NaN) */
+} pndf_status;
+
+/* descriptor flags */
+#define PNDF_CLAMP 0u /* neighbours clamp to the grid edge (non-tileable map) */
+#define PNDF_WRAP 1u  /* neighbours wrap modulo the level grid (tileable map) */
+
+/* pndf_query_batch opts (OR together) */
+#define PNDF_MEAN 0u      /* Eq. 6 average over the rectangle (default) */
+#define PNDF_SUM 1u       /* rectangle integral (no division by the area) */
+#define PNDF_BIN_AUTO 0u  /* bin queries by (level, tile) when the factor set exceeds L2 */
+#define PNDF_BIN_ON 2u    /* always bin */
+#define PNDF_BIN_OFF 4u   /* never bin */
+#define PNDF_TIMING 8u    /* record CUDA events around each phase (read with pndf_store_stats) */
+
+typedef struct pndf_store_s* pndf_store; /* opaque; factors immutable after load */
+
+/* Store geometry.  Level l (0 <= l < L) has stride s_l = base_stride*2^l and an
+ * n_l x n_l grid of footprint centres ((i+1/2)s_l, (j+1/2)s_l), n_l = map_size/s_l
+ * (P:274-279).  Positional index z = off_l + j*n_l + i, off_l = sum_{m<l} n_m^2;
+ * P = sum_l n_l^2 rows. */
+typedef struct {
+    uint32_t abi_version; /* = PNDF_ABI_VERSION                                  */
+    int32_t map_size;     /* N texels per side, power of two, <= 2^20            */
+    int32_t base_stride;  /* s0, power of two dividing N                         */
+    int32_t num_levels;   /* L, 2 <= L <= log2(N/s0) + 1, L <= 24                */
+    int32_t ang_res;      /* A, 1 <= A <= 256 (rect bounds are 8-bit)            */
+    int32_t rank;         /* R, 1 <= R <= 1024                                   */
+    uint32_t flags;       /* PNDF_WRAP or PNDF_CLAMP                             */
+} pndf_desc;
+
+/* One query record, 16 bytes, little-endian.
+ *   u, v  footprint centre in texels; |u|,|v| <= 2^22 (wrapped or clamped to the map)
+ *   size  footprint size S in texels (> 0); level l* = clamp(log2(S/s0), 0, L-1),
+ *         so S = s_l selects level l; sigma_p = 1.5 S / sqrt(12)
+ *   rect  x1 | x2<<8 | y1<<16 | y2<<24, inclusive bounds, x1 <= x2 < A, y1 <= y2 < A
+ * Invalid records (non-finite fields, |u|,|v| > 2^22, size <= 0, bad bounds)
+ * yield NaN and set the store's sticky error. */
+typedef struct {
+    float u, v, size;
+    uint32_t rect;
+} pndf_query;
+
+/* Build a device store from raw CP factors (Eq. 5), synchronously.
+ *   C [R] (NULL = all ones), X [A][R], Y [A][R]  -- host or device memory, fp32
+ *   Z [P][R] level-major, rows j*n_l + i         -- host or device memory, fp32
+ * Layout in HBM: Zc[P][Rp] = fl32(C_r Z_r(z)) with R padded to Rp
+ * (zero ranks, rows 16-byte aligned); PX, PY [(A+1)][hi|lo][Rp] prefix sums
+ * accumulated in fp64 and stored as an fp32 (hi, lo) pair.
+ * Every factor must be finite and >= 0 (nonnegative store), else PNDF_EINVAL.
+ * Inputs are copied: the caller may free them on return.  device = CUDA
+ * ordinal; cuda_stream = cudaStream_t used for the build (NULL = default). */
+pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float* X, const float* Y,
+                              const float* Z, int device, void* cuda_stream, pndf_store* out);
+
+/* Enqueue one batch on cuda_stream and return immediately.
+ *   d_queries [n] pndf_query, d_out [n] fp32 -- caller-owned DEVICE memory that
+ *   must stay valid until pndf_sync; results land at out[i] for query i in the
+ *   caller's order whether or not the batch is binned (bitwise identical either
+ *   way).  n == 0 is a no-op.  Argument errors return synchronously. */
+pndf_status pndf_query_batch(pndf_store s, const pndf_query* d_queries, int64_t n, float* d_out, uint32_t opts,
+                             void* cuda_stream);
+
+/* Block until the store's work on cuda_stream is done; returns and clears the
+ * sticky per-record error (PNDF_EQUERY) or a CUDA error. */
+pndf_status pndf_sync(pndf_store s, void* cuda_stream);
+
+/* End-to-end variant: HOST records in, HOST results out.  Streams the batch
+ * through the device in chunks (H2D copy, binning + query kernels, D2H copy
+ * overlapped on three internal streams) and returns when h_out is complete.
+ * Pinned (page-locked) host buffers give full PCIe bandwidth; pageable ones
+ * work but serialise the copies.  Returns the sticky error like pndf_sync. */
+pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int64_t n, float* h_out,
+                                  uint32_t opts);
+
+/* Release the store and all device memory it owns. NULL is a no-op. */
+pndf_status pndf_free(pndf_store s);
+
+const char* pndf_error_string(pndf_status status);
+const char* pndf_last_cuda_error(void); /* text of the last failing CUDA call on this thread */
+uint32_t pndf_abi_version(void);
+
+/* Introspection (tests / bench). */
+typedef struct {
+    int64_t rows;             /* P                                              */
+    int32_t rank_padded;      /* Rp                                             */
+    int32_t lanes_per_query;  /* G: lanes of a warp that share one query        */
+    int64_t zc_bytes;         /* bytes of Zc                                    */
+    int64_t prefix_bytes;     /* bytes of PX + PY                               */
+    uint64_t kernel_launches; /* kernels this store has launched so far         */
+    uint64_t timed_batches;   /* batches run with PNDF_TIMING since the last reset */
+    double query_ms;          /* summed query-kernel time of those batches      */
+    double bin_ms;            /* summed binning time of those batches           */
+    int32_t last_binned;      /* 1 if the last batch was binned                 */
+    int32_t reserved;
+} pndf_store_stats;
+pndf_status pndf_store_stats_get(pndf_store s, pndf_store_stats* out);
+pndf_status pndf_store_stats_reset(pndf_store s);
+
+/* Copy the device store image to host memory (tests): PXY = [2][(A+1)][2][Rp]
+ * fp32 (table X then Y; hi then lo), Zc rows [z0, z1) as [z1-z0][Rp] fp32.
+ * Either pointer may be NULL. */
+pndf_status pndf_store_image(pndf_store s, float* PXY, float* Zc, int64_t z0, int64_t z1);
+
+/* Tuning knob (bench / tests): lanes per query G in {1,2,4,8,16,32} with
+ * G*4 dividing Rp; 0 restores the default chosen at load. */
+pndf_status pndf_set_lanes(pndf_store s, int32_t lanes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PNDF_H */

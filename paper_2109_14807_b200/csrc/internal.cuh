@@ -1,0 +1,44 @@
+// internal.cuh -- device-side data structures shared by the pndf kernels.
+//
+// Store layout in HBM:
+//   Zc  [P][Rp]               fp32, Zc[z][r] = fl32(C_r * Z_r(z)), ranks >= R are 0,
+//                             rows 16-byte aligned (Rp % 4 == 0)
+//   PXY [2][A+1][2][Rp]       fp32, table 0 = X, 1 = Y; entry k holds the prefix
+//                             sum_{i<k} X_r(i) accumulated in fp64 and split into
+//                             hi = fl32(S), lo = fl32(S - hi)  ("1D SAT")
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "pndf.h"
+
+namespace pndf {
+
+constexpr int kMaxLevels = 24;
+constexpr int kThreads = 256;  // query-kernel block size
+
+struct QParams {
+    const float* Zc;
+    const float* PXY;
+    uint32_t* err;                 // sticky error word (bit 0: invalid record)
+    int64_t level_off[kMaxLevels]; // off_l = sum_{m<l} n_m^2
+    int32_t N;                     // map side
+    int32_t n0;                    // level-0 grid side N/s0
+    int32_t L;                     // levels
+    int32_t A;                     // angular resolution
+    int32_t Rp;                    // padded rank
+    int32_t wrap;                  // 1 = periodic neighbours
+    float inv_s0;                  // 1/s0 (power of two, exact)
+    uint32_t mean;                 // 1 = divide by the rectangle area
+};
+
+// Binning geometry: key = base[l0] + Morton(i0 >> shift, j0 >> shift) at level l0.
+struct BinGeom {
+    int32_t shift;
+    int32_t L;
+    int64_t base[kMaxLevels];
+    int64_t nbins;  // including the trailing "invalid record" bin
+};
+
+}  // namespace pndf

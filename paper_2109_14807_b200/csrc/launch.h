@@ -1,0 +1,32 @@
+// launch.h -- host-side launchers of the query and binning kernels (query.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "internal.cuh"
+
+namespace pndf {
+
+bool lanes_supported(int G, int NV);
+
+// Query kernel over n records; idx != nullptr means the records are binned
+// and idx[i] is record i's position in the caller's output.
+cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,
+                         float* out, int num_sms, cudaStream_t st);
+
+int64_t scan_blocks(int64_t nbins);
+
+// Counting sort of n records by bin key into (binned, idx). hist must hold
+// nbins entries, bsum scan_blocks(nbins) entries.
+cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, uint32_t* keys, uint32_t* hist,
+                           int64_t nbins, uint32_t* bsum, pndf_query* binned, uint32_t* idx, int num_sms,
+                           cudaStream_t st, int* launches);
+
+// Store build kernels (store.cu).
+cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float* Cdev, float* Zc_dst, int Rp,
+                             uint32_t* bad, cudaStream_t st);
+cudaError_t launch_prefix(const float* Xdev, const float* Ydev, int A, int R, int Rp, float* PXY, uint32_t* bad,
+                          cudaStream_t st);
+
+}  // namespace pndf

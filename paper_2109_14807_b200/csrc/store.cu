@@ -1,0 +1,518 @@
+// store.cu -- the C ABI of libpndf: store build, batch
+// enqueue (a1-a6 via query.cu), sync/errors (a7) and the end-to-end host
+// pipeline.  Declarations and argument contracts: include/pndf.h.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <mutex>
+#include <new>
+
+#include "internal.cuh"
+#include "launch.h"
+
+using namespace pndf;
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+
+pndf_status cuda_fail(cudaError_t e, const char* what) {
+    snprintf(g_cuda_err, sizeof(g_cuda_err), "%s: %s", what, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? PNDF_ENOMEM : PNDF_ECUDA;
+}
+
+#define CK(call)                                                   \
+    do {                                                           \
+        cudaError_t _e = (call);                                   \
+        if (_e != cudaSuccess) return cuda_fail(_e, #call);        \
+    } while (0)
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_pow2(int64_t x) { return x > 0 && (x & (x - 1)) == 0; }
+int ilog2(int64_t x) {
+    int l = 0;
+    while ((int64_t(1) << (l + 1)) <= x) ++l;
+    return l;
+}
+
+// Binning scratch for one in-flight batch.
+struct Scratch {
+    uint32_t* keys = nullptr;
+    uint32_t* idx = nullptr;
+    pndf_query* binned = nullptr;
+    uint32_t* hist = nullptr;
+    uint32_t* bsum = nullptr;
+    int64_t cap = 0;
+    void release() {
+        cudaFree(keys);
+        cudaFree(idx);
+        cudaFree(binned);
+        cudaFree(hist);
+        cudaFree(bsum);
+        *this = Scratch();
+    }
+};
+
+// One stage of the host pipeline.
+struct Slot {
+    Scratch scratch;
+    pndf_query* d_rec = nullptr;
+    float* d_out = nullptr;
+    int64_t cap = 0;
+    cudaStream_t st = nullptr;
+    void release() {
+        scratch.release();
+        cudaFree(d_rec);
+        cudaFree(d_out);
+        if (st) cudaStreamDestroy(st);
+        *this = Slot();
+    }
+};
+
+constexpr int kSlots = 3;
+
+}  // namespace
+
+struct pndf_store_s {
+    pndf_desc d;
+    int device = 0;
+    int num_sms = 148;
+    int64_t l2_bytes = 0;
+    int64_t P = 0;
+    int Rp = 0, G0 = 0, NV0 = 0, G = 0, NV = 0;
+    int64_t nbins = 0;  // P + 1 (last = invalid records); 0 if binning infeasible
+    QParams qp{};
+    float* Zc = nullptr;
+    float* PXY = nullptr;
+    uint32_t* err = nullptr;
+    Scratch main;
+    Slot slots[kSlots];
+    cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+    bool timing_pending = false;
+    bool pending_binned = false;
+    pndf_store_stats stats{};
+    std::mutex mu;
+};
+
+namespace {
+
+pndf_status validate_desc(const pndf_desc* d) {
+    if (!d) return PNDF_EINVAL;
+    if (d->abi_version != PNDF_ABI_VERSION) return PNDF_EFORMAT;
+    if (!is_pow2(d->map_size) || d->map_size > (1 << 20)) return PNDF_EINVAL;
+    if (!is_pow2(d->base_stride) || d->base_stride > d->map_size) return PNDF_EINVAL;
+    const int maxL = ilog2(d->map_size / d->base_stride) + 1;
+    if (d->num_levels < 2 || d->num_levels > maxL || d->num_levels > kMaxLevels) return PNDF_EINVAL;
+    if (d->ang_res < 1 || d->ang_res > 256) return PNDF_EINVAL;
+    if (d->rank < 1 || d->rank > 1024) return PNDF_EINVAL;
+    if (d->flags != PNDF_WRAP && d->flags != PNDF_CLAMP) return PNDF_EINVAL;
+    return PNDF_OK;
+}
+
+// Default lane split: G = lanes sharing a query, NV float4 chunks per lane.
+void choose_lanes(int R, int* G, int* NV) {
+    const int q4 = (R + 3) / 4;
+    int g = 1;
+    while (g < q4 && g < 32) g <<= 1;
+    int nv = (q4 + g - 1) / g;
+    if (nv > 4) nv = 8;
+    *G = g;
+    *NV = nv;
+}
+
+pndf_status ensure_scratch(Scratch& s, int64_t n, int64_t nbins, cudaStream_t st) {
+    if (s.cap >= n && s.hist) return PNDF_OK;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (st && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
+        return PNDF_EINVAL;  // no allocation while a CUDA graph is being captured
+    s.release();
+    CK(cudaMalloc(&s.keys, sizeof(uint32_t) * n));
+    CK(cudaMalloc(&s.idx, sizeof(uint32_t) * n));
+    CK(cudaMalloc(&s.binned, sizeof(pndf_query) * n));
+    CK(cudaMalloc(&s.hist, sizeof(uint32_t) * nbins));
+    CK(cudaMalloc(&s.bsum, sizeof(uint32_t) * scan_blocks(nbins)));
+    s.cap = n;
+    return PNDF_OK;
+}
+
+bool want_bins(const pndf_store_s* s, int64_t n, uint32_t opts) {
+    if (s->nbins == 0 || (opts & PNDF_BIN_OFF)) return false;
+    if (opts & PNDF_BIN_ON) return true;
+    // AUTO: the factor set does not stay in L2, and the batch is large enough
+    // for rows to be shared between queries.
+    return (int64_t)s->stats.zc_bytes > s->l2_bytes / 2 && n >= (int64_t(1) << 16);
+}
+
+// Enqueue one batch (device records) on st using scratch sc.
+pndf_status enqueue(pndf_store_s* s, Scratch& sc, const pndf_query* q, int64_t n, float* out, uint32_t opts,
+                    cudaStream_t st, bool timing) {
+    QParams p = s->qp;
+    p.mean = (opts & PNDF_SUM) ? 0u : 1u;
+    const bool binned = want_bins(s, n, opts);
+    if ((opts & PNDF_BIN_ON) && s->nbins == 0) return PNDF_EINVAL;
+    int launches = 0;
+    if (timing) CK(cudaEventRecord(s->ev[0], st));
+    // sub-batches keep indices in uint32 when binning
+    const int64_t step = binned ? (int64_t(1) << 31) : n;
+    if (binned) {
+        pndf_status r = ensure_scratch(sc, std::min(n, step), s->nbins, st);
+        if (r != PNDF_OK) return r;
+    }
+    bool first = true;
+    for (int64_t a = 0; a < n; a += step) {
+        const int64_t m = std::min(step, n - a);
+        if (binned) {
+            CK(launch_binning(p, q + a, m, sc.keys, sc.hist, s->nbins, sc.bsum, sc.binned, sc.idx, s->num_sms, st,
+                              &launches));
+            if (timing && first) CK(cudaEventRecord(s->ev[1], st));
+            CK(launch_query(p, s->G, s->NV, sc.binned, sc.idx, m, out + a, s->num_sms, st));
+        } else {
+            if (timing && first) CK(cudaEventRecord(s->ev[1], st));
+            CK(launch_query(p, s->G, s->NV, q + a, nullptr, m, out + a, s->num_sms, st));
+        }
+        launches += 1;
+        first = false;
+    }
+    if (timing) CK(cudaEventRecord(s->ev[2], st));
+    s->stats.kernel_launches += (uint64_t)launches;
+    s->stats.last_binned = binned ? 1 : 0;
+    return PNDF_OK;
+}
+
+pndf_status read_sticky(pndf_store_s* s) {
+    uint32_t e = 0;
+    CK(cudaMemcpy(&e, s->err, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    if (e) {
+        CK(cudaMemset(s->err, 0, sizeof(uint32_t)));
+        return PNDF_EQUERY;
+    }
+    return PNDF_OK;
+}
+
+void destroy(pndf_store_s* s) {
+    if (!s) return;
+    DeviceGuard g(s->device);
+    cudaDeviceSynchronize();
+    cudaFree(s->Zc);
+    cudaFree(s->PXY);
+    cudaFree(s->err);
+    s->main.release();
+    for (auto& sl : s->slots) sl.release();
+    for (auto& e : s->ev)
+        if (e) cudaEventDestroy(e);
+    delete s;
+}
+
+}  // namespace
+
+// ----------------------------------------------------------------- API --
+extern "C" {
+
+uint32_t pndf_abi_version(void) { return PNDF_ABI_VERSION; }
+
+const char* pndf_error_string(pndf_status st) {
+    switch (st) {
+        case PNDF_OK: return "ok";
+        case PNDF_EINVAL: return "invalid argument";
+        case PNDF_ENOMEM: return "out of memory";
+        case PNDF_ECUDA: return "CUDA error";
+        case PNDF_EFORMAT: return "ABI version mismatch";
+        case PNDF_EQUERY: return "invalid query record(s) in batch (results NaN)";
+        default: return "unknown pndf status";
+    }
+}
+
+const char* pndf_last_cuda_error(void) { return g_cuda_err; }
+
+pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float* X, const float* Y, const float* Z,
+                              int device, void* cuda_stream, pndf_store* out) {
+    if (!out || !X || !Y || !Z) return PNDF_EINVAL;
+    *out = nullptr;
+    pndf_status r = validate_desc(desc);
+    if (r != PNDF_OK) return r;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return PNDF_EINVAL;
+    DeviceGuard guard(device);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+
+    pndf_store_s* s = new (std::nothrow) pndf_store_s();
+    if (!s) return PNDF_ENOMEM;
+    s->d = *desc;
+    s->device = device;
+    const int N = desc->map_size, s0 = desc->base_stride, L = desc->num_levels, A = desc->ang_res,
+              R = desc->rank;
+    const int64_t n0 = N / s0;
+    for (int l = 0; l < L; ++l) s->P += (n0 >> l) * (n0 >> l);
+    choose_lanes(R, &s->G0, &s->NV0);
+    s->G = s->G0;
+    s->NV = s->NV0;
+    s->Rp = 4 * s->G0 * s->NV0;
+    const int Rp = s->Rp;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    s->num_sms = v > 0 ? v : 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device);
+    s->l2_bytes = v;
+    // binning keys are uint32 level offsets + 16-bit Morton coordinates
+    s->nbins = (s->P + 1 < (int64_t)0xffffffffLL && n0 <= 65536) ? s->P + 1 : 0;
+
+    auto fail = [&](pndf_status e) {
+        destroy(s);
+        return e;
+    };
+    const size_t zc_bytes = sizeof(float) * (size_t)s->P * Rp;
+    const size_t pxy_bytes = sizeof(float) * (size_t)2 * (A + 1) * 2 * Rp;
+    cudaError_t e;
+    if ((e = cudaMalloc(&s->Zc, zc_bytes)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(Zc)"));
+    if ((e = cudaMalloc(&s->PXY, pxy_bytes)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(PXY)"));
+    if ((e = cudaMalloc(&s->err, 2 * sizeof(uint32_t))) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(err)"));
+    uint32_t* bad = s->err + 1;
+    cudaMemsetAsync(s->err, 0, 2 * sizeof(uint32_t), st);
+    for (auto& ev : s->ev)
+        if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
+
+    // small factors: C (or ones), X, Y -> device
+    float *dC = nullptr, *dXY = nullptr;
+    if ((e = cudaMalloc(&dC, sizeof(float) * Rp)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(C)"));
+    if ((e = cudaMalloc(&dXY, sizeof(float) * 2 * (size_t)A * R)) != cudaSuccess) {
+        cudaFree(dC);
+        return fail(cuda_fail(e, "cudaMalloc(XY)"));
+    }
+    auto free_small = [&]() {
+        cudaFree(dC);
+        cudaFree(dXY);
+    };
+    {
+        float* hC = new float[Rp];
+        for (int i = 0; i < Rp; ++i) hC[i] = i < R ? 1.0f : 0.0f;
+        e = cudaMemcpy(dC, hC, sizeof(float) * Rp, cudaMemcpyHostToDevice);
+        delete[] hC;
+        if (e == cudaSuccess && C) e = cudaMemcpy(dC, C, sizeof(float) * R, cudaMemcpyDefault);
+        if (e == cudaSuccess) e = cudaMemcpy(dXY, X, sizeof(float) * (size_t)A * R, cudaMemcpyDefault);
+        if (e == cudaSuccess) e = cudaMemcpy(dXY + (size_t)A * R, Y, sizeof(float) * (size_t)A * R, cudaMemcpyDefault);
+        if (e != cudaSuccess) {
+            free_small();
+            return fail(cuda_fail(e, "cudaMemcpy(C/X/Y)"));
+        }
+    }
+    // C is validated by folding it as a one-row "Z" against ones
+    if ((e = launch_prefix(dXY, dXY + (size_t)A * R, A, R, Rp, s->PXY, bad, st)) != cudaSuccess) {
+        free_small();
+        return fail(cuda_fail(e, "prefix kernel"));
+    }
+    if ((e = launch_fold_rows(dC, 1, R, nullptr, dC, R, bad, st)) != cudaSuccess) {
+        free_small();
+        return fail(cuda_fail(e, "validate C"));
+    }
+    s->stats.kernel_launches += 2;
+
+    // positional factors: Zc = fl32(C_r Z_r(z)), padded to Rp
+    cudaPointerAttributes pa;
+    const bool z_dev = cudaPointerGetAttributes(&pa, Z) == cudaSuccess &&
+                       (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
+    cudaGetLastError();
+    if (z_dev) {
+        if ((e = launch_fold_rows(Z, s->P, R, dC, s->Zc, Rp, bad, st)) != cudaSuccess) {
+            free_small();
+            return fail(cuda_fail(e, "fold kernel"));
+        }
+        s->stats.kernel_launches += 1;
+    } else {
+        // host Z: stream through a device staging buffer (or straight into Zc when Rp == R)
+        const int64_t chunk = std::max<int64_t>(1, (int64_t(64) << 20) / R);  // 256 MB of rows
+        float* stage = nullptr;
+        if (Rp != R && (e = cudaMalloc(&stage, sizeof(float) * (size_t)std::min(chunk, s->P) * R)) != cudaSuccess) {
+            free_small();
+            return fail(cuda_fail(e, "cudaMalloc(stage)"));
+        }
+        for (int64_t a = 0; a < s->P && e == cudaSuccess; a += chunk) {
+            const int64_t m = std::min(chunk, s->P - a);
+            float* dst = stage ? stage : s->Zc + (size_t)a * Rp;
+            e = cudaMemcpyAsync(dst, Z + (size_t)a * R, sizeof(float) * (size_t)m * R, cudaMemcpyDefault, st);
+            if (e == cudaSuccess) e = launch_fold_rows(dst, m, R, dC, s->Zc + (size_t)a * Rp, Rp, bad, st);
+            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+            s->stats.kernel_launches += 1;
+        }
+        cudaFree(stage);
+        if (e != cudaSuccess) {
+            free_small();
+            return fail(cuda_fail(e, "Z upload"));
+        }
+    }
+    uint32_t hbad = 0;
+    e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+    free_small();
+    if (e != cudaSuccess) return fail(cuda_fail(e, "store build"));
+    if (hbad) return fail(PNDF_EINVAL);  // negative or non-finite factor
+
+    QParams& p = s->qp;
+    p.Zc = s->Zc;
+    p.PXY = s->PXY;
+    p.err = s->err;
+    for (int l = 0; l < kMaxLevels; ++l) p.level_off[l] = 0;
+    int64_t off = 0;
+    for (int l = 0; l < L; ++l) {
+        p.level_off[l] = off;
+        off += (n0 >> l) * (n0 >> l);
+    }
+    p.N = N;
+    p.n0 = (int32_t)n0;
+    p.L = L;
+    p.A = A;
+    p.Rp = Rp;
+    p.wrap = desc->flags == PNDF_WRAP ? 1 : 0;
+    p.inv_s0 = 1.0f / (float)s0;
+    p.mean = 1;
+    s->stats.rows = s->P;
+    s->stats.rank_padded = Rp;
+    s->stats.lanes_per_query = s->G;
+    s->stats.zc_bytes = (int64_t)zc_bytes;
+    s->stats.prefix_bytes = (int64_t)pxy_bytes;
+    *out = s;
+    return PNDF_OK;
+}
+
+pndf_status pndf_query_batch(pndf_store s, const pndf_query* d_queries, int64_t n, float* d_out, uint32_t opts,
+                             void* cuda_stream) {
+    if (!s || n < 0 || (n > 0 && (!d_queries || !d_out))) return PNDF_EINVAL;
+    if (opts & ~(PNDF_SUM | PNDF_BIN_ON | PNDF_BIN_OFF | PNDF_TIMING)) return PNDF_EINVAL;
+    if ((opts & PNDF_BIN_ON) && (opts & PNDF_BIN_OFF)) return PNDF_EINVAL;
+    if (n == 0) return PNDF_OK;
+    if ((uintptr_t)d_queries % 16 != 0 || (uintptr_t)d_out % 4 != 0) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    const bool timing = (opts & PNDF_TIMING) != 0;
+    pndf_status r = enqueue(s, s->main, d_queries, n, d_out, opts, (cudaStream_t)cuda_stream, timing);
+    if (r == PNDF_OK) {
+        s->timing_pending = timing;
+        s->pending_binned = s->stats.last_binned != 0;
+    }
+    return r;
+}
+
+pndf_status pndf_sync(pndf_store s, void* cuda_stream) {
+    if (!s) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    CK(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+    if (s->timing_pending) {
+        float t01 = 0.f, t12 = 0.f;
+        CK(cudaEventElapsedTime(&t01, s->ev[0], s->ev[1]));
+        CK(cudaEventElapsedTime(&t12, s->ev[1], s->ev[2]));
+        s->stats.bin_ms += t01;
+        s->stats.query_ms += t12;
+        s->stats.timed_batches += 1;
+        s->timing_pending = false;
+    }
+    return read_sticky(s);
+}
+
+pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int64_t n, float* h_out,
+                                  uint32_t opts) {
+    if (!s || n < 0 || (n > 0 && (!h_queries || !h_out))) return PNDF_EINVAL;
+    if (opts & ~(PNDF_SUM | PNDF_BIN_ON | PNDF_BIN_OFF)) return PNDF_EINVAL;
+    if ((opts & PNDF_BIN_ON) && (opts & PNDF_BIN_OFF)) return PNDF_EINVAL;
+    if (n == 0) return PNDF_OK;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    // chunk so that >= 8 chunks overlap when the batch allows, 1M..64M records each
+    int64_t chunk = std::max<int64_t>(int64_t(1) << 20, std::min<int64_t>(int64_t(1) << 26, (n + 7) / 8));
+    chunk = std::min(chunk, n);
+    const bool binned = want_bins(s, chunk, opts);
+    for (auto& sl : s->slots) {
+        if (!sl.st) CK(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
+        if (sl.cap < chunk) {
+            cudaFree(sl.d_rec);
+            cudaFree(sl.d_out);
+            sl.d_rec = nullptr;
+            sl.d_out = nullptr;
+            sl.cap = 0;
+            CK(cudaMalloc(&sl.d_rec, sizeof(pndf_query) * chunk));
+            CK(cudaMalloc(&sl.d_out, sizeof(float) * chunk));
+            sl.cap = chunk;
+        }
+        if (binned) {
+            pndf_status r = ensure_scratch(sl.scratch, chunk, s->nbins, sl.st);
+            if (r != PNDF_OK) return r;
+        }
+    }
+    int64_t c = 0;
+    for (int64_t a = 0; a < n; a += chunk, ++c) {
+        Slot& sl = s->slots[c % kSlots];
+        const int64_t m = std::min(chunk, n - a);
+        CK(cudaMemcpyAsync(sl.d_rec, h_queries + a, sizeof(pndf_query) * m, cudaMemcpyHostToDevice, sl.st));
+        pndf_status r = enqueue(s, sl.scratch, sl.d_rec, m, sl.d_out, opts, sl.st, false);
+        if (r != PNDF_OK) return r;
+        CK(cudaMemcpyAsync(h_out + a, sl.d_out, sizeof(float) * m, cudaMemcpyDeviceToHost, sl.st));
+    }
+    for (auto& sl : s->slots) CK(cudaStreamSynchronize(sl.st));
+    return read_sticky(s);
+}
+
+pndf_status pndf_free(pndf_store s) {
+    destroy(s);
+    return PNDF_OK;
+}
+
+pndf_status pndf_store_stats_get(pndf_store s, pndf_store_stats* out) {
+    if (!s || !out) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->stats.lanes_per_query = s->G;
+    *out = s->stats;
+    return PNDF_OK;
+}
+
+pndf_status pndf_store_stats_reset(pndf_store s) {
+    if (!s) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    s->stats.timed_batches = 0;
+    s->stats.query_ms = 0.0;
+    s->stats.bin_ms = 0.0;
+    return PNDF_OK;
+}
+
+pndf_status pndf_store_image(pndf_store s, float* PXY, float* Zc, int64_t z0, int64_t z1) {
+    if (!s) return PNDF_EINVAL;
+    if (Zc && (z0 < 0 || z1 < z0 || z1 > s->P)) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    if (PXY) CK(cudaMemcpy(PXY, s->PXY, (size_t)s->stats.prefix_bytes, cudaMemcpyDeviceToHost));
+    if (Zc && z1 > z0)
+        CK(cudaMemcpy(Zc, s->Zc + (size_t)z0 * s->Rp, sizeof(float) * (size_t)(z1 - z0) * s->Rp,
+                      cudaMemcpyDeviceToHost));
+    return PNDF_OK;
+}
+
+pndf_status pndf_set_lanes(pndf_store s, int32_t lanes) {
+    if (!s) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    if (lanes == 0) {
+        s->G = s->G0;
+        s->NV = s->NV0;
+        return PNDF_OK;
+    }
+    if (lanes < 1 || lanes > 32 || (lanes & (lanes - 1)) || s->Rp % (4 * lanes)) return PNDF_EINVAL;
+    const int nv = s->Rp / (4 * lanes);
+    if (!lanes_supported(lanes, nv)) return PNDF_EINVAL;
+    s->G = lanes;
+    s->NV = nv;
+    return PNDF_OK;
+}
+
+}  // extern "C"

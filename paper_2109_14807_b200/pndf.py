@@ -1,0 +1,215 @@
+"""Thin ctypes binding of libpndf (include/pndf.h): argument marshalling only.
+
+Every step of the query runs in the CUDA kernels of csrc/; nothing here
+computes.  Names follow the C ABI: ``load_factors`` -> ``pndf_load_factors``,
+``Store.query_batch`` -> ``pndf_query_batch``, ``Store.sync`` -> ``pndf_sync``,
+``Store.query_batch_host`` -> ``pndf_query_batch_host``.  PyTorch (optional)
+supplies device memory and streams; numpy arrays are accepted for host data.
+If the shared library is missing this module raises -- there is no fallback.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libpndf.so")
+
+ABI_VERSION = 1
+OK, EINVAL, ENOMEM, ECUDA, EFORMAT, EQUERY = 0, -1, -2, -3, -4, -5
+CLAMP, WRAP = 0, 1
+MEAN, SUM, BIN_AUTO, BIN_ON, BIN_OFF, TIMING = 0, 1, 0, 2, 4, 8
+
+QUERY_DTYPE = np.dtype([("u", "<f4"), ("v", "<f4"), ("size", "<f4"), ("rect", "<u4")])
+
+
+class PndfError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        self.status = status
+        msg = f"{what}: {error_string(status)} ({status})"
+        if status == ECUDA or status == ENOMEM:
+            msg += f" [{last_cuda_error()}]"
+        super().__init__(msg)
+
+
+class Desc(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_uint32), ("map_size", ctypes.c_int32), ("base_stride", ctypes.c_int32),
+                ("num_levels", ctypes.c_int32), ("ang_res", ctypes.c_int32), ("rank", ctypes.c_int32),
+                ("flags", ctypes.c_uint32)]
+
+
+class StoreStats(ctypes.Structure):
+    _fields_ = [("rows", ctypes.c_int64), ("rank_padded", ctypes.c_int32), ("lanes_per_query", ctypes.c_int32),
+                ("zc_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
+                ("kernel_launches", ctypes.c_uint64), ("timed_batches", ctypes.c_uint64),
+                ("query_ms", ctypes.c_double), ("bin_ms", ctypes.c_double), ("last_binned", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+
+
+EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sync", "pndf_query_batch_host", "pndf_free",
+           "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
+           "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes")
+
+_lib = None
+
+
+def lib():
+    """Load libpndf.so (raises if it has not been built -- no CPU fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_2109_14807_b200.build` "
+                               "(the CUDA extension is required; there is no fallback path)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i32, i64, u32 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32
+        L.pndf_load_factors.restype = i32
+        L.pndf_load_factors.argtypes = [ctypes.POINTER(Desc), P, P, P, P, ctypes.c_int, P, ctypes.POINTER(P)]
+        L.pndf_query_batch.restype = i32
+        L.pndf_query_batch.argtypes = [P, P, i64, P, u32, P]
+        L.pndf_sync.restype = i32
+        L.pndf_sync.argtypes = [P, P]
+        L.pndf_query_batch_host.restype = i32
+        L.pndf_query_batch_host.argtypes = [P, P, i64, P, u32]
+        L.pndf_free.restype = i32
+        L.pndf_free.argtypes = [P]
+        L.pndf_error_string.restype = ctypes.c_char_p
+        L.pndf_error_string.argtypes = [i32]
+        L.pndf_last_cuda_error.restype = ctypes.c_char_p
+        L.pndf_abi_version.restype = u32
+        L.pndf_store_stats_get.restype = i32
+        L.pndf_store_stats_get.argtypes = [P, ctypes.POINTER(StoreStats)]
+        L.pndf_store_stats_reset.restype = i32
+        L.pndf_store_stats_reset.argtypes = [P]
+        L.pndf_store_image.restype = i32
+        L.pndf_store_image.argtypes = [P, P, P, i64, i64]
+        L.pndf_set_lanes.restype = i32
+        L.pndf_set_lanes.argtypes = [P, i32]
+        _lib = L
+    return _lib
+
+
+def error_string(status: int) -> str:
+    return lib().pndf_error_string(status).decode()
+
+
+def last_cuda_error() -> str:
+    return lib().pndf_last_cuda_error().decode()
+
+
+def _check(status: int, what: str):
+    if status != OK:
+        raise PndfError(status, what)
+
+
+def _ptr(x):
+    """Raw address of a numpy array or torch tensor (host or device); None -> NULL."""
+    if x is None:
+        return None
+    if isinstance(x, np.ndarray):
+        assert x.flags["C_CONTIGUOUS"], "arrays must be C-contiguous"
+        return ctypes.c_void_p(x.ctypes.data)
+    if hasattr(x, "data_ptr"):
+        assert x.is_contiguous(), "tensors must be contiguous"
+        return ctypes.c_void_p(x.data_ptr())
+    if isinstance(x, int):
+        return ctypes.c_void_p(x)
+    raise TypeError(type(x))
+
+
+def _stream(stream):
+    if stream is None:
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+        except ImportError:
+            pass
+        return None
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def make_desc(N: int, s0: int, L: int, A: int, R: int, wrap: bool = True) -> Desc:
+    return Desc(abi_version=ABI_VERSION, map_size=N, base_stride=s0, num_levels=L, ang_res=A, rank=R,
+                flags=WRAP if wrap else CLAMP)
+
+
+class Store:
+    """A device factor store (opaque pndf_store handle)."""
+
+    def __init__(self, handle: ctypes.c_void_p, desc: Desc):
+        self._h = handle
+        self.desc = desc
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("store freed")
+        return self._h
+
+    def query_batch(self, queries, out, opts: int = 0, stream=None, n: int | None = None):
+        """Enqueue pndf_query_batch on ``stream``: queries = device tensor of 16-byte records
+        (e.g. int32 [n, 4]), out = device float32 [n]."""
+        n = out.shape[0] if n is None else n
+        _check(lib().pndf_query_batch(self.handle, _ptr(queries), n, _ptr(out), opts, _stream(stream)),
+               "pndf_query_batch")
+
+    def sync(self, stream=None, raise_on_query_error: bool = True) -> int:
+        st = lib().pndf_sync(self.handle, _stream(stream))
+        if st == EQUERY and not raise_on_query_error:
+            return st
+        _check(st, "pndf_sync")
+        return st
+
+    def query_batch_host(self, h_queries, h_out, opts: int = 0, raise_on_query_error: bool = True) -> int:
+        n = h_out.shape[0]
+        st = lib().pndf_query_batch_host(self.handle, _ptr(h_queries), n, _ptr(h_out), opts)
+        if st == EQUERY and not raise_on_query_error:
+            return st
+        _check(st, "pndf_query_batch_host")
+        return st
+
+    def stats(self) -> dict:
+        s = StoreStats()
+        _check(lib().pndf_store_stats_get(self.handle, ctypes.byref(s)), "pndf_store_stats_get")
+        return s.as_dict()
+
+    def reset_stats(self):
+        _check(lib().pndf_store_stats_reset(self.handle), "pndf_store_stats_reset")
+
+    def image(self, z0: int = 0, z1: int | None = None, prefix: bool = True):
+        st = self.stats()
+        Rp, A = st["rank_padded"], self.desc.ang_res
+        z1 = st["rows"] if z1 is None else z1
+        pxy = np.empty((2, A + 1, 2, Rp), np.float32) if prefix else None
+        zc = np.empty((z1 - z0, Rp), np.float32)
+        _check(lib().pndf_store_image(self.handle, _ptr(pxy), _ptr(zc), z0, z1), "pndf_store_image")
+        return pxy, zc
+
+    def set_lanes(self, lanes: int):
+        _check(lib().pndf_set_lanes(self.handle, lanes), "pndf_set_lanes")
+
+    def free(self):
+        if self._h is not None:
+            lib().pndf_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
+def load_factors(desc: Desc, C, X, Y, Z, device: int = 0, stream=None) -> Store:
+    """pndf_load_factors: raw fp32 factors (host numpy or device tensors) -> device store."""
+    h = ctypes.c_void_p()
+    _check(lib().pndf_load_factors(ctypes.byref(desc), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), device, _stream(stream),
+                                   ctypes.byref(h)), "pndf_load_factors")
+    return Store(h, desc)

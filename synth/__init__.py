@@ -70,6 +70,7 @@ def lib():
         L.synth_num_rows.restype = i64
         L.synth_num_rows.argtypes = [i32, i32, i32]
         L.synth_build_z_exact.argtypes = [i32, P, i32, i32, i32, i64, i64, P]
+        L.synth_build_z_rows.argtypes = [i32, P, i32, i32, i32, P, i64, P]
         L.synth_hist_tensor.argtypes = [i32, P, i32, i32, i32, P]
         L.synth_atom_profiles.argtypes = [i32, i32, P, f64, P, P]
         L.synth_gen_queries.argtypes = [ctypes.POINTER(_QDist), u64, i64, i64, P, P]
@@ -203,6 +204,70 @@ def build_z_exact(cfg: Config, atom_map: np.ndarray, z0: int = 0, z1: int | None
     z1 = cfg.P if z1 is None else z1
     Z = np.empty((z1 - z0, cfg.R), np.float32)
     lib().synth_build_z_exact(cfg.N, _p(atom_map), cfg.R, cfg.s0, cfg.L, z0, z1, _p(Z))
+    return Z
+
+
+def build_z_rows(cfg: Config, atom_map: np.ndarray, rows: np.ndarray) -> np.ndarray:
+    """Rows `rows` of the exact-rank Z (same bits as build_z_exact)."""
+    rows = np.ascontiguousarray(rows, np.int64)
+    out = np.empty((rows.shape[0], cfg.R), np.float32)
+    lib().synth_build_z_rows(cfg.N, _p(atom_map), cfg.R, cfg.s0, cfg.L, _p(rows), rows.shape[0], _p(out))
+    return out
+
+
+_CUDA_SRC = os.path.join(_HERE, "csrc", "synth_cuda.cu")
+_CUDA_LIB = os.path.join(_HERE, "_libsynth_cuda.so")
+_cuda_lib = None
+
+
+def build_cuda_lib(force: bool = False) -> str:
+    """nvcc -> _libsynth_cuda.so (the GPU twin of the exact-rank Z builder)."""
+    if force or not os.path.exists(_CUDA_LIB) or os.path.getmtime(_CUDA_LIB) < os.path.getmtime(_CUDA_SRC):
+        tmp = _CUDA_LIB + f".{os.getpid()}.tmp"
+        subprocess.check_call(["nvcc", "-shared", "-Xcompiler", "-fPIC", "-gencode", "arch=compute_100a,code=sm_100a",
+                               "-O3", "-lineinfo", _CUDA_SRC, "-o", tmp])
+        os.replace(tmp, _CUDA_LIB)
+    return _CUDA_LIB
+
+
+def build_z_exact_cuda(cfg: Config, atom_map: np.ndarray, device: int = 0):
+    """Exact-rank Z built on the GPU (bit-identical to build_z_exact): torch float32 [P, R] on cuda:device."""
+    import torch
+    global _cuda_lib
+    if _cuda_lib is None:
+        if not os.path.exists(_CUDA_LIB):
+            build_cuda_lib()
+        _cuda_lib = ctypes.CDLL(_CUDA_LIB)
+        P_ = ctypes.c_void_p
+        _cuda_lib.synth_cuda_build_z_exact.restype = ctypes.c_int
+        _cuda_lib.synth_cuda_build_z_exact.argtypes = [ctypes.c_int, P_, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                                       P_, P_, P_, P_, P_, P_, P_]
+    dev = torch.device("cuda", device)
+    tabs, offs, lens, qmins, tots = [], [], [], [], []
+    o = 0
+    for l in range(cfg.L):
+        qmin, w = footprint_table(cfg.s0 << l, cfg.N)
+        tabs.append(w)
+        offs.append(o)
+        lens.append(w.shape[0])
+        qmins.append(qmin)
+        sw = int(w.astype(np.uint64).sum())
+        tots.append(float(sw) * float(sw))
+        o += w.shape[0]
+    tab_dev = torch.from_numpy(np.concatenate(tabs).view(np.int32)).to(dev)
+    am_dev = torch.from_numpy(atom_map.view(np.int16)).to(dev)
+    Z = torch.empty((cfg.P, cfg.R), dtype=torch.float32, device=dev)
+    offs = np.array(offs, np.int64); lens = np.array(lens, np.int32)
+    qmins = np.array(qmins, np.int32); tots = np.array(tots, np.float64)
+    with torch.cuda.device(dev):
+        st = torch.cuda.current_stream(dev)
+        rc = _cuda_lib.synth_cuda_build_z_exact(cfg.N, ctypes.c_void_p(am_dev.data_ptr()), cfg.R, cfg.s0, cfg.L,
+                                                ctypes.c_void_p(tab_dev.data_ptr()), _p(offs), _p(lens), _p(qmins),
+                                                _p(tots), ctypes.c_void_p(Z.data_ptr()),
+                                                ctypes.c_void_p(st.cuda_stream))
+        if rc != 0:
+            raise RuntimeError(f"synth_cuda_build_z_exact failed: cudaError {rc}")
+        st.synchronize()
     return Z
 
 

@@ -304,6 +304,42 @@ EXPORT void synth_build_z_exact(int32_t N, const uint16_t* atom_map, int32_t R, 
     free(w);
 }
 
+/* Same values as synth_build_z_exact for an arbitrary list of rows (the rows
+ * a sampled parity / baseline set touches); out[k][R] for rows[k]. */
+EXPORT void synth_build_z_rows(int32_t N, const uint16_t* atom_map, int32_t R, int32_t s0, int32_t L,
+                               const int64_t* rows, int64_t nrows, float* out) {
+    int64_t offs[64];
+    int64_t off = 0;
+    for (int32_t l = 0; l < L; ++l) { offs[l] = off; off += level_rows(N, s0, l); }
+    offs[L] = off;
+    uint32_t* tabs = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)N * L);
+    int32_t qmins[64], wfs[64];
+    double tots[64];
+    for (int32_t l = 0; l < L; ++l) {
+        wfs[l] = synth_footprint_table(s0 << l, N, &qmins[l], tabs + (size_t)l * N);
+        uint64_t sw = 0;
+        for (int p = 0; p < wfs[l]; ++p) sw += tabs[(size_t)l * N + p];
+        tots[l] = (double)sw * (double)sw;
+    }
+#pragma omp parallel
+    {
+        uint64_t* acc = (uint64_t*)malloc(sizeof(uint64_t) * R);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t k = 0; k < nrows; ++k) {
+            int64_t z = rows[k];
+            int32_t l = 0;
+            while (l + 1 < L && z >= offs[l + 1]) ++l;
+            int32_t s = s0 << l, n = N / s;
+            int64_t c = z - offs[l];
+            memset(acc, 0, sizeof(uint64_t) * R);
+            footprint_accumulate(N, atom_map, s, qmins[l], wfs[l], tabs + (size_t)l * N, c % n, c / n, acc);
+            for (int r = 0; r < R; ++r) out[k * R + r] = (float)((double)acc[r] / tots[l]);
+        }
+        free(acc);
+    }
+    free(tabs);
+}
+
 /* Full footprint NDF tensor (pure normal histogram, Eq. 2 with sigma_r -> 0,
  * bin masses summing to 1 per footprint): D[z][x][y], x = n_x bin, y = n_y bin. */
 EXPORT void synth_hist_tensor(int32_t N, const uint16_t* bins, int32_t A, int32_t s0, int32_t L, double* D) {

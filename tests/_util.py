@@ -1,0 +1,76 @@
+"""Shared helpers for the GPU parity tests (test infrastructure)."""
+from __future__ import annotations
+
+import functools
+
+import numpy as np
+
+import oracle
+import synth
+
+# BASELINE.json north_star: "within 1e-4 relative (or 1e-7 absolute on near-zero values) in fp32"
+RTOL = 1e-4
+ATOL = 1e-7
+
+
+def assert_parity(gpu: np.ndarray, ref: np.ndarray, what: str = ""):
+    """|g - o| <= 1e-4 |o|  or  |g - o| <= 1e-7, element by element; NaN only where the oracle is NaN."""
+    gpu = np.asarray(gpu, np.float64)
+    ref = np.asarray(ref, np.float64)
+    assert gpu.shape == ref.shape
+    nan_o, nan_g = np.isnan(ref), np.isnan(gpu)
+    assert np.array_equal(nan_o, nan_g), f"{what}: NaN pattern differs ({nan_o.sum()} vs {nan_g.sum()})"
+    m = ~nan_o
+    err = np.abs(gpu[m] - ref[m])
+    ok = (err <= RTOL * np.abs(ref[m])) | (err <= ATOL)
+    if not ok.all():
+        bad = np.flatnonzero(~ok)[:5]
+        raise AssertionError(f"{what}: {int((~ok).sum())}/{ok.size} outside tolerance; e.g. gpu={gpu[m][bad]} "
+                             f"oracle={ref[m][bad]}")
+    rel = err / np.maximum(np.abs(ref[m]), 1e-300)
+    return dict(n=int(m.sum()), max_abs=float(err.max(initial=0)), max_rel_nonzero=float(
+        rel[np.abs(ref[m]) > 1e-6].max(initial=0)), zeros=int((ref[m] == 0).sum()))
+
+
+def torch_records(recs: np.ndarray, device="cuda"):
+    import torch
+    return torch.from_numpy(np.ascontiguousarray(recs).view(np.int32).reshape(-1, 4)).to(device)
+
+
+def run_gpu(desc_args: dict, f, recs: np.ndarray, opts: int = 0, lanes: int = 0):
+    """Load a store from raw factors, run one batch through the C ABI, return fp32 results + sticky status."""
+    import torch
+    from paper_2109_14807_b200 import pndf
+    d = pndf.make_desc(**desc_args)
+    st = pndf.load_factors(d, f.C, f.X, f.Y, f.Z)
+    if lanes:
+        st.set_lanes(lanes)
+    q = torch_records(recs)
+    out = torch.empty(recs.shape[0], dtype=torch.float32, device="cuda")
+    st.query_batch(q, out, opts)
+    status = st.sync(raise_on_query_error=False)
+    res = out.cpu().numpy()
+    st.free()
+    return res, status
+
+
+def desc_args(cfg) -> dict:
+    return dict(N=cfg.N, s0=cfg.s0, L=cfg.L, A=cfg.A, R=cfg.R, wrap=cfg.wrap)
+
+
+@functools.lru_cache(maxsize=None)
+def config_inputs(k: int, host_z: bool = True):
+    """(cfg, nxy-free bins, factors) for BASELINE config k (cached per process)."""
+    cfg = synth.CONFIGS[k]
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    f = synth.build_factors(cfg, nxy, bins, with_z=host_z)
+    return cfg, bins, f
+
+
+def oracle_on(cfg, f, recs, mean=True, zsparse=None):
+    d = oracle.desc_of(cfg)
+    if zsparse is None:
+        return oracle.query_batch(d, f.C, f.X, f.Y, f.Z, recs, mean=mean)
+    Zs, zmap = zsparse
+    return oracle.query_batch(d, f.C, f.X, f.Y, Zs, recs, mean=mean, zmap=zmap)

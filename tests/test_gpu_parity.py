@@ -1,0 +1,288 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the fp64 oracle, element by element.
+
+Tolerance (BASELINE.json north_star): |g - o| <= 1e-4 |o| or <= 1e-7 absolute.
+Integer-valued work (store image bits, binning permutation effects, NaN pattern
+of invalid records) is compared bit-exactly.
+"""
+import ctypes
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests._util import assert_parity, config_inputs, desc_args, oracle_on, run_gpu, torch_records
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def _pndf():
+    from paper_2109_14807_b200 import pndf
+    return pndf
+
+
+def _rand_records(rng, n, N, A, lg_lo, lg_hi, span=(-1.0, 2.0)):
+    u = rng.uniform(span[0] * N, span[1] * N, n)
+    v = rng.uniform(span[0] * N, span[1] * N, n)
+    S = np.exp2(rng.uniform(lg_lo, lg_hi, n))
+    x1 = rng.integers(0, A, n)
+    x2 = np.minimum(A - 1, x1 + rng.integers(0, max(1, A // 3), n))
+    y1 = rng.integers(0, A, n)
+    y2 = np.minimum(A - 1, y1 + rng.integers(0, max(1, A // 3), n))
+    return synth.make_records(u, v, S, x1, x2, y1, y2)
+
+
+SHAPES = [  # N, s0, L, A, R, wrap
+    (8, 1, 4, 1, 1, True), (16, 1, 5, 5, 3, False), (64, 2, 6, 32, 8, True), (32, 1, 6, 64, 17, True),
+    (128, 1, 8, 128, 64, False), (64, 1, 7, 256, 100, True), (32, 1, 6, 16, 256, True),
+    (16, 1, 5, 8, 1024, True), (256, 4, 7, 8, 33, True), (64, 1, 3, 20, 12, False),
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "N%d_s%d_L%d_A%d_R%d_%s" % (*s[:5], "w" if s[5] else "c"))
+@pytest.mark.parametrize("mode", ["mean", "sum"])
+def test_random_store_parity(shape, mode):
+    N, s0, L, A, R, wrap = shape
+    P = sum((N // (s0 << l)) ** 2 for l in range(L))
+    f = synth.random_factors(A, R, P, seed=N + R, sparsity=0.4)
+    rng = np.random.default_rng(R * 7 + A)
+    recs = _rand_records(rng, 3001, N, A, -2.0, L + 2.0)  # ragged: 3001 is no multiple of any warp split
+    d = oracle.make_desc(N, s0, L, A, R, wrap)
+    mean = mode == "mean"
+    ref = oracle.query_batch(d, f.C, f.X, f.Y, f.Z, recs, mean=mean)
+    for opts in (0 if mean else 1, (0 if mean else 1) | 2):  # unbinned, binned
+        got, st = run_gpu(dict(N=N, s0=s0, L=L, A=A, R=R, wrap=wrap), f, recs, opts)
+        assert st == 0
+        assert_parity(got, ref, f"{shape} opts={opts}")
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_config_full_parity(k):
+    """Configs 1-2: every query of the batch."""
+    cfg, bins, f = config_inputs(k)
+    recs = synth.gen_queries(cfg, bins)
+    ref = oracle_on(cfg, f, recs)
+    got, st = run_gpu(desc_args(cfg), f, recs, 0)
+    assert st == 0
+    stats = assert_parity(got, ref, f"config {k}")
+    assert stats["zeros"] < 0.9 * stats["n"]  # not dominated by blank-region queries
+    got_b, _ = run_gpu(desc_args(cfg), f, recs, 2)
+    assert got_b.tobytes() == got.tobytes()  # binning never changes a bit
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_config_sampled_parity(k):
+    """Configs 3-4 at full size in bench's launch configuration (one batch, BIN_AUTO): sampled outputs."""
+    cfg, bins, f = config_inputs(k)
+    recs = synth.gen_queries(cfg, bins)
+    got, st = run_gpu(desc_args(cfg), f, recs, 0)
+    assert st == 0
+    rng = np.random.default_rng(k)
+    idx = np.unique(rng.integers(0, cfg.n_queries, 100_000))
+    ref = oracle_on(cfg, f, recs[idx])
+    assert_parity(got[idx], ref, f"config {k}")
+    del recs
+
+
+def test_config5_full_size_sampled():
+    """Config 5 at full size (4096^2, A=R=256, P=22.4M rows, 10^9 queries in one batch as bench.py times it);
+    the oracle checks a sample, with the Z rows it needs rebuilt on the host by the CPU generator."""
+    pndf = _pndf()
+    cfg = synth.CONFIGS[5]
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    del nxy
+    f = synth.build_factors(cfg, None, bins, with_z=False)
+    am = f.info["atom_map"]
+    Zd = synth.build_z_exact_cuda(cfg, am)
+    st = pndf.load_factors(pndf.make_desc(**desc_args(cfg)), f.C, f.X, f.Y, Zd)
+    n = cfg.n_queries
+    q = torch.empty((n, 4), dtype=torch.int32, device="cuda")
+    chunk = 50_000_000
+    for a in range(0, n, chunk):
+        b = min(n, a + chunk)
+        q[a:b].copy_(torch_records(synth.gen_queries(cfg, bins, a, b), "cpu"))
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    st.query_batch(q, out, 0)
+    st.sync()
+    rng = np.random.default_rng(5)
+    idx = np.unique(rng.integers(0, n, 20_000))
+    recs = np.ascontiguousarray(q[torch.from_numpy(idx).cuda()].cpu().numpy()).view(synth.QREC).reshape(-1)
+    got = out[torch.from_numpy(idx).cuda()].cpu().numpy()
+    rows, _ = oracle.neighbours(oracle.desc_of(cfg), recs)
+    need = np.unique(rows[rows >= 0])
+    Zs, zmap = oracle.sparse_z(need, cfg.P, lambda u: synth.build_z_rows(cfg, am, u))
+    # the GPU generator built the same Z bits the CPU generator does (input parity)
+    assert np.array_equal(Zd[torch.from_numpy(need).cuda()].cpu().numpy(), Zs)
+    ref = oracle_on(cfg, f, recs, zsparse=(Zs, zmap))
+    assert_parity(got, ref, "config 5")
+    st.free()
+
+
+def test_binning_bitwise_identical_config3():
+    cfg, bins, f = config_inputs(3)
+    recs = synth.gen_queries(cfg, bins, 0, 2_000_000)
+    a, _ = run_gpu(desc_args(cfg), f, recs, 2)  # BIN_ON
+    b, _ = run_gpu(desc_args(cfg), f, recs, 4)  # BIN_OFF
+    assert a.tobytes() == b.tobytes()
+
+
+def test_host_pipeline_matches_device_path():
+    pndf = _pndf()
+    cfg, bins, f = config_inputs(3)
+    recs = synth.gen_queries(cfg, bins, 0, 3_000_017)
+    st = pndf.load_factors(pndf.make_desc(**desc_args(cfg)), f.C, f.X, f.Y, f.Z)
+    h_out = np.empty(recs.shape[0], np.float32)
+    st.query_batch_host(recs, h_out, 0)
+    q = torch_records(recs)
+    out = torch.empty(recs.shape[0], dtype=torch.float32, device="cuda")
+    st.query_batch(q, out, 0)
+    st.sync()
+    assert out.cpu().numpy().tobytes() == h_out.tobytes()
+    pin = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).pin_memory()
+    pout = torch.empty(recs.shape[0], dtype=torch.float32).pin_memory()
+    st.query_batch_host(pin, pout, 2)
+    assert pout.numpy().tobytes() == h_out.tobytes()
+    st.free()
+
+
+def test_edge_cases():
+    pndf = _pndf()
+    N, s0, L, A, R = 32, 1, 6, 256, 8
+    P = sum((N >> l) ** 2 for l in range(L))
+    f = synth.random_factors(A, R, P, seed=1)
+    d = oracle.make_desc(N, s0, L, A, R, True)
+    recs = synth.make_records(
+        [0.0, 31.999998, -1e6, 4e6, 16.0, 5.5, 5.5, 5.5, 0.5, 0.5],
+        [0.0, 31.999998, 3e6, -4e6, 16.0, 5.5, 5.5, 5.5, 0.5, 0.5],
+        [1.0, 1e30, 1e-30, 7.3, 2.0 ** 5, 2.0 ** 4.5, 1.0, 3.0, 1.0, 1.0],
+        [0, 255, 0, 17, 0, 0, 128, 255, 3, 3], [255, 255, 0, 200, 255, 0, 128, 255, 3, 3],
+        [0, 255, 255, 3, 0, 0, 0, 0, 7, 7], [255, 255, 255, 4, 0, 255, 255, 255, 7, 7])
+    ref = oracle.query_batch(d, f.C, f.X, f.Y, f.Z, recs)
+    st = pndf.load_factors(pndf.make_desc(N, s0, L, A, R, True), f.C, f.X, f.Y, f.Z)
+    for n in (1, 2, 7, 10):
+        q = torch_records(recs[:n])
+        out = torch.empty(n, dtype=torch.float32, device="cuda")
+        st.query_batch(q, out, 0)
+        st.sync()
+        assert_parity(out.cpu().numpy(), ref[:n], f"edge n={n}")
+    # empty batch is a no-op
+    st.query_batch(torch.empty((0, 4), dtype=torch.int32, device="cuda"),
+                   torch.empty(0, dtype=torch.float32, device="cuda"), 0)
+    st.sync()
+    # invalid records: NaN + sticky EQUERY, cleared by sync, store stays usable
+    bad = synth.make_records([1, np.nan, 1, 1, 5e6], [1, 1, 1, 1, 1], [1, 1, 0, -2, 1],
+                             [0, 0, 5, 0, 0], [3, 3, 3, 3, 3], [0, 0, 0, 0, 0], [3, 3, 3, 3, 3])
+    q = torch_records(bad)
+    out = torch.empty(5, dtype=torch.float32, device="cuda")
+    st.query_batch(q, out, 0)
+    assert st.sync(raise_on_query_error=False) == pndf.EQUERY
+    o = out.cpu().numpy()
+    assert np.isfinite(o[0]) and np.isnan(o[1:]).all()
+    assert st.sync() == 0
+    st.free()
+
+
+def test_argument_errors():
+    pndf = _pndf()
+    f = synth.random_factors(4, 2, 85, seed=1)
+    with pytest.raises(pndf.PndfError):   # L too large for N/s0
+        pndf.load_factors(pndf.make_desc(8, 1, 5, 4, 2), f.C, f.X, f.Y, f.Z)
+    with pytest.raises(pndf.PndfError):   # A > 256
+        pndf.load_factors(pndf.make_desc(8, 1, 4, 300, 2), f.C, f.X, f.Y, f.Z)
+    Zn = f.Z.copy(); Zn[3, 1] = -1e-3
+    with pytest.raises(pndf.PndfError):   # negative factor
+        pndf.load_factors(pndf.make_desc(8, 1, 4, 4, 2), f.C, f.X, f.Y, Zn)
+    Xn = f.X.copy(); Xn[0, 0] = np.inf
+    with pytest.raises(pndf.PndfError):   # non-finite factor
+        pndf.load_factors(pndf.make_desc(8, 1, 4, 4, 2), f.C, Xn, f.Y, f.Z)
+    Cn = f.C.copy(); Cn[1] = np.nan
+    with pytest.raises(pndf.PndfError):
+        pndf.load_factors(pndf.make_desc(8, 1, 4, 4, 2), Cn, f.X, f.Y, f.Z)
+    st = pndf.load_factors(pndf.make_desc(8, 1, 4, 4, 2), f.C, f.X, f.Y, f.Z)
+    out = torch.empty(4, dtype=torch.float32, device="cuda")
+    q = torch.zeros((4, 4), dtype=torch.int32, device="cuda")
+    with pytest.raises(pndf.PndfError):
+        st.query_batch(q, out, 0x100)     # unknown opts bit
+    with pytest.raises(pndf.PndfError):
+        st.query_batch(q, out, 2 | 4)     # BIN_ON | BIN_OFF
+    with pytest.raises(pndf.PndfError):
+        st.set_lanes(3)
+    st.free()
+
+
+def test_store_image_bits():
+    """Store build (row a0): Zc = fl32(C*Z), padded ranks 0; prefix = fp64 running sum split into fp32 hi/lo.
+    Reconstructed here independently with numpy."""
+    pndf = _pndf()
+    N, s0, L, A, R = 16, 1, 5, 37, 13
+    P = sum((N >> l) ** 2 for l in range(L))
+    f = synth.random_factors(A, R, P, seed=3, sparsity=0.2)
+    st = pndf.load_factors(pndf.make_desc(N, s0, L, A, R), f.C, f.X, f.Y, f.Z)
+    pxy, zc = st.image()
+    Rp = st.stats()["rank_padded"]
+    assert Rp % 4 == 0 and Rp >= R
+    want = np.zeros((P, Rp), np.float32)
+    want[:, :R] = f.C[None, :] * f.Z   # numpy fp32 multiply = fl32 of the exact product
+    assert zc.tobytes() == want.tobytes()
+    for t, F in enumerate((f.X, f.Y)):
+        S = np.zeros((A + 1, Rp))
+        for k in range(A):            # sequential fp64 running sum, index order
+            S[k + 1, :R] = S[k, :R] + F[k].astype(np.float64)
+        hi = S.astype(np.float32)
+        lo = (S - hi.astype(np.float64)).astype(np.float32)
+        assert pxy[t, :, 0].tobytes() == hi.tobytes()
+        assert pxy[t, :, 1].tobytes() == lo.tobytes()
+    st.free()
+
+
+@pytest.mark.parametrize("k", [2, 5])
+def test_lane_splits_agree(k):
+    """Every supported lane split G computes the same query within tolerance (the rank reduction order differs)."""
+    pndf = _pndf()
+    if k == 5:
+        cfg = synth.CONFIGS[5].scaled(N=256)
+    else:
+        cfg = synth.CONFIGS[k]
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    f = synth.build_factors(cfg, nxy, bins)
+    recs = synth.gen_queries(cfg, bins, 0, 50_000)
+    ref = oracle_on(cfg, f, recs)
+    st = pndf.load_factors(pndf.make_desc(**desc_args(cfg)), f.C, f.X, f.Y, f.Z)
+    Rp = st.stats()["rank_padded"]
+    q = torch_records(recs)
+    for G in (1, 2, 4, 8, 16, 32):
+        if Rp % (4 * G) or (Rp // (4 * G)) not in (1, 2, 3, 4, 8):
+            continue
+        st.set_lanes(G)
+        out = torch.empty(recs.shape[0], dtype=torch.float32, device="cuda")
+        st.query_batch(q, out, 0)
+        st.sync()
+        assert_parity(out.cpu().numpy(), ref, f"G={G}")
+    st.free()
+
+
+def test_cuda_graph_replay():
+    """pndf_query_batch is capturable (scratch pre-sized by a first run): replaying the graph gives the same bits."""
+    pndf = _pndf()
+    cfg, bins, f = config_inputs(2)
+    recs = synth.gen_queries(cfg, bins, 0, 200_000)
+    st = pndf.load_factors(pndf.make_desc(**desc_args(cfg)), f.C, f.X, f.Y, f.Z)
+    q = torch_records(recs)
+    out = torch.empty(recs.shape[0], dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        st.query_batch(q, out, 2, stream=s)
+        st.sync(stream=s)
+        first = out.clone()
+        out.zero_()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            st.query_batch(q, out, 2, stream=s)
+        g.replay()
+        s.synchronize()
+    assert out.cpu().numpy().tobytes() == first.cpu().numpy().tobytes()
+    st.free()
