@@ -59,7 +59,7 @@ typedef struct pndf_store_s* pndf_store; /* opaque; factors immutable after load
 /* Store geometry.  Level l (0 <= l < L) has stride s_l = base_stride*2^l and an
  * n_l x n_l grid of footprint centres ((i+1/2)s_l, (j+1/2)s_l), n_l = map_size/s_l
  * (P:274-279).  Positional index z = off_l + j*n_l + i, off_l = sum_{m<l} n_m^2;
- * P = sum_l n_l^2 rows. */
+ * P = sum_l n_l^2 rows, P < 2^31. */
 typedef struct {
     uint32_t abi_version; /* = PNDF_ABI_VERSION                                  */
     int32_t map_size;     /* N texels per side, power of two, <= 2^20            */

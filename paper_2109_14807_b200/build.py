@@ -22,12 +22,15 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in DEPS)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: str | None = None, defines=()) -> str:
+    """Build libpndf.so (or an experiment variant at `out` with extra -D defines)."""
+    target = out or LIB
+    if not force and out is None and not stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = LIB + f".{os.getpid()}.tmp"
-    cmd = [nvcc, "-shared", *NVCC_FLAGS, "-I", os.path.join(ROOT, "include"), *SOURCES, "-o", tmp]
+    tmp = target + f".{os.getpid()}.tmp"
+    cmd = [nvcc, "-shared", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
+           *SOURCES, "-o", tmp]
     r = subprocess.run(cmd, capture_output=True, text=True)
     os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
     with open(os.path.join(ROOT, "build", "ptxas.log"), "w") as f:
@@ -35,11 +38,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if r.returncode != 0:
         sys.stderr.write(r.stderr[-4000:])
         raise RuntimeError("nvcc failed building libpndf.so (see build/ptxas.log)")
-    os.replace(tmp, LIB)
+    os.replace(tmp, target)
     if verbose:
-        print(f"built {LIB}")
-    return LIB
+        print(f"built {target}")
+    return target
 
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
+    if "--variants" in sys.argv:  # tuning experiments: occupancy targets of the query kernel
+        for mb in (1, 3):
+            build(out=os.path.join(PKG, f"libpndf_minb{mb}.so"), defines=[f"PNDF_MINB={mb}"], verbose=True)

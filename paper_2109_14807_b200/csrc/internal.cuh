@@ -33,12 +33,13 @@ struct QParams {
     uint32_t mean;                 // 1 = divide by the rectangle area
 };
 
-// Binning geometry: key = base[l0] + Morton(i0 >> shift, j0 >> shift) at level l0.
-struct BinGeom {
-    int32_t shift;
-    int32_t L;
-    int64_t base[kMaxLevels];
-    int64_t nbins;  // including the trailing "invalid record" bin
+// Device scratch of one in-flight binned batch (radix sort double buffers).
+struct BinScratch {
+    uint32_t* keys[2] = {nullptr, nullptr};
+    uint32_t* vals[2] = {nullptr, nullptr};
+    uint32_t* counts = nullptr;  // radix_tiles(cap) * 256 digit counts / offsets
+    uint32_t* bsum = nullptr;    // scan block sums
+    int64_t cap = 0;
 };
 
 }  // namespace pndf

@@ -15,13 +15,14 @@ bool lanes_supported(int G, int NV);
 cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,
                          float* out, int num_sms, cudaStream_t st);
 
-int64_t scan_blocks(int64_t nbins);
+int64_t scan_blocks(int64_t nb);
+int64_t radix_tiles(int64_t n);
 
-// Counting sort of n records by bin key into (binned, idx). hist must hold
-// nbins entries, bsum scan_blocks(nbins) entries.
-cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, uint32_t* keys, uint32_t* hist,
-                           int64_t nbins, uint32_t* bsum, pndf_query* binned, uint32_t* idx, int num_sms,
-                           cudaStream_t st, int* launches);
+// Sort the n records by bin key (store with P rows) with an LSD radix sort;
+// *perm receives the device permutation (query indices in binned order).
+// Scratch: keys/vals [cap], counts [radix_tiles(cap)*512], bsum [scan_blocks(that)].
+cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int64_t P, BinScratch& sc,
+                           int num_sms, cudaStream_t st, int* launches, const uint32_t** perm);
 
 // Store build kernels (store.cu).
 cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float* Cdev, float* Zc_dst, int Rp,

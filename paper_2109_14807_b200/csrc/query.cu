@@ -1,7 +1,7 @@
 // query.cu -- sm_100a kernels of the batched NDF range query (the hot path).
 //
 // Rows of SURVEY.md §8(a) implemented here:
-//   a1  query binning        bin_keys_kernel, scan_*_kernel, bin_scatter_kernel
+//   a1  query binning        bin_keys_kernel + LSD radix sort (rs_hist/scan/rs_scatter)
 //   a2  decode + level select  decode()
 //   a3  spatial neighbours     decode()
 //   a4  positional gather + interpolation  query_kernel: 8 rows of Zc, float4 per lane
@@ -31,10 +31,12 @@ __device__ __forceinline__ pndf_query ldg_query(const pndf_query* q) {
     return r;
 }
 
-// off_l = sum_{m<l} (n0 >> m)^2 = 4 (n0^2 - n_l^2) / 3 for power-of-two n0 (exact)
+// off_l = sum_{m<l} (n0 >> m)^2 = 4 n_l^2 (4^l - 1)/3 for power-of-two n0, and
+// (4^l - 1)/3 = 0x5555... (l bit pairs): exact, no division.
 __device__ __forceinline__ int64_t level_offset(int64_t n0, int l) {
     const int64_t nl = n0 >> l;
-    return 4 * (n0 * n0 - nl * nl) / 3;
+    const uint64_t m = l ? (0x5555555555555555ULL >> (64 - 2 * l)) : 0ULL;
+    return (int64_t)((uint64_t)(nl * nl) * 4ULL * m);
 }
 
 __device__ __forceinline__ uint32_t part1by1(uint32_t x) {
@@ -78,14 +80,15 @@ __device__ __forceinline__ void level_select(const QParams& p, float size, int& 
 
 // a3: neighbour cell along one axis at level l: f = u/s_l - 1/2 (exact in fp32
 // for |u| <= 2^22), i0 = floor(f), a = f - i0; wrap (power-of-two grid) or clamp.
+template <bool WRAP>
 __device__ __forceinline__ void axis_cells(const QParams& p, float u, int l, int& i0, int& i1, float& a) {
     const int n = p.n0 >> l;
-    const float f = fmaf(u, ldexpf(p.inv_s0, -l), -0.5f);
+    const float f = fmaf(u, __int_as_float(__float_as_int(p.inv_s0) - (l << 23)), -0.5f);  // u / (s0 2^l) - 1/2
     const float fl = floorf(f);
     a = f - fl;
     i0 = (int)fl;
     i1 = i0 + 1;
-    if (p.wrap) {
+    if (WRAP) {
         i0 &= n - 1;
         i1 &= n - 1;
     } else {
@@ -94,126 +97,290 @@ __device__ __forceinline__ void axis_cells(const QParams& p, float u, int l, int
     }
 }
 
-// a2 + a3: the 8 (row, weight) pairs of a valid record.
-__device__ __forceinline__ void neighbours(const QParams& p, const pndf_query& q, int64_t (&row)[8], float (&w)[8]) {
+// ------------------------------------------------- decoded query (smem) --
+// One warp decodes 32 records at once (one per lane) into these descriptors,
+// then the whole warp gathers for them G lanes per query.
+struct __align__(16) QDesc {
+    int32_t row[8];  // Zc rows of the 8 neighbours (level l0: (i0,j0),(i1,j0),(i0,j1),(i1,j1); then l0+1)
+    float w[8];      // trilinear weights (1-t)(1-a)(1-b), ...
+    uint32_t px;     // prefix entries x1 | (x2+1) << 16
+    uint32_t py;     // prefix entries y1 | (y2+1) << 16
+    float div;       // rectangle area (MEAN), 1 (SUM), NaN (invalid record)
+    int32_t out;     // output index within the (sub-)batch, -1 = no query
+};
+static_assert(sizeof(QDesc) == 80, "QDesc layout");
+
+template <bool WRAP>
+__device__ __forceinline__ void decode(const QParams& p, const pndf_query& rec, int32_t out_index, QDesc& d) {
+    int x1, x2, y1, y2;
+    if (!record_valid(p, rec, x1, x2, y1, y2)) {
+        atomicOr(p.err, 1u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            d.row[k] = 0;
+            d.w[k] = 0.f;
+        }
+        d.px = 0;
+        d.py = 0;
+        d.div = __int_as_float(0x7fc00000);
+        d.out = out_index;
+        return;
+    }
     int l0;
     float t;
-    level_select(p, q.size, l0, t);
+    level_select(p, rec.size, l0, t);
 #pragma unroll
     for (int dl = 0; dl < 2; ++dl) {
         const int l = l0 + dl;
         const float wl = dl ? t : 1.f - t;
         int i0, i1, j0, j1;
         float a, b;
-        axis_cells(p, q.u, l, i0, i1, a);
-        axis_cells(p, q.v, l, j0, j1, b);
-        const int64_t n = p.n0 >> l;
-        const int64_t off = level_offset(p.n0, l);
-        row[4 * dl + 0] = off + (int64_t)j0 * n + i0;
-        row[4 * dl + 1] = off + (int64_t)j0 * n + i1;
-        row[4 * dl + 2] = off + (int64_t)j1 * n + i0;
-        row[4 * dl + 3] = off + (int64_t)j1 * n + i1;
+        axis_cells<WRAP>(p, rec.u, l, i0, i1, a);
+        axis_cells<WRAP>(p, rec.v, l, j0, j1, b);
+        const int32_t n = p.n0 >> l;
+        const int32_t off = (int32_t)level_offset(p.n0, l);
+        d.row[4 * dl + 0] = off + j0 * n + i0;
+        d.row[4 * dl + 1] = off + j0 * n + i1;
+        d.row[4 * dl + 2] = off + j1 * n + i0;
+        d.row[4 * dl + 3] = off + j1 * n + i1;
         const float wa = wl * (1.f - a), wb = wl * a;
-        w[4 * dl + 0] = wa * (1.f - b);
-        w[4 * dl + 1] = wb * (1.f - b);
-        w[4 * dl + 2] = wa * b;
-        w[4 * dl + 3] = wb * b;
+        d.w[4 * dl + 0] = wa * (1.f - b);
+        d.w[4 * dl + 1] = wb * (1.f - b);
+        d.w[4 * dl + 2] = wa * b;
+        d.w[4 * dl + 3] = wb * b;
     }
+    d.px = (uint32_t)x1 | ((uint32_t)(x2 + 1) << 16);
+    d.py = (uint32_t)y1 | ((uint32_t)(y2 + 1) << 16);
+    d.div = p.mean ? (float)((x2 - x1 + 1) * (y2 - y1 + 1)) : 1.f;
+    d.out = out_index;
 }
 
 // ------------------------------------------------------- query kernel --
-// G lanes share one query; each lane owns NV float4 rank chunks at float
-// offsets (gl + v*G)*4, so the G lanes of a query read each 4*G-float slice of
-// a row contiguously (coalesced 16-byte loads).  Per lane and chunk: 8 Zc
-// loads (a4) + 8 prefix loads (a5, hi/lo of 4 rows), all issued before use.
-// Per-query results do not depend on the query's position in the batch, so
-// binned and unbinned batches are bitwise identical.
-template <int G, int NV, bool BINNED>
-__global__ void __launch_bounds__(kThreads) query_kernel(const QParams p, const pndf_query* __restrict__ q,
-                                                         const uint32_t* __restrict__ idx, int64_t n,
-                                                         float* __restrict__ out) {
-    constexpr int QPW = 32 / G;
-    const int lane = threadIdx.x & 31;
-    const int gl = lane % G;
-    const int grp = lane / G;
-    const int64_t gw = ((int64_t)blockIdx.x * kThreads + threadIdx.x) >> 5;
-    const int64_t nw = ((int64_t)gridDim.x * kThreads) >> 5;
-    const size_t Rp = (size_t)p.Rp;
-    const float* __restrict__ PX = p.PXY;
-    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * 2 * Rp;
-    const float* __restrict__ Zc = p.Zc;
+// Work split: CTA b owns the contiguous query range [b*chunk, (b+1)*chunk), so
+// binned (sorted) queries that share Zc rows run on the same SM and hit in L1.
+// Each warp takes 32 consecutive queries of the CTA's range at a time:
+//   1. decode: lane i decodes query i into a QDesc in shared memory;
+//   2. gather: G lanes per query (QPW = 32/G queries per step); each lane owns
+//      NV float4 rank chunks at float offsets (gl + v*G)*4, so a query's G lanes
+//      read each row slice contiguously; 8 Zc + 8 prefix (hi, lo) loads per chunk,
+//      all issued before use; RP = 4*G*NV is a compile-time row stride;
+//   3. reduce: xor-butterfly over the G lanes (IEEE + is commutative, so all
+//      lanes of the group hold identical bits), then lane j of the warp keeps
+//      query j's value and the warp writes 32 results at once.
+// A query's result never depends on where it sits in the batch, so binned and
+// unbinned batches are bitwise identical.
+constexpr int kWarpsPerBlock = kThreads / 32;
+#ifndef PNDF_MINB
+#define PNDF_MINB 2  // min resident blocks per SM (tuned on B200: 2-3 beat 1, see profiles/)
+#endif
 
-    for (int64_t base = gw * QPW; base < n; base += nw * QPW) {
-        const int64_t qi = base + grp;
-        float part = 0.f;
-        int status = 0;  // 0: no query, 1: valid, 2: invalid record
-        float area = 1.f;
-        int64_t oi = qi;
-        if (qi < n) {
-            const pndf_query rec = ldg_query(q + qi);
-            if (BINNED) oi = (int64_t)__ldg(idx + qi);
-            int x1, x2, y1, y2;
-            if (record_valid(p, rec, x1, x2, y1, y2)) {
-                status = 1;
-                area = (float)((x2 - x1 + 1) * (y2 - y1 + 1));
-                int64_t row[8];
-                float w[8];
-                neighbours(p, rec, row, w);
-                const float* px0 = PX + (size_t)(2 * x1) * Rp;
-                const float* px1 = PX + (size_t)(2 * (x2 + 1)) * Rp;
-                const float* py0 = PY + (size_t)(2 * y1) * Rp;
-                const float* py1 = PY + (size_t)(2 * (y2 + 1)) * Rp;
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const int c = (gl + v * G) * 4;
-                    float4 zr[8];
-#pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        zr[k] = (w[k] != 0.f) ? ldg4(Zc + (size_t)row[k] * Rp + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-                    const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
-                    const float4 xl1 = ldg4(px1 + Rp + c), xl0 = ldg4(px0 + Rp + c);
-                    const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
-                    const float4 yl1 = ldg4(py1 + Rp + c), yl0 = ldg4(py0 + Rp + c);
-                    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) {
-                        z.x = fmaf(w[k], zr[k].x, z.x);
-                        z.y = fmaf(w[k], zr[k].y, z.y);
-                        z.z = fmaf(w[k], zr[k].z, z.z);
-                        z.w = fmaf(w[k], zr[k].w, z.w);
-                    }
-                    // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
-                    // under cancellation (Sterbenz), lo carries the fp64 residual.
-                    const float dx0 = (xh1.x - xh0.x) + (xl1.x - xl0.x), dy0 = (yh1.x - yh0.x) + (yl1.x - yl0.x);
-                    const float dx1 = (xh1.y - xh0.y) + (xl1.y - xl0.y), dy1 = (yh1.y - yh0.y) + (yl1.y - yl0.y);
-                    const float dx2 = (xh1.z - xh0.z) + (xl1.z - xl0.z), dy2 = (yh1.z - yh0.z) + (yl1.z - yl0.z);
-                    const float dx3 = (xh1.w - xh0.w) + (xl1.w - xl0.w), dy3 = (yh1.w - yh0.w) + (yl1.w - yl0.w);
-                    part = fmaf(dx0 * dy0, z.x, part);
-                    part = fmaf(dx1 * dy1, z.y, part);
-                    part = fmaf(dx2 * dy2, z.z, part);
-                    part = fmaf(dx3 * dy3, z.w, part);
-                }
+template <int G, int NV, bool WRAP, bool BINNED>
+__global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParams p, const pndf_query* __restrict__ q,
+                                                         const uint32_t* __restrict__ idx, int64_t n,
+                                                         int64_t chunk, float* __restrict__ out) {
+    constexpr int QPW = 32 / G;
+    constexpr int RP = 4 * G * NV;
+    __shared__ QDesc sdesc[kWarpsPerBlock][32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gl = lane % G, grp = lane / G;
+    QDesc* wd = sdesc[warp];
+    const float* __restrict__ Zc = p.Zc;
+    const float* __restrict__ PX = p.PXY;
+    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * 2 * RP;
+
+    const int64_t c0 = (int64_t)blockIdx.x * chunk;
+    const int64_t c1 = min(n, c0 + chunk);
+    for (int64_t base = c0 + (int64_t)warp * 32; base < c1; base += (int64_t)kWarpsPerBlock * 32) {
+        // 1. decode 32 records, one per lane
+        {
+            const int64_t qi = base + lane;
+            if (qi < c1) {
+                // binned: idx is the radix-sorted permutation; gather the record through it
+                const int64_t src = BINNED ? (int64_t)__ldg(idx + qi) : qi;
+                const pndf_query rec = ldg_query(q + src);
+                const int32_t oi = (int32_t)src;
+                decode<WRAP>(p, rec, oi, wd[lane]);
             } else {
-                status = 2;
+                wd[lane].out = -1;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    wd[lane].row[k] = 0;
+                    wd[lane].w[k] = 0.f;
+                }
+                wd[lane].px = 0;
+                wd[lane].py = 0;
+                wd[lane].div = 1.f;
             }
         }
-        // a6: fixed xor-butterfly over the G lanes of the query (IEEE + is commutative,
-        // so every lane of the group ends with the same bits).
+        __syncwarp();
+        // 2-3. gather + reduce, QPW queries per step.  With G == 32 a warp runs one
+        // query per step and keeps the previous query's Zc rows in registers: binned
+        // neighbours with the same half cell (all 8 rows equal) skip the Zc loads.
+        float res = 0.f;
+        float4 zc[NV][8];
+        int cached[8];
 #pragma unroll
-        for (int o = G / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-        if (gl == 0 && status != 0) {
-            out[oi] = (status == 1) ? (p.mean ? part / area : part) : __int_as_float(0x7fc00000);
-            if (status == 2) atomicOr(p.err, 1u);
+        for (int k = 0; k < 8; ++k) cached[k] = -1;
+#pragma unroll 1
+        for (int s = 0; s < 32; s += QPW) {
+            const QDesc& d = wd[s + grp];
+            const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
+            const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
+            const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
+            const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
+            const uint4 tail = *reinterpret_cast<const uint4*>(&d.px);
+            const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
+                                (int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
+            const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
+            const float* px0 = PX + (size_t)(2 * (tail.x & 0xffffu)) * RP;
+            const float* px1 = PX + (size_t)(2 * (tail.x >> 16)) * RP;
+            const float* py0 = PY + (size_t)(2 * (tail.y & 0xffffu)) * RP;
+            const float* py1 = PY + (size_t)(2 * (tail.y >> 16)) * RP;
+            bool reuse = false;
+            if (G == 32) {  // warp-uniform: every lane reads the same descriptor
+                reuse = true;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) reuse = reuse && (row[k] == cached[k]);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) cached[k] = row[k];
+            }
+            if (!reuse) {
+#pragma unroll
+                for (int v = 0; v < NV; ++v)
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) zc[v][k] = ldg4(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
+            }
+            float part = 0.f;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const int c = (gl + v * G) * 4;
+                const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
+                const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
+                const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
+                const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
+                float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    z.x = fmaf(w[k], zc[v][k].x, z.x);
+                    z.y = fmaf(w[k], zc[v][k].y, z.y);
+                    z.z = fmaf(w[k], zc[v][k].z, z.z);
+                    z.w = fmaf(w[k], zc[v][k].w, z.w);
+                }
+                // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
+                // under cancellation (Sterbenz), lo carries the fp64 residual.
+                const float dx0 = (xh1.x - xh0.x) + (xl1.x - xl0.x), dy0 = (yh1.x - yh0.x) + (yl1.x - yl0.x);
+                const float dx1 = (xh1.y - xh0.y) + (xl1.y - xl0.y), dy1 = (yh1.y - yh0.y) + (yl1.y - yl0.y);
+                const float dx2 = (xh1.z - xh0.z) + (xl1.z - xl0.z), dy2 = (yh1.z - yh0.z) + (yl1.z - yl0.z);
+                const float dx3 = (xh1.w - xh0.w) + (xl1.w - xl0.w), dy3 = (yh1.w - yh0.w) + (yl1.w - yl0.w);
+                part = fmaf(dx0 * dy0, z.x, part);
+                part = fmaf(dx1 * dy1, z.y, part);
+                part = fmaf(dx2 * dy2, z.z, part);
+                part = fmaf(dx3 * dy3, z.w, part);
+            }
+#pragma unroll
+            for (int o = G / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+            // lane s+j takes query s+j's value from lane j*G
+            const float got = __shfl_sync(0xffffffffu, part, ((lane - s) & (QPW - 1)) * G);
+            if (lane >= s && lane < s + QPW) res = got;
         }
+        const QDesc& mine = wd[lane];
+        const int32_t oi = mine.out;
+        const float div = mine.div;
+        __syncwarp();
+        if (oi >= 0) out[oi] = res / div;  // a6: Eq. 6 mean (div = area) or sum (div = 1)
     }
 }
 
+// ----------------------------------------------------------- launchers --
+template <int G, int NV, bool W, bool B>
+static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
+                            int num_sms, cudaStream_t st) {
+    static int occ = -1;
+    if (occ < 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, query_kernel<G, NV, W, B>, kThreads, 0) !=
+                cudaSuccess ||
+            occ < 1)
+            occ = 1;
+    }
+    int64_t grid = (int64_t)num_sms * occ;
+    const int64_t need = (n + kThreads - 1) / kThreads;  // at least one query per lane per block
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    int64_t chunk = (n + grid - 1) / grid;
+    chunk = (chunk + 31) / 32 * 32;
+    grid = (n + chunk - 1) / chunk;
+    query_kernel<G, NV, W, B><<<(unsigned)grid, kThreads, 0, st>>>(p, q, idx, n, chunk, out);
+    return cudaGetLastError();
+}
+
+template <int G, bool W, bool B>
+static cudaError_t dispatch_nv(int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
+                               float* out, int num_sms, cudaStream_t st) {
+    switch (NV) {
+        case 1: return launch_q<G, 1, W, B>(p, q, idx, n, out, num_sms, st);
+        case 2: return launch_q<G, 2, W, B>(p, q, idx, n, out, num_sms, st);
+        case 3: return launch_q<G, 3, W, B>(p, q, idx, n, out, num_sms, st);
+        case 4: return launch_q<G, 4, W, B>(p, q, idx, n, out, num_sms, st);
+        case 8: return launch_q<G, 8, W, B>(p, q, idx, n, out, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool W, bool B>
+static cudaError_t dispatch_g(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
+                              float* out, int num_sms, cudaStream_t st) {
+    switch (G) {
+        case 1: return dispatch_nv<1, W, B>(NV, p, q, idx, n, out, num_sms, st);
+        case 2: return dispatch_nv<2, W, B>(NV, p, q, idx, n, out, num_sms, st);
+        case 4: return dispatch_nv<4, W, B>(NV, p, q, idx, n, out, num_sms, st);
+        case 8: return dispatch_nv<8, W, B>(NV, p, q, idx, n, out, num_sms, st);
+        case 16: return dispatch_nv<16, W, B>(NV, p, q, idx, n, out, num_sms, st);
+        case 32: return dispatch_nv<32, W, B>(NV, p, q, idx, n, out, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+bool lanes_supported(int G, int NV) {
+    const bool g = (G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32);
+    const bool v = (NV == 1 || NV == 2 || NV == 3 || NV == 4 || NV == 8);
+    return g && v;
+}
+
+cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,
+                         float* out, int num_sms, cudaStream_t st) {
+    if (4 * G * NV != p.Rp) return cudaErrorInvalidValue;
+    if (p.wrap) {
+        if (idx) return dispatch_g<true, true>(G, NV, p, q, idx, n, out, num_sms, st);
+        return dispatch_g<true, false>(G, NV, p, q, idx, n, out, num_sms, st);
+    }
+    if (idx) return dispatch_g<false, true>(G, NV, p, q, idx, n, out, num_sms, st);
+    return dispatch_g<false, false>(G, NV, p, q, idx, n, out, num_sms, st);
+}
+
 // ------------------------------------------------------------ binning --
-// a1: key = off_{l0} + Morton(i0, j0) -- the record's lower-left neighbour cell
-// on its lower level l0, in Z-order within the level, so queries that share Zc
-// rows become neighbours in the binned order.  Invalid records -> last bin.
+// a1: key = the record's half cell on its lower level l0 (Z-order within the
+// level), so queries that share all 8 Zc rows get equal keys and queries that
+// share some rows get nearby keys.  Invalid records -> the last key.
+// The permutation comes from a stable LSD radix sort (8- or 9-bit digits):
+//   rs_hist_kernel     per-tile digit histograms, digit-major in global memory
+//   scan_*_kernel      exclusive scan of the histograms -> each tile's digit offsets
+//   rs_scatter_kernel  stable tile-local ranking (match_any + per-warp counts),
+//                      staged in shared memory, written out digit run by run.
+__device__ __forceinline__ uint64_t part1by1_64(uint64_t x) {
+    x &= 0x00000000ffffffffULL;
+    x = (x | (x << 16)) & 0x0000ffff0000ffffULL;
+    x = (x | (x << 8)) & 0x00ff00ff00ff00ffULL;
+    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0fULL;
+    x = (x | (x << 2)) & 0x3333333333333333ULL;
+    x = (x | (x << 1)) & 0x5555555555555555ULL;
+    return x;
+}
+
+// half = 1: key = 4 off_{l0} + Morton(floor(2 f_u), floor(2 f_v)) -- a half cell of
+// level l0, so equal keys share all 8 Zc rows (level l0+1's cell is fixed by the
+// half cell); half = 0: cell keys off_{l0} + Morton(i0, j0).
 __global__ void bin_keys_kernel(const QParams p, const pndf_query* __restrict__ q, int64_t n, uint32_t* keys,
-                                uint32_t* hist, uint32_t invalid_key) {
+                                uint32_t invalid_key, int half) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
         const pndf_query rec = ldg_query(q + i);
         int x1, x2, y1, y2;
@@ -222,14 +389,16 @@ __global__ void bin_keys_kernel(const QParams p, const pndf_query* __restrict__ 
             int l0;
             float t;
             level_select(p, rec.size, l0, t);
-            int i0, i1, j0, j1;
-            float a, b;
-            axis_cells(p, rec.u, l0, i0, i1, a);
-            axis_cells(p, rec.v, l0, j0, j1, b);
-            key = (uint32_t)level_offset(p.n0, l0) + (part1by1((uint32_t)i0) | (part1by1((uint32_t)j0) << 1));
+            const int64_t n_l = p.n0 >> l0;
+            const float inv_s = __int_as_float(__float_as_int(p.inv_s0) - (l0 << 23));
+            const int64_t m = (n_l << half) - 1;
+            const float fu = fmaf(rec.u, inv_s, -0.5f), fv = fmaf(rec.v, inv_s, -0.5f);
+            const int64_t hu = (int64_t)floorf(half ? 2.f * fu : fu) & m;
+            const int64_t hv = (int64_t)floorf(half ? 2.f * fv : fv) & m;
+            key = (uint32_t)((level_offset(p.n0, l0) << (2 * half)) +
+                             (int64_t)(part1by1_64((uint64_t)hu) | (part1by1_64((uint64_t)hv) << 1)));
         }
         keys[i] = key;
-        atomicAdd(hist + key, 1u);
     }
 }
 
@@ -326,91 +495,203 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(uint32_t* inou
         if (base + k < nb) inout[base + k] = v[k] + off;
 }
 
-__global__ void bin_scatter_kernel(const pndf_query* __restrict__ q, const uint32_t* __restrict__ keys, int64_t n,
-                                   uint32_t* cursor, pndf_query* binned, uint32_t* idx) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const uint32_t pos = atomicAdd(cursor + keys[i], 1u);
-        reinterpret_cast<uint4*>(binned)[pos] = __ldg(reinterpret_cast<const uint4*>(q + i));
-        idx[pos] = (uint32_t)i;
+constexpr int kRsThreads = 256;
+constexpr int kRsItems = 16;
+constexpr int kRsTile = kRsThreads * kRsItems;  // 4096 keys per tile
+constexpr int kRsWarps = kRsThreads / 32;
+
+// counts[d * ntiles + tile] = #keys of the tile whose digit is d (digits of BITS bits)
+template <int BITS>
+__global__ void __launch_bounds__(kRsThreads) rs_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                                                             uint32_t* counts, int64_t ntiles) {
+    constexpr int RADIX = 1 << BITS;
+    __shared__ uint32_t h[RADIX];
+    for (int d = threadIdx.x; d < RADIX; d += kRsThreads) h[d] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+#pragma unroll 4
+    for (int i = 0; i < kRsItems; ++i) {
+        const int64_t k = t0 + (int64_t)i * kRsThreads + threadIdx.x;
+        if (k < n) atomicAdd(&h[(__ldg(keys + k) >> shift) & (RADIX - 1)], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < RADIX; d += kRsThreads) counts[(int64_t)d * ntiles + blockIdx.x] = h[d];
+}
+
+// Stable scatter of one tile.  Item order inside the tile is round-major
+// (item i*256 + t belongs to thread t in round i); an item's rank among equal
+// digits = earlier rounds + earlier warps of its round + lower lanes of its warp.
+// The tile is staged in shared memory in digit order, then written out so that
+// consecutive items of a digit run go to consecutive global addresses.
+template <int BITS>
+__global__ void __launch_bounds__(kRsThreads) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
+                                                                const uint32_t* __restrict__ vals_in, int64_t n,
+                                                                int shift, const uint32_t* __restrict__ offsets,
+                                                                int64_t ntiles, uint32_t* keys_out,
+                                                                uint32_t* vals_out) {
+    constexpr int RADIX = 1 << BITS;
+    constexpr int DPT = RADIX / kRsThreads;  // digits owned per thread
+    constexpr int DPL = RADIX / 32;          // digits per lane in the tile scan
+    extern __shared__ uint32_t rs_smem[];  // rs_smem_bytes<BITS>() of dynamic shared memory
+    uint32_t* s_keys = rs_smem;                                      // [kRsTile]
+    uint32_t* s_vals = s_keys + kRsTile;                             // [kRsTile]
+    uint32_t(*s_cnt)[RADIX] = reinterpret_cast<uint32_t(*)[RADIX]>(s_vals + kRsTile);  // [kRsWarps][RADIX]
+    uint32_t* s_run = s_vals + kRsTile + kRsWarps * RADIX;  // tile histogram, then items placed so far
+    uint32_t* s_start = s_run + RADIX;                      // tile-local start of each digit run
+    uint32_t* s_goff = s_start + RADIX;                     // global start of this tile's digit run
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+    const int nt = (int)((n - t0) < (int64_t)kRsTile ? (n - t0) : (int64_t)kRsTile);
+
+    uint32_t k[kRsItems], v[kRsItems];
+#pragma unroll
+    for (int i = 0; i < kRsItems; ++i) {
+        const int64_t g = t0 + (int64_t)i * kRsThreads + t;
+        const bool ok = g < n;
+        k[i] = ok ? __ldg(keys_in + g) : 0xffffffffu;
+        v[i] = ok ? (vals_in ? __ldg(vals_in + g) : (uint32_t)g) : 0u;
+    }
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) {
+        const int d = t + j * kRsThreads;
+#pragma unroll
+        for (int w = 0; w < kRsWarps; ++w) s_cnt[w][d] = 0;
+        s_run[d] = 0;
+        s_goff[d] = offsets[(int64_t)d * ntiles + blockIdx.x];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kRsItems; ++i)
+        if (i * kRsThreads + t < nt) atomicAdd(&s_run[(k[i] >> shift) & (RADIX - 1)], 1u);
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the tile histogram, DPL digits per lane
+        uint32_t c[DPL], sum = 0;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) {
+            c[j] = s_run[lane * DPL + j];
+            sum += c[j];
+        }
+        uint32_t incl = sum;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        uint32_t acc = incl - sum;
+#pragma unroll
+        for (int j = 0; j < DPL; ++j) {
+            s_start[lane * DPL + j] = acc;
+            acc += c[j];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < DPT; ++j) s_run[t + j * kRsThreads] = 0;
+    __syncthreads();
+    // stable ranking, one round (256 items) at a time (unrolled: k[], v[] stay in registers)
+#pragma unroll
+    for (int i = 0; i < kRsItems; ++i) {
+        const bool ok = i * kRsThreads + t < nt;
+        const uint32_t d = (k[i] >> shift) & (RADIX - 1);
+        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : 0xffffffffu);
+        const uint32_t lt = peers & ((1u << lane) - 1u);
+        const uint32_t rank = __popc(lt);
+        if (ok && lt == 0) s_cnt[warp][d] = __popc(peers);
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < DPT; ++j) {  // thread t owns digits t + j*256: offsets over this round's warps
+            const int dd = t + j * kRsThreads;
+            uint32_t acc = s_run[dd];
+#pragma unroll
+            for (int w = 0; w < kRsWarps; ++w) {
+                const uint32_t c = s_cnt[w][dd];
+                s_cnt[w][dd] = acc;
+                acc += c;
+            }
+            s_run[dd] = acc;
+        }
+        __syncthreads();
+        if (ok) {
+            const uint32_t pos = s_start[d] + s_cnt[warp][d] + rank;
+            s_keys[pos] = k[i];
+            s_vals[pos] = v[i];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < DPT; ++j)
+#pragma unroll
+            for (int w = 0; w < kRsWarps; ++w) s_cnt[w][t + j * kRsThreads] = 0;
+        __syncthreads();
+    }
+    for (int j = t; j < nt; j += kRsThreads) {
+        const uint32_t key = s_keys[j];
+        const uint32_t d = (key >> shift) & (RADIX - 1);
+        const uint32_t pos = s_goff[d] + (uint32_t)j - s_start[d];
+        keys_out[pos] = key;
+        vals_out[pos] = s_vals[j];
     }
 }
 
-// ----------------------------------------------------------- launchers --
-template <int G, int NV, bool B>
-static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
-                            int num_sms, cudaStream_t st) {
-    static int occ = -1;
-    if (occ < 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, query_kernel<G, NV, B>, kThreads, 0) != cudaSuccess ||
-            occ < 1)
-            occ = 1;
-    }
-    const int64_t qpb = (int64_t)(kThreads / 32) * (32 / G);
-    int64_t grid = (n + qpb - 1) / qpb;
-    const int64_t cap = (int64_t)num_sms * occ;
-    if (grid > cap) grid = cap;
-    if (grid < 1) grid = 1;
-    query_kernel<G, NV, B><<<(unsigned)grid, kThreads, 0, st>>>(p, q, idx, n, out);
+int64_t scan_blocks(int64_t nb) { return (nb + kScanTile - 1) / kScanTile; }
+int64_t radix_tiles(int64_t n) { return (n + kRsTile - 1) / kRsTile; }
+
+static cudaError_t scan_exclusive(uint32_t* a, int64_t nb, uint32_t* bsum, cudaStream_t st) {
+    const int64_t nblk = scan_blocks(nb);
+    scan_reduce_kernel<<<(unsigned)nblk, kScanThreads, 0, st>>>(a, nb, bsum);
+    scan_bsum_kernel<<<1, kScanThreads, 0, st>>>(bsum, nblk);
+    scan_apply_kernel<<<(unsigned)nblk, kScanThreads, 0, st>>>(a, nb, bsum);
     return cudaGetLastError();
 }
 
-template <int G, bool B>
-static cudaError_t dispatch_nv(int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
-                               float* out, int num_sms, cudaStream_t st) {
-    switch (NV) {
-        case 1: return launch_q<G, 1, B>(p, q, idx, n, out, num_sms, st);
-        case 2: return launch_q<G, 2, B>(p, q, idx, n, out, num_sms, st);
-        case 3: return launch_q<G, 3, B>(p, q, idx, n, out, num_sms, st);
-        case 4: return launch_q<G, 4, B>(p, q, idx, n, out, num_sms, st);
-        case 8: return launch_q<G, 8, B>(p, q, idx, n, out, num_sms, st);
-        default: return cudaErrorInvalidValue;
-    }
+template <int BITS>
+constexpr size_t rs_smem_bytes() {
+    return sizeof(uint32_t) * (2 * kRsTile + (kRsWarps + 3) * (1 << BITS));
 }
 
-template <bool B>
-static cudaError_t dispatch_g(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
-                              float* out, int num_sms, cudaStream_t st) {
-    switch (G) {
-        case 1: return dispatch_nv<1, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 2: return dispatch_nv<2, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 4: return dispatch_nv<4, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 8: return dispatch_nv<8, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 16: return dispatch_nv<16, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 32: return dispatch_nv<32, B>(NV, p, q, idx, n, out, num_sms, st);
-        default: return cudaErrorInvalidValue;
-    }
+template <int BITS>
+static void radix_pass(const uint32_t* kin, const uint32_t* vin, int64_t n, int shift, BinScratch& sc, int64_t ntiles,
+                       uint32_t* kout, uint32_t* vout, cudaStream_t st) {
+    rs_hist_kernel<BITS><<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, n, shift, sc.counts, ntiles);
+    scan_exclusive(sc.counts, ntiles << BITS, sc.bsum, st);
+    cudaFuncSetAttribute(rs_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)rs_smem_bytes<BITS>());
+    rs_scatter_kernel<BITS><<<(unsigned)ntiles, kRsThreads, rs_smem_bytes<BITS>(), st>>>(kin, vin, n, shift,
+                                                                                         sc.counts, ntiles, kout, vout);
 }
 
-bool lanes_supported(int G, int NV) {
-    const bool g = (G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32);
-    const bool v = (NV == 1 || NV == 2 || NV == 3 || NV == 4 || NV == 8);
-    return g && v;
+int64_t bin_key_space(int64_t P, int* half) {
+    // half-cell keys (4 per cell) when they fit in 32 bits, else cell keys
+    *half = (4 * P + 1 < (int64_t)0xffffffffLL) ? 1 : 0;
+    return (*half ? 4 * P : P) + 1;
 }
 
-cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,
-                         float* out, int num_sms, cudaStream_t st) {
-    if (idx) return dispatch_g<true>(G, NV, p, q, idx, n, out, num_sms, st);
-    return dispatch_g<false>(G, NV, p, q, idx, n, out, num_sms, st);
-}
-
-int64_t scan_blocks(int64_t nbins) { return (nbins + kScanTile - 1) / kScanTile; }
-
-cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, uint32_t* keys, uint32_t* hist,
-                           int64_t nbins, uint32_t* bsum, pndf_query* binned, uint32_t* idx, int num_sms,
-                           cudaStream_t st, int* launches) {
-    cudaError_t e = cudaMemsetAsync(hist, 0, sizeof(uint32_t) * (size_t)nbins, st);
-    if (e != cudaSuccess) return e;
-    const int eg = num_sms * 8;
+cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int64_t P, BinScratch& sc,
+                           int num_sms, cudaStream_t st, int* launches, const uint32_t** perm) {
+    int half;
+    const int64_t nkeys = bin_key_space(P, &half);
+    int kbits = 1;
+    while (kbits < 32 && ((int64_t)1 << kbits) < nkeys) ++kbits;
+    // <= 24 bits: 8-bit digits; <= 27: 9-bit digits (3 passes); else 8-bit digits (4 passes)
+    const int bits = (kbits > 24 && kbits <= 27) ? 9 : 8;
+    const int passes = (kbits + bits - 1) / bits;
+    const int64_t ntiles = radix_tiles(n);
     int64_t g = (n + 255) / 256;
-    if (g > eg) g = eg;
+    if (g > (int64_t)num_sms * 8) g = (int64_t)num_sms * 8;
     if (g < 1) g = 1;
-    bin_keys_kernel<<<(unsigned)g, 256, 0, st>>>(p, q, n, keys, hist, (uint32_t)(nbins - 1));
-    const int64_t nblk = scan_blocks(nbins);
-    scan_reduce_kernel<<<(unsigned)nblk, kScanThreads, 0, st>>>(hist, nbins, bsum);
-    scan_bsum_kernel<<<1, kScanThreads, 0, st>>>(bsum, nblk);
-    scan_apply_kernel<<<(unsigned)nblk, kScanThreads, 0, st>>>(hist, nbins, bsum);
-    bin_scatter_kernel<<<(unsigned)g, 256, 0, st>>>(q, keys, n, hist, binned, idx);
-    *launches += 5;
+    bin_keys_kernel<<<(unsigned)g, 256, 0, st>>>(p, q, n, sc.keys[0], (uint32_t)(nkeys - 1), half);
+    *launches += 1;
+    int cur = 0;
+    const uint32_t* vals = nullptr;  // pass 0: identity permutation
+    for (int ps = 0; ps < passes; ++ps) {
+        if (bits == 9)
+            radix_pass<9>(sc.keys[cur], vals, n, 9 * ps, sc, ntiles, sc.keys[cur ^ 1], sc.vals[cur ^ 1], st);
+        else
+            radix_pass<8>(sc.keys[cur], vals, n, 8 * ps, sc, ntiles, sc.keys[cur ^ 1], sc.vals[cur ^ 1], st);
+        vals = sc.vals[cur ^ 1];
+        cur ^= 1;
+        *launches += 5;
+    }
+    *perm = vals;
     return cudaGetLastError();
 }
 

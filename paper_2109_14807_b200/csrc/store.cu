@@ -50,18 +50,13 @@ int ilog2(int64_t x) {
 }
 
 // Binning scratch for one in-flight batch.
-struct Scratch {
-    uint32_t* keys = nullptr;
-    uint32_t* idx = nullptr;
-    pndf_query* binned = nullptr;
-    uint32_t* hist = nullptr;
-    uint32_t* bsum = nullptr;
-    int64_t cap = 0;
+struct Scratch : BinScratch {
     void release() {
-        cudaFree(keys);
-        cudaFree(idx);
-        cudaFree(binned);
-        cudaFree(hist);
+        for (int i = 0; i < 2; ++i) {
+            cudaFree(keys[i]);
+            cudaFree(vals[i]);
+        }
+        cudaFree(counts);
         cudaFree(bsum);
         *this = Scratch();
     }
@@ -119,6 +114,12 @@ pndf_status validate_desc(const pndf_desc* d) {
     if (d->num_levels < 2 || d->num_levels > maxL || d->num_levels > kMaxLevels) return PNDF_EINVAL;
     if (d->ang_res < 1 || d->ang_res > 256) return PNDF_EINVAL;
     if (d->rank < 1 || d->rank > 1024) return PNDF_EINVAL;
+    {  // positional rows are addressed with int32 indices
+        const int64_t n0 = d->map_size / d->base_stride;
+        int64_t P = 0;
+        for (int l = 0; l < d->num_levels; ++l) P += (n0 >> l) * (n0 >> l);
+        if (P >= (int64_t(1) << 31)) return PNDF_EINVAL;
+    }
     if (d->flags != PNDF_WRAP && d->flags != PNDF_CLAMP) return PNDF_EINVAL;
     return PNDF_OK;
 }
@@ -134,17 +135,19 @@ void choose_lanes(int R, int* G, int* NV) {
     *NV = nv;
 }
 
-pndf_status ensure_scratch(Scratch& s, int64_t n, int64_t nbins, cudaStream_t st) {
-    if (s.cap >= n && s.hist) return PNDF_OK;
+pndf_status ensure_scratch(Scratch& s, int64_t n, cudaStream_t st) {
+    if (s.cap >= n && s.counts) return PNDF_OK;
     cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
     if (st && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
         return PNDF_EINVAL;  // no allocation while a CUDA graph is being captured
     s.release();
-    CK(cudaMalloc(&s.keys, sizeof(uint32_t) * n));
-    CK(cudaMalloc(&s.idx, sizeof(uint32_t) * n));
-    CK(cudaMalloc(&s.binned, sizeof(pndf_query) * n));
-    CK(cudaMalloc(&s.hist, sizeof(uint32_t) * nbins));
-    CK(cudaMalloc(&s.bsum, sizeof(uint32_t) * scan_blocks(nbins)));
+    const int64_t nb = radix_tiles(n) * 512;
+    for (int i = 0; i < 2; ++i) {
+        CK(cudaMalloc(&s.keys[i], sizeof(uint32_t) * n));
+        CK(cudaMalloc(&s.vals[i], sizeof(uint32_t) * n));
+    }
+    CK(cudaMalloc(&s.counts, sizeof(uint32_t) * nb));
+    CK(cudaMalloc(&s.bsum, sizeof(uint32_t) * scan_blocks(nb)));
     s.cap = n;
     return PNDF_OK;
 }
@@ -152,9 +155,10 @@ pndf_status ensure_scratch(Scratch& s, int64_t n, int64_t nbins, cudaStream_t st
 bool want_bins(const pndf_store_s* s, int64_t n, uint32_t opts) {
     if (s->nbins == 0 || (opts & PNDF_BIN_OFF)) return false;
     if (opts & PNDF_BIN_ON) return true;
-    // AUTO: the factor set does not stay in L2, and the batch is large enough
-    // for rows to be shared between queries.
-    return (int64_t)s->stats.zc_bytes > s->l2_bytes / 2 && n >= (int64_t(1) << 16);
+    // AUTO: the factor set does not stay in L2, and the batch reuses rows enough
+    // (>= 8 queries per positional row) for the sort to pay for itself (measured
+    // on B200: config 4, 18 queries/row, gains 11%; config 3, 1.8/row, loses 40%).
+    return (int64_t)s->stats.zc_bytes > s->l2_bytes / 2 && n >= 8 * s->P;
 }
 
 // Enqueue one batch (device records) on st using scratch sc.
@@ -166,20 +170,20 @@ pndf_status enqueue(pndf_store_s* s, Scratch& sc, const pndf_query* q, int64_t n
     if ((opts & PNDF_BIN_ON) && s->nbins == 0) return PNDF_EINVAL;
     int launches = 0;
     if (timing) CK(cudaEventRecord(s->ev[0], st));
-    // sub-batches keep indices in uint32 when binning
-    const int64_t step = binned ? (int64_t(1) << 31) : n;
+    // sub-batches keep per-query indices in int32 (kernel descriptors, binning permutation)
+    const int64_t step = int64_t(1) << 30;
     if (binned) {
-        pndf_status r = ensure_scratch(sc, std::min(n, step), s->nbins, st);
+        pndf_status r = ensure_scratch(sc, std::min(n, step), st);
         if (r != PNDF_OK) return r;
     }
     bool first = true;
     for (int64_t a = 0; a < n; a += step) {
         const int64_t m = std::min(step, n - a);
         if (binned) {
-            CK(launch_binning(p, q + a, m, sc.keys, sc.hist, s->nbins, sc.bsum, sc.binned, sc.idx, s->num_sms, st,
-                              &launches));
+            const uint32_t* perm = nullptr;
+            CK(launch_binning(p, q + a, m, s->P, sc, s->num_sms, st, &launches, &perm));
             if (timing && first) CK(cudaEventRecord(s->ev[1], st));
-            CK(launch_query(p, s->G, s->NV, sc.binned, sc.idx, m, out + a, s->num_sms, st));
+            CK(launch_query(p, s->G, s->NV, q + a, perm, m, out + a, s->num_sms, st));
         } else {
             if (timing && first) CK(cudaEventRecord(s->ev[1], st));
             CK(launch_query(p, s->G, s->NV, q + a, nullptr, m, out + a, s->num_sms, st));
@@ -268,8 +272,8 @@ pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float
     s->num_sms = v > 0 ? v : 148;
     cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device);
     s->l2_bytes = v;
-    // binning keys are uint32 level offsets + 16-bit Morton coordinates
-    s->nbins = (s->P + 1 < (int64_t)0xffffffffLL && n0 <= 65536) ? s->P + 1 : 0;
+    // binning keys are uint32 (level offset + Morton code of the cell or half cell)
+    s->nbins = (s->P + 1 < (int64_t)0xffffffffLL) ? s->P + 1 : 0;
 
     auto fail = [&](pndf_status e) {
         destroy(s);
@@ -448,7 +452,7 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
             sl.cap = chunk;
         }
         if (binned) {
-            pndf_status r = ensure_scratch(sl.scratch, chunk, s->nbins, sl.st);
+            pndf_status r = ensure_scratch(sl.scratch, chunk, sl.st);
             if (r != PNDF_OK) return r;
         }
     }

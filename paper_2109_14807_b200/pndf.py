@@ -15,7 +15,7 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libpndf.so")
+LIB_PATH = os.environ.get("PNDF_LIB") or os.path.join(_PKG, "libpndf.so")  # PNDF_LIB: tuning variants
 
 ABI_VERSION = 1
 OK, EINVAL, ENOMEM, ECUDA, EFORMAT, EQUERY = 0, -1, -2, -3, -4, -5

@@ -46,7 +46,8 @@ def run_gpu(desc_args: dict, f, recs: np.ndarray, opts: int = 0, lanes: int = 0)
     if lanes:
         st.set_lanes(lanes)
     q = torch_records(recs)
-    out = torch.empty(recs.shape[0], dtype=torch.float32, device="cuda")
+    # NaN-filled so a permutation that skips a query cannot pass off a stale value
+    out = torch.full((recs.shape[0],), float("nan"), dtype=torch.float32, device="cuda")
     st.query_batch(q, out, opts)
     status = st.sync(raise_on_query_error=False)
     res = out.cpu().numpy()
