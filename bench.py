@@ -48,6 +48,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled oracle check of the timed batch")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="target CPU work of the oracle sample")
     return ap.parse_args()
 
@@ -70,12 +71,52 @@ def measured_peaks():
 
 
 def ncu_traffic(cfg_idx: int):
-    """dram bytes per query-kernel launch from the committed ncu --set full summary, if any."""
+    """DRAM bytes per query of the query kernel from the committed ncu --set full summary, if any
+    (profiles/ncu_traffic.json, written from a capture of the same launch configuration)."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     d = json.load(open(p))
     return d.get(f"config{cfg_idx}")
+
+
+def l2_read_gbs():
+    """Measured L2-resident read bandwidth of this GPU (tools/membw.cu, float4 loads, 48 MB set)."""
+    import ctypes
+    src = os.path.join(ROOT, "tools", "membw.cu")
+    so = os.path.join(ROOT, "tools", "libmembw.so")
+    try:
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(src):
+            subprocess.check_call(["nvcc", "-shared", "-Xcompiler", "-fPIC", "-gencode",
+                                   "arch=compute_100a,code=sm_100a", "-O3", "-o", so, src])
+        lib = ctypes.CDLL(so)
+        lib.membw_l2_read_gbs.restype = ctypes.c_double
+        lib.membw_l2_read_gbs.argtypes = [ctypes.c_int]
+        v = lib.membw_l2_read_gbs(48)
+        return v if v > 0 else None
+    except Exception:
+        return None
+
+
+def parity_sample(cfg, f, h_q, d_out, k=4096, seed=7):
+    """Check k sampled outputs of the timed batch against the fp64 oracle (BJ tolerance)."""
+    import oracle
+    import torch
+    n = d_out.shape[0]
+    rng = np.random.default_rng(seed)
+    idx = np.unique(rng.integers(0, n, min(k, n)))
+    recs = np.ascontiguousarray(h_q[torch.from_numpy(idx)].numpy()).view(synth.QREC).reshape(-1)
+    got = d_out[torch.from_numpy(idx).to(d_out.device)].cpu().numpy().astype(np.float64)
+    d = oracle.desc_of(cfg)
+    rows, _ = oracle.neighbours(d, recs)
+    Zs, zmap = oracle.sparse_z(rows, cfg.P, lambda u: z_rows_for(cfg, f, u))
+    ref = oracle.query_batch(d, f.C, f.X, f.Y, Zs, recs, mean=True, zmap=zmap)
+    err = np.abs(got - ref)
+    ok = (err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)
+    nz = np.abs(ref) > 1e-6
+    return {"checked": int(idx.shape[0]), "pass": bool(ok.all()), "max_abs_err": float(err.max()),
+            "max_rel_err_nonzero": float((err[nz] / np.abs(ref[nz])).max()) if nz.any() else 0.0,
+            "tolerance": "1e-4 rel or 1e-7 abs (BASELINE.json north_star)"}
 
 
 class ClockSampler:
@@ -225,11 +266,12 @@ def run_ours(args, cfg, rank, world, local_rank):
     import torch
     import torch.distributed as dist
     from paper_2109_14807_b200 import pndf
+    from paper_2109_14807_b200.shard import reduce_times_and_checksum, shard_range
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     n_total = args.queries or cfg.n_queries
-    i0, i1 = rank * n_total // world, (rank + 1) * n_total // world
+    i0, i1 = shard_range(n_total, rank, world)
     n = i1 - i0
 
     # ---- store (untimed): map on host, exact-rank Z built on this GPU (synth CUDA twin)
@@ -239,7 +281,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         Z = synth.build_z_exact_cuda(cfg, f.info["atom_map"], local_rank)
     else:
         Z = f.Z
-    desc = pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap)
+    prefix = {"auto": pndf.PREFIX_AUTO, "hilo": pndf.PREFIX_HILO, "u32": pndf.PREFIX_U32}[
+        os.environ.get("PNDF_PREFIX", "auto")]  # SAT storage format (experiments); AUTO by default
+    desc = pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap, prefix=prefix)
     store = pndf.load_factors(desc, f.C, f.X, f.Y, Z, device=local_rank)
     del Z
     torch.cuda.empty_cache()
@@ -253,6 +297,8 @@ def run_ours(args, cfg, rank, world, local_rank):
     d_out = torch.empty(n, dtype=torch.float32, device=dev)
     opts = {"auto": pndf.BIN_AUTO, "on": pndf.BIN_ON, "off": pndf.BIN_OFF}[args.bin]
     setup_s = time.perf_counter() - t_setup
+
+    l2_gbs = l2_read_gbs() if rank == 0 else None
 
     # ---- warm-up
     for _ in range(args.warmup):
@@ -284,16 +330,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     b_ms = st["bin_ms"] / max(1, st["timed_batches"])
 
     checksum = float(d_out.double().sum().item())
-    t = torch.tensor([ms_rank, q_ms, b_ms, checksum], dtype=torch.float64, device=dev)
-    if world > 1:
-        tmax = t[:3].clone()
-        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
-        tsum = t[3:].clone()
-        dist.all_reduce(tsum, op=dist.ReduceOp.SUM)
-        ms_step, q_ms_max, b_ms_max = tmax.tolist()
-        checksum = tsum.item()
-    else:
-        ms_step, q_ms_max, b_ms_max = ms_rank, q_ms, b_ms
+    (ms_step, q_ms_max, b_ms_max), checksum = reduce_times_and_checksum([ms_rank, q_ms, b_ms], checksum, dev)
     value = n_total / (ms_step * 1e-3)
 
     # ---- end to end through the public API with HOST buffers (H2D + kernels + D2H inside)
@@ -309,10 +346,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             t0 = time.perf_counter()
             store.query_batch_host(h_q, h_out, opts)
             times.append(time.perf_counter() - t0)
-        te = torch.tensor([float(np.mean(times))], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": n_total / te.item(), "unit": UNIT, "h2d_bytes_per_step": int(h_q.numel() * 4),
+        (te,), _ = reduce_times_and_checksum([float(np.mean(times))], 0.0, dev)
+        e2e = {"value": n_total / te, "unit": UNIT, "h2d_bytes_per_step": int(h_q.numel() * 4),
                "d2h_bytes_per_step": int(h_out.numel() * 4),
                "bitwise_equal_to_device_path": bool(torch.equal(h_out.to(dev), d_out))}
 
@@ -322,17 +357,24 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     peaks, peak_src = measured_peaks()
     Bq = bytes_per_query(cfg.R)
-    achieved = Bq * n / (q_ms * 1e-3) / 1e9  # GB/s of the query kernel on rank 0
-    traffic = ncu_traffic(cfg.idx)
+    achieved = Bq * n / (q_ms * 1e-3) / 1e9  # algorithmic GB/s of the query kernel on rank 0
+    tr = ncu_traffic(cfg.idx)
+    traffic = None if tr is None else int(tr["dram_bytes_per_query"] * n)
     roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
             "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
             "kernel": "pndf::query_kernel", "kernel_ms": q_ms, "bytes_per_query": Bq,
-            "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs, copy benchmark)"
+            "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs, copy benchmark, burst)"
             if peak_src == "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)",
+            "l2_peak_gbs_measured": l2_gbs, "frac_of_l2": (achieved / l2_gbs) if l2_gbs else None,
+            "traffic_source": None if tr is None else tr.get("source"),
+            "note": "achieved counts the method's bytes (8 Zc + 4 prefix rows of R fp32 + record + result "
+                    "per query); binned queries reuse Zc rows from registers/L1/L2, so DRAM traffic is far "
+                    "below it and frac > 1 vs HBM; frac_of_l2 is against this run's measured L2 read BW",
             "binning_ms": b_ms, "query_share_of_step": q_ms / ms_rank if ms_rank else None}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, f, bins, i0, args.cpu_seconds)
+    parity = parity_sample(cfg, f, h_q, d_out) if not args.no_parity else None
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -340,10 +382,12 @@ def run_ours(args, cfg, rank, world, local_rank):
                        "parallelism": f"query-sharded x{world}, factors replicated",
                        "binning": args.bin, "binned": bool(st["last_binned"]),
                        "lanes_per_query": st["lanes_per_query"], "rank_padded": st["rank_padded"],
+                       "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]],
                        "l2": "inputs larger than L2 (Zc %.1f GB, records %.1f GB vs 126 MB L2); no flush" % (
                            st["zc_bytes"] / 1e9, n * 16 / 1e9),
                        "setup_s": round(setup_s, 1)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "parity_sample": parity,
             "clocks": clk, "checksum": checksum}
     print(json.dumps(line), flush=True)
     store.free()

@@ -42,9 +42,13 @@ typedef enum {
     PNDF_EQUERY = -5   /* sticky, device-side: >= 1 record of a batch was invalid (its result is NaN) */
 } pndf_status;
 
-/* descriptor flags */
-#define PNDF_CLAMP 0u /* neighbours clamp to the grid edge (non-tileable map) */
-#define PNDF_WRAP 1u  /* neighbours wrap modulo the level grid (tileable map) */
+/* descriptor flags: border mode | SAT storage format */
+#define PNDF_CLAMP 0u       /* neighbours clamp to the grid edge (non-tileable map) */
+#define PNDF_WRAP 1u        /* neighbours wrap modulo the level grid (tileable map) */
+#define PNDF_PREFIX_AUTO 0u /* U32 when it keeps every nonzero range sum within 2^-15 relative, else HILO */
+#define PNDF_PREFIX_HILO 2u /* fp32 (hi, lo) pair of the fp64 prefix: 8 B/entry, ~1 ulp for any store */
+#define PNDF_PREFIX_U32 4u  /* uint32 fixed point, per-rank power-of-two scale: 4 B/entry */
+#define PNDF_PREFIX_MASK 6u
 
 /* pndf_query_batch opts (OR together) */
 #define PNDF_MEAN 0u      /* Eq. 6 average over the rectangle (default) */
@@ -67,7 +71,7 @@ typedef struct {
     int32_t num_levels;   /* L, 2 <= L <= log2(N/s0) + 1, L <= 24                */
     int32_t ang_res;      /* A, 1 <= A <= 256 (rect bounds are 8-bit)            */
     int32_t rank;         /* R, 1 <= R <= 1024                                   */
-    uint32_t flags;       /* PNDF_WRAP or PNDF_CLAMP                             */
+    uint32_t flags;       /* PNDF_WRAP or PNDF_CLAMP, | PNDF_PREFIX_*            */
 } pndf_desc;
 
 /* One query record, 16 bytes, little-endian.
@@ -85,9 +89,11 @@ typedef struct {
 /* Build a device store from raw CP factors (Eq. 5), synchronously.
  *   C [R] (NULL = all ones), X [A][R], Y [A][R]  -- host or device memory, fp32
  *   Z [P][R] level-major, rows j*n_l + i         -- host or device memory, fp32
- * Layout in HBM: Zc[P][Rp] = fl32(C_r Z_r(z)) with R padded to Rp
- * (zero ranks, rows 16-byte aligned); PX, PY [(A+1)][hi|lo][Rp] prefix sums
- * accumulated in fp64 and stored as an fp32 (hi, lo) pair.
+ * Layout in HBM: Zc[P][Rp] = fl32(M_r Z_r(z)) with R padded to Rp
+ * (zero ranks, rows 16-byte aligned); prefix sums of X, Y accumulated in fp64 and
+ * stored either as an fp32 (hi, lo) pair [2][(A+1)][2][Rp] (HILO, M_r = C_r) or as
+ * uint32 fixed point [2][(A+1)][Rp] with per-rank scale 2^e_r folded into
+ * M_r = C_r 2^-(ex_r + ey_r) (U32); see the PNDF_PREFIX_* flags.
  * Every factor must be finite and >= 0 (nonnegative store), else PNDF_EINVAL.
  * Inputs are copied: the caller may free them on return.  device = CUDA
  * ordinal; cuda_stream = cudaStream_t used for the build (NULL = default). */
@@ -133,14 +139,14 @@ typedef struct {
     double query_ms;          /* summed query-kernel time of those batches      */
     double bin_ms;            /* summed binning time of those batches           */
     int32_t last_binned;      /* 1 if the last batch was binned                 */
-    int32_t reserved;
+    int32_t prefix_format;    /* 0 = HILO, 1 = U32                              */
 } pndf_store_stats;
 pndf_status pndf_store_stats_get(pndf_store s, pndf_store_stats* out);
 pndf_status pndf_store_stats_reset(pndf_store s);
 
-/* Copy the device store image to host memory (tests): PXY = [2][(A+1)][2][Rp]
- * fp32 (table X then Y; hi then lo), Zc rows [z0, z1) as [z1-z0][Rp] fp32.
- * Either pointer may be NULL. */
+/* Copy the device store image to host memory (tests): PXY = prefix_bytes of the
+ * SAT tables (HILO [2][(A+1)][2][Rp] fp32, or U32 [2][(A+1)][Rp] uint32), Zc rows
+ * [z0, z1) as [z1-z0][Rp] fp32.  Either pointer may be NULL. */
 pndf_status pndf_store_image(pndf_store s, float* PXY, float* Zc, int64_t z0, int64_t z1);
 
 /* Tuning knob (bench / tests): lanes per query G in {1,2,4,8,16,32} with

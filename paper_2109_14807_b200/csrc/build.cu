@@ -1,11 +1,17 @@
 // build.cu -- store build kernels (once per store, untimed).
 //
-//   fold_rows_kernel  Zc[z][r] = fl32(C_r * Z_r(z)) for r < R, 0 for R <= r < Rp;
-//                     flags any negative or non-finite factor (nonnegative store).
-//   prefix_kernel     1-D SATs of the angular factors ("a 1D SAT for each
-//                     1D vector"): S_k = sum_{i<k} X_r(i) accumulated in fp64 in
-//                     index order, stored as hi = fl32(S_k), lo = fl32(S_k - hi).
+// The 1-D SATs of the angular factors ("a 1D SAT for each 1D vector ...
+// gives exact results"): S_k = sum_{i<k} X_r(i) accumulated in fp64 in index
+// order, stored in one of two formats (chosen per store):
+//   HILO  hi = fl32(S_k), lo = fl32(S_k - hi)     -- 8 B/entry, ~1 ulp for any store
+//   U32   q_k = round(S_k 2^e_r), uint32 fixed point with a per-rank power-of-two
+//         scale e_r (the largest with q_A < 2^32) -- 4 B/entry; differences are
+//         exact integers, so Xbar has error <= 2^-e_r; used only when that is
+//         <= 2^-15 of the smallest nonzero factor entry of every rank.
+// Zc[z][r] = fl32(M_r * Z_r(z)) with M_r = C_r (HILO) or C_r 2^-(ex_r+ey_r) (U32,
+// a power-of-two rescale that is exact unless it underflows -- flagged).
 #include <cuda_runtime.h>
+#include <float.h>
 #include <stdint.h>
 
 #include "launch.h"
@@ -14,10 +20,11 @@ namespace pndf {
 
 __device__ __forceinline__ bool bad_factor(float v) { return !(v >= 0.0f) || isinf(v); }
 
-__global__ void fold_rows_kernel(const float* Zsrc, int64_t rows, int R, const float* __restrict__ C,
-                                 float* Zc, int Rp, uint32_t* bad) {
+// flags: bit 0 = negative / non-finite factor, bit 1 = a nonzero product underflowed
+__global__ void fold_rows_kernel(const float* Zsrc, int64_t rows, int R, const float* __restrict__ M, float* Zc,
+                                 int Rp, uint32_t* flags) {
     const int64_t total = rows * (int64_t)Rp;
-    bool any_bad = false;
+    bool any_bad = false, any_uflow = false;
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
         const int64_t z = t / Rp;
         const int r = (int)(t - z * Rp);
@@ -25,55 +32,100 @@ __global__ void fold_rows_kernel(const float* Zsrc, int64_t rows, int R, const f
         if (r < R) {
             const float zr = Zsrc[z * R + r];
             any_bad |= bad_factor(zr);
-            v = C ? C[r] * zr : zr;
+            v = M ? M[r] * zr : zr;
+            any_uflow |= (zr != 0.0f && M && M[r] != 0.0f && fabsf(v) < FLT_MIN);
         }
         Zc[t] = v;
     }
-    if (__any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicOr(bad, 1u);
+    if (__any_sync(0xffffffffu, any_bad) && (threadIdx.x & 31) == 0) atomicOr(flags, 1u);
+    if (__any_sync(0xffffffffu, any_uflow) && (threadIdx.x & 31) == 0) atomicOr(flags, 2u);
 }
 
-// One thread per (table, rank); A <= 256 so the sequential fp64 scan is short.
-__global__ void prefix_kernel(const float* __restrict__ X, const float* __restrict__ Y, int A, int R, int Rp,
-                              float* PXY, uint32_t* bad) {
+// One thread per (table, rank): fp64 total and smallest nonzero entry.
+__global__ void prefix_stats_kernel(const float* __restrict__ X, const float* __restrict__ Y, int A, int R, int Rp,
+                                    double* total, float* minnz, uint32_t* flags) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * Rp) return;
+    const int table = t / Rp, r = t % Rp;
+    const float* F = table ? Y : X;
+    double S = 0.0;
+    float mn = FLT_MAX;
+    bool any_bad = false;
+    if (r < R)
+        for (int k = 0; k < A; ++k) {
+            const float v = F[(size_t)k * R + r];
+            any_bad |= bad_factor(v);
+            S += (double)v;
+            if (v > 0.0f && v < mn) mn = v;
+        }
+    total[t] = S;
+    minnz[t] = mn;
+    if (any_bad) atomicOr(flags, 1u);
+}
+
+// HILO: PXY[table][k][0|1][Rp]
+__global__ void prefix_hilo_kernel(const float* __restrict__ X, const float* __restrict__ Y, int A, int R, int Rp,
+                                   float* PXY) {
     const int t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= 2 * Rp) return;
     const int table = t / Rp, r = t % Rp;
     const float* F = table ? Y : X;
     float* out = PXY + (size_t)table * (A + 1) * 2 * Rp;
     double S = 0.0;
-    bool any_bad = false;
     for (int k = 0; k <= A; ++k) {
         const float hi = (float)S;
         const float lo = (float)(S - (double)hi);
         out[(size_t)(2 * k) * Rp + r] = hi;
         out[(size_t)(2 * k + 1) * Rp + r] = lo;
-        if (k < A && r < R) {
-            const float v = F[(size_t)k * R + r];
-            any_bad |= bad_factor(v);
-            S += (double)v;
-        }
+        if (k < A && r < R) S += (double)F[(size_t)k * R + r];
     }
-    if (any_bad) atomicOr(bad, 1u);
 }
 
-cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float* Cdev, float* Zc_dst, int Rp,
-                             uint32_t* bad, cudaStream_t st) {
+// U32: PQ[table][k][Rp], q_k = round(S_k 2^e)
+__global__ void prefix_u32_kernel(const float* __restrict__ X, const float* __restrict__ Y, int A, int R, int Rp,
+                                  const int* __restrict__ exps, uint32_t* PQ) {
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= 2 * Rp) return;
+    const int table = t / Rp, r = t % Rp;
+    const float* F = table ? Y : X;
+    uint32_t* out = PQ + (size_t)table * (A + 1) * Rp;
+    const int e = exps[t];
+    double S = 0.0;
+    for (int k = 0; k <= A; ++k) {
+        out[(size_t)k * Rp + r] = __double2uint_rn(ldexp(S, e));
+        if (k < A && r < R) S += (double)F[(size_t)k * R + r];
+    }
+}
+
+static int grid_for(int64_t total, int threads, int cap_blocks) {
+    int64_t g = (total + threads - 1) / threads;
+    if (g > cap_blocks) g = cap_blocks;
+    return g < 1 ? 1 : (int)g;
+}
+
+cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float* Mdev, float* Zc_dst, int Rp,
+                             uint32_t* flags, cudaStream_t st) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const int64_t total = rows * (int64_t)Rp;
-    int64_t g = (total + 255) / 256;
-    if (g > (int64_t)sms * 16) g = (int64_t)sms * 16;
-    if (g < 1) g = 1;
-    fold_rows_kernel<<<(unsigned)g, 256, 0, st>>>(Zsrc, rows, R, Cdev, Zc_dst, Rp, bad);
+    fold_rows_kernel<<<grid_for(rows * (int64_t)Rp, 256, sms * 16), 256, 0, st>>>(Zsrc, rows, R, Mdev, Zc_dst, Rp,
+                                                                                  flags);
     return cudaGetLastError();
 }
 
-cudaError_t launch_prefix(const float* Xdev, const float* Ydev, int A, int R, int Rp, float* PXY, uint32_t* bad,
-                          cudaStream_t st) {
-    const int threads = 128;
-    const int g = (2 * Rp + threads - 1) / threads;
-    prefix_kernel<<<g, threads, 0, st>>>(Xdev, Ydev, A, R, Rp, PXY, bad);
+cudaError_t launch_prefix_stats(const float* Xdev, const float* Ydev, int A, int R, int Rp, double* total,
+                                float* minnz, uint32_t* flags, cudaStream_t st) {
+    prefix_stats_kernel<<<grid_for(2 * Rp, 128, 1 << 20), 128, 0, st>>>(Xdev, Ydev, A, R, Rp, total, minnz, flags);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_prefix(const float* Xdev, const float* Ydev, int A, int R, int Rp, int u32, const int* exps,
+                          void* table, cudaStream_t st) {
+    if (u32)
+        prefix_u32_kernel<<<grid_for(2 * Rp, 128, 1 << 20), 128, 0, st>>>(Xdev, Ydev, A, R, Rp, exps,
+                                                                          (uint32_t*)table);
+    else
+        prefix_hilo_kernel<<<grid_for(2 * Rp, 128, 1 << 20), 128, 0, st>>>(Xdev, Ydev, A, R, Rp, (float*)table);
     return cudaGetLastError();
 }
 

@@ -1,11 +1,13 @@
 // internal.cuh -- device-side data structures shared by the pndf kernels.
 //
-// Store layout in HBM (DESIGN.md §5):
-//   Zc  [P][Rp]               fp32, Zc[z][r] = fl32(C_r * Z_r(z)), ranks >= R are 0,
-//                             rows 16-byte aligned (Rp % 4 == 0)
-//   PXY [2][A+1][2][Rp]       fp32, table 0 = X, 1 = Y; entry k holds the prefix
+// Store layout in HBM (DESIGN.md §4):
+//   Zc  [P][Rp]               fp32, Zc[z][r] = fl32(M_r * Z_r(z)), ranks >= R are 0,
+//                             rows 16-byte aligned (Rp % 4 == 0); M_r = C_r (HILO) or
+//                             C_r 2^-(ex_r+ey_r) (U32)
+//   PXY [2][A+1][2][Rp] fp32  HILO: table 0 = X, 1 = Y; entry k holds the prefix
 //                             sum_{i<k} X_r(i) accumulated in fp64 and split into
 //                             hi = fl32(S), lo = fl32(S - hi)  ("1D SAT")
+//   or  [2][A+1][Rp]   uint32 U32: round(S 2^e_r), see build.cu
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,6 +31,7 @@ struct QParams {
     int32_t A;                     // angular resolution
     int32_t Rp;                    // padded rank
     int32_t wrap;                  // 1 = periodic neighbours
+    int32_t prefix_u32;            // 1 = uint32 fixed-point SATs (PQ[2][A+1][Rp]), 0 = fp32 (hi, lo)
     float inv_s0;                  // 1/s0 (power of two, exact)
     uint32_t mean;                 // 1 = divide by the rectangle area
 };

@@ -24,10 +24,12 @@ int64_t radix_tiles(int64_t n);
 cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int64_t P, BinScratch& sc,
                            int num_sms, cudaStream_t st, int* launches, const uint32_t** perm);
 
-// Store build kernels (store.cu).
-cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float* Cdev, float* Zc_dst, int Rp,
-                             uint32_t* bad, cudaStream_t st);
-cudaError_t launch_prefix(const float* Xdev, const float* Ydev, int A, int R, int Rp, float* PXY, uint32_t* bad,
-                          cudaStream_t st);
+// Store build kernels (build.cu).
+cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float* Mdev, float* Zc_dst, int Rp,
+                             uint32_t* flags, cudaStream_t st);
+cudaError_t launch_prefix_stats(const float* Xdev, const float* Ydev, int A, int R, int Rp, double* total,
+                                float* minnz, uint32_t* flags, cudaStream_t st);
+cudaError_t launch_prefix(const float* Xdev, const float* Ydev, int A, int R, int Rp, int u32, const int* exps,
+                          void* table, cudaStream_t st);
 
 }  // namespace pndf

@@ -5,7 +5,7 @@
 //   a2  decode + level select  decode()
 //   a3  spatial neighbours     decode()
 //   a4  positional gather + interpolation  query_kernel: 8 rows of Zc, float4 per lane
-//   a5  angular prefix differencing        query_kernel: 4 prefix rows (hi,lo)
+//   a5  angular prefix differencing        query_kernel: 4 SAT rows, (hi,lo) fp32 or u32 fixed point
 //   a6  rank product + reduce + write      query_kernel: Eq. 6, xor-shuffle
 //                                          reduction over the G lanes of a query
 // This is a gather-and-reduce (~11 flop per rank per query), bound by the memory
@@ -174,7 +174,7 @@ constexpr int kWarpsPerBlock = kThreads / 32;
 #define PNDF_MINB 2  // min resident blocks per SM (tuned on B200: 2-3 beat 1, see profiles/)
 #endif
 
-template <int G, int NV, bool WRAP, bool BINNED>
+template <int G, int NV, bool WRAP, bool BINNED, bool U32>
 __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParams p, const pndf_query* __restrict__ q,
                                                          const uint32_t* __restrict__ idx, int64_t n,
                                                          int64_t chunk, float* __restrict__ out) {
@@ -185,8 +185,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
     const int gl = lane % G, grp = lane / G;
     QDesc* wd = sdesc[warp];
     const float* __restrict__ Zc = p.Zc;
+    // SAT rows: HILO = [hi row | lo row] per entry (stride 2*RP floats), U32 = one uint32 row
+    constexpr int PSTRIDE = U32 ? RP : 2 * RP;
     const float* __restrict__ PX = p.PXY;
-    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * 2 * RP;
+    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * PSTRIDE;
 
     const int64_t c0 = (int64_t)blockIdx.x * chunk;
     const int64_t c1 = min(n, c0 + chunk);
@@ -232,10 +234,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
             const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
                                 (int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
             const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
-            const float* px0 = PX + (size_t)(2 * (tail.x & 0xffffu)) * RP;
-            const float* px1 = PX + (size_t)(2 * (tail.x >> 16)) * RP;
-            const float* py0 = PY + (size_t)(2 * (tail.y & 0xffffu)) * RP;
-            const float* py1 = PY + (size_t)(2 * (tail.y >> 16)) * RP;
+            const float* px0 = PX + (size_t)(tail.x & 0xffffu) * PSTRIDE;
+            const float* px1 = PX + (size_t)(tail.x >> 16) * PSTRIDE;
+            const float* py0 = PY + (size_t)(tail.y & 0xffffu) * PSTRIDE;
+            const float* py1 = PY + (size_t)(tail.y >> 16) * PSTRIDE;
             bool reuse = false;
             if (G == 32) {  // warp-uniform: every lane reads the same descriptor
                 reuse = true;
@@ -254,10 +256,29 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const int c = (gl + v * G) * 4;
-                const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
-                const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
-                const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
-                const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
+                float4 dx, dy;
+                if (U32) {
+                    // exact integer differences of the fixed-point SATs (scale folded into Zc)
+                    const uint4 qx1 = __ldg(reinterpret_cast<const uint4*>(px1 + c));
+                    const uint4 qx0 = __ldg(reinterpret_cast<const uint4*>(px0 + c));
+                    const uint4 qy1 = __ldg(reinterpret_cast<const uint4*>(py1 + c));
+                    const uint4 qy0 = __ldg(reinterpret_cast<const uint4*>(py0 + c));
+                    dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                     __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                    dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                     __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                } else {
+                    // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
+                    // under cancellation (Sterbenz), lo carries the fp64 residual.
+                    const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
+                    const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
+                    const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
+                    const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
+                    dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                     (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                    dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                     (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                }
                 float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                 for (int k = 0; k < 8; ++k) {
@@ -266,16 +287,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                     z.z = fmaf(w[k], zc[v][k].z, z.z);
                     z.w = fmaf(w[k], zc[v][k].w, z.w);
                 }
-                // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
-                // under cancellation (Sterbenz), lo carries the fp64 residual.
-                const float dx0 = (xh1.x - xh0.x) + (xl1.x - xl0.x), dy0 = (yh1.x - yh0.x) + (yl1.x - yl0.x);
-                const float dx1 = (xh1.y - xh0.y) + (xl1.y - xl0.y), dy1 = (yh1.y - yh0.y) + (yl1.y - yl0.y);
-                const float dx2 = (xh1.z - xh0.z) + (xl1.z - xl0.z), dy2 = (yh1.z - yh0.z) + (yl1.z - yl0.z);
-                const float dx3 = (xh1.w - xh0.w) + (xl1.w - xl0.w), dy3 = (yh1.w - yh0.w) + (yl1.w - yl0.w);
-                part = fmaf(dx0 * dy0, z.x, part);
-                part = fmaf(dx1 * dy1, z.y, part);
-                part = fmaf(dx2 * dy2, z.z, part);
-                part = fmaf(dx3 * dy3, z.w, part);
+                part = fmaf(dx.x * dy.x, z.x, part);
+                part = fmaf(dx.y * dy.y, z.y, part);
+                part = fmaf(dx.z * dy.z, z.z, part);
+                part = fmaf(dx.w * dy.w, z.w, part);
             }
 #pragma unroll
             for (int o = G / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
@@ -292,12 +307,12 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 }
 
 // ----------------------------------------------------------- launchers --
-template <int G, int NV, bool W, bool B>
+template <int G, int NV, bool W, bool B, bool U>
 static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
                             int num_sms, cudaStream_t st) {
     static int occ = -1;
     if (occ < 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, query_kernel<G, NV, W, B>, kThreads, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, query_kernel<G, NV, W, B, U>, kThreads, 0) !=
                 cudaSuccess ||
             occ < 1)
             occ = 1;
@@ -309,33 +324,33 @@ static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_
     int64_t chunk = (n + grid - 1) / grid;
     chunk = (chunk + 31) / 32 * 32;
     grid = (n + chunk - 1) / chunk;
-    query_kernel<G, NV, W, B><<<(unsigned)grid, kThreads, 0, st>>>(p, q, idx, n, chunk, out);
+    query_kernel<G, NV, W, B, U><<<(unsigned)grid, kThreads, 0, st>>>(p, q, idx, n, chunk, out);
     return cudaGetLastError();
 }
 
-template <int G, bool W, bool B>
+template <int G, bool W, bool B, bool U>
 static cudaError_t dispatch_nv(int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
                                float* out, int num_sms, cudaStream_t st) {
     switch (NV) {
-        case 1: return launch_q<G, 1, W, B>(p, q, idx, n, out, num_sms, st);
-        case 2: return launch_q<G, 2, W, B>(p, q, idx, n, out, num_sms, st);
-        case 3: return launch_q<G, 3, W, B>(p, q, idx, n, out, num_sms, st);
-        case 4: return launch_q<G, 4, W, B>(p, q, idx, n, out, num_sms, st);
-        case 8: return launch_q<G, 8, W, B>(p, q, idx, n, out, num_sms, st);
+        case 1: return launch_q<G, 1, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 2: return launch_q<G, 2, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 3: return launch_q<G, 3, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 4: return launch_q<G, 4, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 8: return launch_q<G, 8, W, B, U>(p, q, idx, n, out, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
-template <bool W, bool B>
+template <bool W, bool B, bool U>
 static cudaError_t dispatch_g(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
                               float* out, int num_sms, cudaStream_t st) {
     switch (G) {
-        case 1: return dispatch_nv<1, W, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 2: return dispatch_nv<2, W, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 4: return dispatch_nv<4, W, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 8: return dispatch_nv<8, W, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 16: return dispatch_nv<16, W, B>(NV, p, q, idx, n, out, num_sms, st);
-        case 32: return dispatch_nv<32, W, B>(NV, p, q, idx, n, out, num_sms, st);
+        case 1: return dispatch_nv<1, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 2: return dispatch_nv<2, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 4: return dispatch_nv<4, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 8: return dispatch_nv<8, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 16: return dispatch_nv<16, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 32: return dispatch_nv<32, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
@@ -346,15 +361,22 @@ bool lanes_supported(int G, int NV) {
     return g && v;
 }
 
+template <bool U>
+static cudaError_t dispatch_wb(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
+                               float* out, int num_sms, cudaStream_t st) {
+    if (p.wrap) {
+        if (idx) return dispatch_g<true, true, U>(G, NV, p, q, idx, n, out, num_sms, st);
+        return dispatch_g<true, false, U>(G, NV, p, q, idx, n, out, num_sms, st);
+    }
+    if (idx) return dispatch_g<false, true, U>(G, NV, p, q, idx, n, out, num_sms, st);
+    return dispatch_g<false, false, U>(G, NV, p, q, idx, n, out, num_sms, st);
+}
+
 cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,
                          float* out, int num_sms, cudaStream_t st) {
     if (4 * G * NV != p.Rp) return cudaErrorInvalidValue;
-    if (p.wrap) {
-        if (idx) return dispatch_g<true, true>(G, NV, p, q, idx, n, out, num_sms, st);
-        return dispatch_g<true, false>(G, NV, p, q, idx, n, out, num_sms, st);
-    }
-    if (idx) return dispatch_g<false, true>(G, NV, p, q, idx, n, out, num_sms, st);
-    return dispatch_g<false, false>(G, NV, p, q, idx, n, out, num_sms, st);
+    if (p.prefix_u32) return dispatch_wb<true>(G, NV, p, q, idx, n, out, num_sms, st);
+    return dispatch_wb<false>(G, NV, p, q, idx, n, out, num_sms, st);
 }
 
 // ------------------------------------------------------------ binning --

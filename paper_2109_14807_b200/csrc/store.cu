@@ -7,6 +7,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <cmath>
+#include <vector>
 #include <mutex>
 #include <new>
 
@@ -120,7 +122,8 @@ pndf_status validate_desc(const pndf_desc* d) {
         for (int l = 0; l < d->num_levels; ++l) P += (n0 >> l) * (n0 >> l);
         if (P >= (int64_t(1) << 31)) return PNDF_EINVAL;
     }
-    if (d->flags != PNDF_WRAP && d->flags != PNDF_CLAMP) return PNDF_EINVAL;
+    if (d->flags & ~(PNDF_WRAP | PNDF_PREFIX_MASK)) return PNDF_EINVAL;
+    if ((d->flags & PNDF_PREFIX_MASK) == PNDF_PREFIX_MASK) return PNDF_EINVAL;
     return PNDF_OK;
 }
 
@@ -280,90 +283,136 @@ pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float
         return e;
     };
     const size_t zc_bytes = sizeof(float) * (size_t)s->P * Rp;
-    const size_t pxy_bytes = sizeof(float) * (size_t)2 * (A + 1) * 2 * Rp;
+    const size_t pxy_bytes_max = sizeof(float) * (size_t)2 * (A + 1) * 2 * Rp;  // HILO (U32 uses half)
     cudaError_t e;
     if ((e = cudaMalloc(&s->Zc, zc_bytes)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(Zc)"));
-    if ((e = cudaMalloc(&s->PXY, pxy_bytes)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(PXY)"));
+    if ((e = cudaMalloc(&s->PXY, pxy_bytes_max)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(PXY)"));
     if ((e = cudaMalloc(&s->err, 2 * sizeof(uint32_t))) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(err)"));
-    uint32_t* bad = s->err + 1;
+    uint32_t* flags = s->err + 1;  // bit 0: bad factor, bit 1: underflow of the U32 rescale
     cudaMemsetAsync(s->err, 0, 2 * sizeof(uint32_t), st);
     for (auto& ev : s->ev)
         if ((e = cudaEventCreate(&ev)) != cudaSuccess) return fail(cuda_fail(e, "cudaEventCreate"));
 
-    // small factors: C (or ones), X, Y -> device
-    float *dC = nullptr, *dXY = nullptr;
-    if ((e = cudaMalloc(&dC, sizeof(float) * Rp)) != cudaSuccess) return fail(cuda_fail(e, "cudaMalloc(C)"));
-    if ((e = cudaMalloc(&dXY, sizeof(float) * 2 * (size_t)A * R)) != cudaSuccess) {
-        cudaFree(dC);
-        return fail(cuda_fail(e, "cudaMalloc(XY)"));
-    }
+    // small factors: C (or ones), X, Y -> device; per-rank stats; multipliers; exponents
+    float *dC = nullptr, *dXY = nullptr, *dM = nullptr, *dmin = nullptr;
+    double* dtot = nullptr;
+    int* dexp = nullptr;
     auto free_small = [&]() {
         cudaFree(dC);
         cudaFree(dXY);
+        cudaFree(dM);
+        cudaFree(dmin);
+        cudaFree(dtot);
+        cudaFree(dexp);
     };
-    {
-        float* hC = new float[Rp];
-        for (int i = 0; i < Rp; ++i) hC[i] = i < R ? 1.0f : 0.0f;
-        e = cudaMemcpy(dC, hC, sizeof(float) * Rp, cudaMemcpyHostToDevice);
-        delete[] hC;
-        if (e == cudaSuccess && C) e = cudaMemcpy(dC, C, sizeof(float) * R, cudaMemcpyDefault);
-        if (e == cudaSuccess) e = cudaMemcpy(dXY, X, sizeof(float) * (size_t)A * R, cudaMemcpyDefault);
-        if (e == cudaSuccess) e = cudaMemcpy(dXY + (size_t)A * R, Y, sizeof(float) * (size_t)A * R, cudaMemcpyDefault);
-        if (e != cudaSuccess) {
-            free_small();
-            return fail(cuda_fail(e, "cudaMemcpy(C/X/Y)"));
-        }
-    }
-    // C is validated by folding it as a one-row "Z" against ones
-    if ((e = launch_prefix(dXY, dXY + (size_t)A * R, A, R, Rp, s->PXY, bad, st)) != cudaSuccess) {
+    auto fail_small = [&](cudaError_t ce, const char* what) {
         free_small();
-        return fail(cuda_fail(e, "prefix kernel"));
-    }
-    if ((e = launch_fold_rows(dC, 1, R, nullptr, dC, R, bad, st)) != cudaSuccess) {
-        free_small();
-        return fail(cuda_fail(e, "validate C"));
-    }
+        return fail(cuda_fail(ce, what));
+    };
+    if ((e = cudaMalloc(&dC, sizeof(float) * Rp)) != cudaSuccess) return fail_small(e, "cudaMalloc(C)");
+    if ((e = cudaMalloc(&dM, sizeof(float) * Rp)) != cudaSuccess) return fail_small(e, "cudaMalloc(M)");
+    if ((e = cudaMalloc(&dXY, sizeof(float) * 2 * (size_t)A * R)) != cudaSuccess) return fail_small(e, "cudaMalloc(XY)");
+    if ((e = cudaMalloc(&dtot, sizeof(double) * 2 * Rp)) != cudaSuccess) return fail_small(e, "cudaMalloc(tot)");
+    if ((e = cudaMalloc(&dmin, sizeof(float) * 2 * Rp)) != cudaSuccess) return fail_small(e, "cudaMalloc(min)");
+    if ((e = cudaMalloc(&dexp, sizeof(int) * 2 * Rp)) != cudaSuccess) return fail_small(e, "cudaMalloc(exp)");
+    std::vector<float> hC(Rp, 0.0f);
+    for (int i = 0; i < R; ++i) hC[i] = 1.0f;
+    if (C && (e = cudaMemcpy(hC.data(), C, sizeof(float) * R, cudaMemcpyDefault)) != cudaSuccess)
+        return fail_small(e, "cudaMemcpy(C)");
+    if ((e = cudaMemcpy(dC, hC.data(), sizeof(float) * Rp, cudaMemcpyHostToDevice)) != cudaSuccess)
+        return fail_small(e, "cudaMemcpy(C)");
+    if ((e = cudaMemcpy(dXY, X, sizeof(float) * (size_t)A * R, cudaMemcpyDefault)) != cudaSuccess)
+        return fail_small(e, "cudaMemcpy(X)");
+    if ((e = cudaMemcpy(dXY + (size_t)A * R, Y, sizeof(float) * (size_t)A * R, cudaMemcpyDefault)) != cudaSuccess)
+        return fail_small(e, "cudaMemcpy(Y)");
+    // validate C (fold it as a one-row "Z") and X, Y (stats kernel); gather totals / min nonzero
+    if ((e = launch_fold_rows(dC, 1, R, nullptr, dC, R, flags, st)) != cudaSuccess) return fail_small(e, "validate C");
+    if ((e = launch_prefix_stats(dXY, dXY + (size_t)A * R, A, R, Rp, dtot, dmin, flags, st)) != cudaSuccess)
+        return fail_small(e, "prefix stats");
     s->stats.kernel_launches += 2;
+    std::vector<double> htot(2 * Rp);
+    std::vector<float> hmin(2 * Rp);
+    uint32_t hflags = 0;
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_small(e, "store build");
+    cudaMemcpy(htot.data(), dtot, sizeof(double) * 2 * Rp, cudaMemcpyDeviceToHost);
+    cudaMemcpy(hmin.data(), dmin, sizeof(float) * 2 * Rp, cudaMemcpyDeviceToHost);
+    if ((e = cudaMemcpy(&hflags, flags, sizeof(uint32_t), cudaMemcpyDeviceToHost)) != cudaSuccess)
+        return fail_small(e, "store build");
+    if (hflags & 1u) {  // negative or non-finite C, X or Y
+        free_small();
+        return fail(PNDF_EINVAL);
+    }
+    // SAT format: U32 when every rank's fixed-point step 2^-e (~ total 2^-31) is <= 2^-15 of its
+    // smallest nonzero entry (so any nonzero range sum is within 2^-15 relative), else HILO.
+    const uint32_t pmode = desc->flags & PNDF_PREFIX_MASK;
+    std::vector<int> hexp(2 * Rp, 0);
+    bool u32_ok = true;
+    for (int t = 0; t < 2 * Rp; ++t) {
+        const double T = htot[t];
+        if (T <= 0.0) continue;
+        int ex = (int)std::floor(std::log2(4294967294.0 / T));
+        while (std::ldexp(T, ex) > 4294967294.0) --ex;
+        hexp[t] = ex;
+        if (std::ldexp(1.0, -ex) > std::ldexp((double)hmin[t], -15)) u32_ok = false;
+    }
+    bool use_u32 = (pmode == PNDF_PREFIX_U32) || (pmode == PNDF_PREFIX_AUTO && u32_ok);
 
-    // positional factors: Zc = fl32(C_r Z_r(z)), padded to Rp
+    // positional factors: Zc = fl32(M_r Z_r(z)), padded to Rp; U32 falls back to HILO on underflow
     cudaPointerAttributes pa;
     const bool z_dev = cudaPointerGetAttributes(&pa, Z) == cudaSuccess &&
                        (pa.type == cudaMemoryTypeDevice || pa.type == cudaMemoryTypeManaged);
     cudaGetLastError();
-    if (z_dev) {
-        if ((e = launch_fold_rows(Z, s->P, R, dC, s->Zc, Rp, bad, st)) != cudaSuccess) {
-            free_small();
-            return fail(cuda_fail(e, "fold kernel"));
-        }
+    for (int attempt = 0; attempt < 2; ++attempt) {
+        std::vector<float> hM(Rp, 0.0f);
+        for (int r = 0; r < R; ++r)
+            hM[r] = use_u32 ? std::ldexp(hC[r], -(hexp[r] + hexp[Rp + r])) : hC[r];
+        if ((e = cudaMemcpy(dM, hM.data(), sizeof(float) * Rp, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail_small(e, "cudaMemcpy(M)");
+        if ((e = cudaMemcpy(dexp, hexp.data(), sizeof(int) * 2 * Rp, cudaMemcpyHostToDevice)) != cudaSuccess)
+            return fail_small(e, "cudaMemcpy(exp)");
+        cudaMemsetAsync(flags, 0, sizeof(uint32_t), st);
+        if ((e = launch_prefix(dXY, dXY + (size_t)A * R, A, R, Rp, use_u32 ? 1 : 0, dexp, s->PXY, st)) !=
+            cudaSuccess)
+            return fail_small(e, "prefix kernel");
         s->stats.kernel_launches += 1;
-    } else {
-        // host Z: stream through a device staging buffer (or straight into Zc when Rp == R)
-        const int64_t chunk = std::max<int64_t>(1, (int64_t(64) << 20) / R);  // 256 MB of rows
-        float* stage = nullptr;
-        if (Rp != R && (e = cudaMalloc(&stage, sizeof(float) * (size_t)std::min(chunk, s->P) * R)) != cudaSuccess) {
-            free_small();
-            return fail(cuda_fail(e, "cudaMalloc(stage)"));
-        }
-        for (int64_t a = 0; a < s->P && e == cudaSuccess; a += chunk) {
-            const int64_t m = std::min(chunk, s->P - a);
-            float* dst = stage ? stage : s->Zc + (size_t)a * Rp;
-            e = cudaMemcpyAsync(dst, Z + (size_t)a * R, sizeof(float) * (size_t)m * R, cudaMemcpyDefault, st);
-            if (e == cudaSuccess) e = launch_fold_rows(dst, m, R, dC, s->Zc + (size_t)a * Rp, Rp, bad, st);
-            if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (z_dev) {
+            if ((e = launch_fold_rows(Z, s->P, R, dM, s->Zc, Rp, flags, st)) != cudaSuccess)
+                return fail_small(e, "fold kernel");
             s->stats.kernel_launches += 1;
+        } else {
+            // host Z: stream through a device staging buffer (or straight into Zc when Rp == R)
+            const int64_t chunk = std::max<int64_t>(1, (int64_t(64) << 20) / R);  // 256 MB of rows
+            float* stage = nullptr;
+            if (Rp != R && (e = cudaMalloc(&stage, sizeof(float) * (size_t)std::min(chunk, s->P) * R)) !=
+                               cudaSuccess)
+                return fail_small(e, "cudaMalloc(stage)");
+            for (int64_t a = 0; a < s->P && e == cudaSuccess; a += chunk) {
+                const int64_t m = std::min(chunk, s->P - a);
+                float* dst = stage ? stage : s->Zc + (size_t)a * Rp;
+                e = cudaMemcpyAsync(dst, Z + (size_t)a * R, sizeof(float) * (size_t)m * R, cudaMemcpyDefault, st);
+                if (e == cudaSuccess) e = launch_fold_rows(dst, m, R, dM, s->Zc + (size_t)a * Rp, Rp, flags, st);
+                if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+                s->stats.kernel_launches += 1;
+            }
+            cudaFree(stage);
+            if (e != cudaSuccess) return fail_small(e, "Z upload");
         }
-        cudaFree(stage);
-        if (e != cudaSuccess) {
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return fail_small(e, "store build");
+        if ((e = cudaMemcpy(&hflags, flags, sizeof(uint32_t), cudaMemcpyDeviceToHost)) != cudaSuccess)
+            return fail_small(e, "store build");
+        if (hflags & 1u) {  // negative or non-finite Z
             free_small();
-            return fail(cuda_fail(e, "Z upload"));
+            return fail(PNDF_EINVAL);
         }
+        if ((hflags & 2u) && use_u32 && pmode != PNDF_PREFIX_U32) {
+            use_u32 = false;  // the power-of-two rescale underflowed: rebuild with HILO
+            continue;
+        }
+        break;
     }
-    uint32_t hbad = 0;
-    e = cudaStreamSynchronize(st);
-    if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, sizeof(uint32_t), cudaMemcpyDeviceToHost);
     free_small();
-    if (e != cudaSuccess) return fail(cuda_fail(e, "store build"));
-    if (hbad) return fail(PNDF_EINVAL);  // negative or non-finite factor
+    cudaMemsetAsync(flags, 0, sizeof(uint32_t), st);
+    const size_t pxy_bytes = use_u32 ? pxy_bytes_max / 2 : pxy_bytes_max;
 
     QParams& p = s->qp;
     p.Zc = s->Zc;
@@ -380,7 +429,8 @@ pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float
     p.L = L;
     p.A = A;
     p.Rp = Rp;
-    p.wrap = desc->flags == PNDF_WRAP ? 1 : 0;
+    p.wrap = (desc->flags & PNDF_WRAP) ? 1 : 0;
+    p.prefix_u32 = use_u32 ? 1 : 0;
     p.inv_s0 = 1.0f / (float)s0;
     p.mean = 1;
     s->stats.rows = s->P;
@@ -388,6 +438,7 @@ pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float
     s->stats.lanes_per_query = s->G;
     s->stats.zc_bytes = (int64_t)zc_bytes;
     s->stats.prefix_bytes = (int64_t)pxy_bytes;
+    s->stats.prefix_format = use_u32 ? 1 : 0;
     *out = s;
     return PNDF_OK;
 }

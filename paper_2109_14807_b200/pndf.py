@@ -20,6 +20,7 @@ LIB_PATH = os.environ.get("PNDF_LIB") or os.path.join(_PKG, "libpndf.so")  # PND
 ABI_VERSION = 1
 OK, EINVAL, ENOMEM, ECUDA, EFORMAT, EQUERY = 0, -1, -2, -3, -4, -5
 CLAMP, WRAP = 0, 1
+PREFIX_AUTO, PREFIX_HILO, PREFIX_U32 = 0, 2, 4
 MEAN, SUM, BIN_AUTO, BIN_ON, BIN_OFF, TIMING = 0, 1, 0, 2, 4, 8
 
 QUERY_DTYPE = np.dtype([("u", "<f4"), ("v", "<f4"), ("size", "<f4"), ("rect", "<u4")])
@@ -45,10 +46,10 @@ class StoreStats(ctypes.Structure):
                 ("zc_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
                 ("kernel_launches", ctypes.c_uint64), ("timed_batches", ctypes.c_uint64),
                 ("query_ms", ctypes.c_double), ("bin_ms", ctypes.c_double), ("last_binned", ctypes.c_int32),
-                ("reserved", ctypes.c_int32)]
+                ("prefix_format", ctypes.c_int32)]
 
     def as_dict(self):
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sync", "pndf_query_batch_host", "pndf_free",
@@ -135,9 +136,9 @@ def _stream(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def make_desc(N: int, s0: int, L: int, A: int, R: int, wrap: bool = True) -> Desc:
+def make_desc(N: int, s0: int, L: int, A: int, R: int, wrap: bool = True, prefix: int = PREFIX_AUTO) -> Desc:
     return Desc(abi_version=ABI_VERSION, map_size=N, base_stride=s0, num_levels=L, ang_res=A, rank=R,
-                flags=WRAP if wrap else CLAMP)
+                flags=(WRAP if wrap else CLAMP) | prefix)
 
 
 class Store:
@@ -187,7 +188,12 @@ class Store:
         st = self.stats()
         Rp, A = st["rank_padded"], self.desc.ang_res
         z1 = st["rows"] if z1 is None else z1
-        pxy = np.empty((2, A + 1, 2, Rp), np.float32) if prefix else None
+        if not prefix:
+            pxy = None
+        elif st["prefix_format"] == 1:
+            pxy = np.empty((2, A + 1, Rp), np.uint32)
+        else:
+            pxy = np.empty((2, A + 1, 2, Rp), np.float32)
         zc = np.empty((z1 - z0, Rp), np.float32)
         _check(lib().pndf_store_image(self.handle, _ptr(pxy), _ptr(zc), z0, z1), "pndf_store_image")
         return pxy, zc

@@ -37,12 +37,15 @@ def torch_records(recs: np.ndarray, device="cuda"):
     return torch.from_numpy(np.ascontiguousarray(recs).view(np.int32).reshape(-1, 4)).to(device)
 
 
-def run_gpu(desc_args: dict, f, recs: np.ndarray, opts: int = 0, lanes: int = 0):
+def run_gpu(desc_args: dict, f, recs: np.ndarray, opts: int = 0, lanes: int = 0, prefix: int = 0,
+            want_format: int | None = None):
     """Load a store from raw factors, run one batch through the C ABI, return fp32 results + sticky status."""
     import torch
     from paper_2109_14807_b200 import pndf
-    d = pndf.make_desc(**desc_args)
+    d = pndf.make_desc(**desc_args, prefix=prefix)
     st = pndf.load_factors(d, f.C, f.X, f.Y, f.Z)
+    if want_format is not None:
+        assert st.stats()["prefix_format"] == want_format
     if lanes:
         st.set_lanes(lanes)
     q = torch_records(recs)
@@ -75,3 +78,22 @@ def oracle_on(cfg, f, recs, mean=True, zsparse=None):
         return oracle.query_batch(d, f.C, f.X, f.Y, f.Z, recs, mean=mean)
     Zs, zmap = zsparse
     return oracle.query_batch(d, f.C, f.X, f.Y, Zs, recs, mean=mean, zmap=zmap)
+
+
+def expected_prefix_format(f) -> int:
+    """The AUTO rule restated in numpy: U32 (1) iff for every rank of X and Y the fixed-point step
+    2^-e (e = largest with total*2^e <= 2^32-2) is <= 2^-15 of the smallest nonzero entry."""
+    import math
+    for F in (f.X, f.Y):
+        F = np.asarray(F, np.float64)
+        for r in range(F.shape[1]):
+            T = float(F[:, r].sum())
+            if T <= 0:
+                continue
+            e = math.floor(math.log2(4294967294.0 / T))
+            while math.ldexp(T, e) > 4294967294.0:
+                e -= 1
+            nz = F[:, r][F[:, r] > 0]
+            if math.ldexp(1.0, -e) > math.ldexp(float(nz.min()), -15):
+                return 0
+    return 1

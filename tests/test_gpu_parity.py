@@ -11,7 +11,8 @@ import pytest
 
 import oracle
 import synth
-from tests._util import assert_parity, config_inputs, desc_args, oracle_on, run_gpu, torch_records
+from tests._util import (assert_parity, config_inputs, desc_args, expected_prefix_format, oracle_on, run_gpu,
+                         torch_records)
 
 pytestmark = pytest.mark.gpu
 
@@ -52,24 +53,30 @@ def test_random_store_parity(shape, mode):
     d = oracle.make_desc(N, s0, L, A, R, wrap)
     mean = mode == "mean"
     ref = oracle.query_batch(d, f.C, f.X, f.Y, f.Z, recs, mean=mean)
-    for opts in (0 if mean else 1, (0 if mean else 1) | 2):  # unbinned, binned
-        got, st = run_gpu(dict(N=N, s0=s0, L=L, A=A, R=R, wrap=wrap), f, recs, opts)
-        assert st == 0
-        assert_parity(got, ref, f"{shape} opts={opts}")
+    fmt = expected_prefix_format(f)
+    for prefix, want in ((0, fmt), (2, 0)):  # AUTO (U32 when the rule allows it), forced HILO
+        for opts in (0 if mean else 1, (0 if mean else 1) | 2):  # unbinned, binned
+            got, st = run_gpu(dict(N=N, s0=s0, L=L, A=A, R=R, wrap=wrap), f, recs, opts, prefix=prefix,
+                              want_format=want)
+            assert st == 0
+            assert_parity(got, ref, f"{shape} opts={opts} prefix={prefix}")
 
 
 @pytest.mark.parametrize("k", [1, 2])
 def test_config_full_parity(k):
-    """Configs 1-2: every query of the batch."""
+    """Configs 1-2: every query of the batch, in both SAT formats."""
     cfg, bins, f = config_inputs(k)
     recs = synth.gen_queries(cfg, bins)
     ref = oracle_on(cfg, f, recs)
-    got, st = run_gpu(desc_args(cfg), f, recs, 0)
-    assert st == 0
-    stats = assert_parity(got, ref, f"config {k}")
-    assert stats["zeros"] < 0.9 * stats["n"]  # not dominated by blank-region queries
-    got_b, _ = run_gpu(desc_args(cfg), f, recs, 2)
-    assert got_b.tobytes() == got.tobytes()  # binning never changes a bit
+    fmt = expected_prefix_format(f)
+    assert fmt == (1 if k == 2 else 0)  # config 2's profiles allow the 4-byte SAT; config 1's ALS factors do not
+    for prefix, want in ((0, fmt), (2, 0)):
+        got, st = run_gpu(desc_args(cfg), f, recs, 0, prefix=prefix, want_format=want)
+        assert st == 0
+        stats = assert_parity(got, ref, f"config {k} prefix={prefix}")
+        assert stats["zeros"] < 0.9 * stats["n"]  # not dominated by blank-region queries
+        got_b, _ = run_gpu(desc_args(cfg), f, recs, 2, prefix=prefix)
+        assert got_b.tobytes() == got.tobytes()  # binning never changes a bit
 
 
 @pytest.mark.parametrize("k", [3, 4])
@@ -213,28 +220,46 @@ def test_argument_errors():
     st.free()
 
 
-def test_store_image_bits():
-    """Store build (row a0): Zc = fl32(C*Z), padded ranks 0; prefix = fp64 running sum split into fp32 hi/lo.
-    Reconstructed here independently with numpy."""
+@pytest.mark.parametrize("prefix", [2, 4])
+def test_store_image_bits(prefix):
+    """Store build (row a0), reconstructed independently with numpy:
+    HILO: Zc = fl32(C*Z), prefix = fp64 running sum split into fp32 (hi, lo);
+    U32:  q_k = round(S_k 2^e_r) with the largest e_r keeping q_A <= 2^32-2, Zc = fl32(C*Z) 2^-(ex_r+ey_r)."""
+    import math
     pndf = _pndf()
     N, s0, L, A, R = 16, 1, 5, 37, 13
     P = sum((N >> l) ** 2 for l in range(L))
     f = synth.random_factors(A, R, P, seed=3, sparsity=0.2)
-    st = pndf.load_factors(pndf.make_desc(N, s0, L, A, R), f.C, f.X, f.Y, f.Z)
+    st = pndf.load_factors(pndf.make_desc(N, s0, L, A, R, prefix=prefix), f.C, f.X, f.Y, f.Z)
     pxy, zc = st.image()
     Rp = st.stats()["rank_padded"]
     assert Rp % 4 == 0 and Rp >= R
-    want = np.zeros((P, Rp), np.float32)
-    want[:, :R] = f.C[None, :] * f.Z   # numpy fp32 multiply = fl32 of the exact product
-    assert zc.tobytes() == want.tobytes()
+    assert st.stats()["prefix_format"] == (1 if prefix == 4 else 0)
+    exps = np.zeros((2, Rp), np.int64)
     for t, F in enumerate((f.X, f.Y)):
         S = np.zeros((A + 1, Rp))
         for k in range(A):            # sequential fp64 running sum, index order
             S[k + 1, :R] = S[k, :R] + F[k].astype(np.float64)
-        hi = S.astype(np.float32)
-        lo = (S - hi.astype(np.float64)).astype(np.float32)
-        assert pxy[t, :, 0].tobytes() == hi.tobytes()
-        assert pxy[t, :, 1].tobytes() == lo.tobytes()
+        if prefix == 2:
+            hi = S.astype(np.float32)
+            lo = (S - hi.astype(np.float64)).astype(np.float32)
+            assert pxy[t, :, 0].tobytes() == hi.tobytes()
+            assert pxy[t, :, 1].tobytes() == lo.tobytes()
+        else:
+            for r in range(R):
+                T = S[A, r]
+                e = math.floor(math.log2(4294967294.0 / T))
+                while math.ldexp(T, e) > 4294967294.0:
+                    e -= 1
+                exps[t, r] = e
+                q = np.rint(np.ldexp(S[:, r], e)).astype(np.uint64)
+                assert np.array_equal(pxy[t, :, r].astype(np.uint64), q)
+            assert (pxy[t, :, R:] == 0).all()
+    want = np.zeros((P, Rp), np.float32)
+    want[:, :R] = f.C[None, :] * f.Z   # numpy fp32 multiply = fl32 of the exact product
+    if prefix == 4:
+        want[:, :R] = np.ldexp(want[:, :R], -(exps[0, :R] + exps[1, :R]).astype(np.int32))
+    assert zc.tobytes() == want.tobytes()
     st.free()
 
 

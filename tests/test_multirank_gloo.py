@@ -1,0 +1,70 @@
+"""N > 1 bookkeeping on CPU: two gloo ranks shard the query stream, answer their shards (with the
+oracle standing in for the device), and reduce times / checksums exactly like bench.py does."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+from paper_2109_14807_b200.shard import shard_range
+
+
+def test_shard_ranges_tile_the_stream():
+    for n in (0, 1, 7, 10**9 + 3):
+        for w in (1, 2, 3, 4, 8):
+            got = [shard_range(n, r, w) for r in range(w)]
+            assert got[0][0] == 0 and got[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(got, got[1:]))
+            sizes = [b - a for a, b in got]
+            assert max(sizes) - min(sizes) <= 1
+    with pytest.raises(ValueError):
+        shard_range(10, 2, 2)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, n, out_dir):
+    import torch.distributed as dist
+    import oracle
+    import synth
+    from paper_2109_14807_b200.shard import reduce_times_and_checksum, shard_range
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    cfg = synth.CONFIGS[2].scaled(N=128)
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    f = synth.build_factors(cfg, nxy, bins)
+    i0, i1 = shard_range(n, rank, world)
+    recs = synth.gen_queries(cfg, bins, i0, i1)  # counter-based: independent of the split
+    res = oracle.query_batch(oracle.desc_of(cfg), f.C, f.X, f.Y, f.Z, recs)
+    np.save(os.path.join(out_dir, f"res_{rank}.npy"), res)
+    (tmax,), total = reduce_times_and_checksum([float(rank + 1)], float(res.sum()))
+    if rank == 0:
+        np.save(os.path.join(out_dir, "reduced.npy"), np.array([tmax, total]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_gloo_ranks_match_one_process(tmp_path):
+    import oracle
+    import synth
+    n = 20_011
+    mp.spawn(_worker, args=(2, _free_port(), n, str(tmp_path)), nprocs=2, join=True)
+    parts = [np.load(tmp_path / f"res_{r}.npy") for r in range(2)]
+    cfg = synth.CONFIGS[2].scaled(N=128)
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    f = synth.build_factors(cfg, nxy, bins)
+    full = oracle.query_batch(oracle.desc_of(cfg), f.C, f.X, f.Y, f.Z, synth.gen_queries(cfg, bins, 0, n))
+    assert np.concatenate(parts).tobytes() == full.tobytes()  # per-query results independent of the split
+    tmax, total = np.load(tmp_path / "reduced.npy")
+    assert tmax == 2.0                                         # MAX over ranks of the step time
+    assert total == pytest.approx(parts[0].sum() + parts[1].sum(), rel=1e-15)

@@ -55,6 +55,29 @@ static void run_l1(void* v) {
     l1_kernel<<<a->grid, a->block>>>(a->p, a->n4, a->reps, a->sink);
 }
 
+// Library entry for bench.py: best-of-3 L2-resident float4 read bandwidth (GB/s)
+// over a working set of ws_mb MB on the current device; < 0 on error.
+extern "C" __attribute__((visibility("default"))) double membw_l2_read_gbs(int ws_mb) {
+    int sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t ws = (size_t)ws_mb << 20;
+    float4* buf = nullptr;
+    float* sink = nullptr;
+    if (cudaMalloc(&buf, ws) != cudaSuccess || cudaMalloc(&sink, 4) != cudaSuccess) return -1.0;
+    cudaMemset(buf, 0, ws);
+    double best = 0.0;
+    for (int r = 0; r < 3; ++r) {
+        Arg a{buf, ws / 16, 40, sink, sms * 8, 512};
+        const double ms = time_ms(run_read, &a);
+        const double gbs = (double)ws * 40 / ms / 1e6;
+        if (gbs > best) best = gbs;
+    }
+    cudaFree(buf);
+    cudaFree(sink);
+    return best;
+}
+
 int main(int argc, char** argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
