@@ -46,6 +46,9 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
 
 if __name__ == "__main__":
     build(force="--force" in sys.argv, verbose=True)
-    if "--variants" in sys.argv:  # tuning experiments: occupancy targets of the query kernel
-        for mb in (1, 3):
-            build(out=os.path.join(PKG, f"libpndf_minb{mb}.so"), defines=[f"PNDF_MINB={mb}"], verbose=True)
+    # tuning experiments: --variant NAME:DEF=V,DEF=V  ->  libpndf_NAME.so (select with PNDF_LIB)
+    for a in sys.argv[1:]:
+        if a.startswith("--variant="):
+            name, _, defs = a[len("--variant="):].partition(":")
+            build(out=os.path.join(PKG, f"libpndf_{name}.so"), defines=[d for d in defs.split(",") if d],
+                  verbose=True)

@@ -97,6 +97,32 @@ __device__ __forceinline__ void axis_cells(const QParams& p, float u, int l, int
     }
 }
 
+// a1 key: the record's half cell on its lower level l0, Z-ordered within the level:
+//   key = 4 off_{l0} + Morton(floor(2 f_u) mod 2n, floor(2 f_v) mod 2n).
+// With wrapped neighbours, equal keys <=> the same 8 Zc rows (level l0's cell is
+// floor(f) and level l0+1's cell floor((floor(2f) - 1)/4) -- both functions of
+// floor(2f)).  half = 0 falls back to cell keys off_{l0} + Morton(i0, j0).
+__device__ __forceinline__ uint64_t part1by1_64(uint64_t x) {
+    x &= 0x00000000ffffffffULL;
+    x = (x | (x << 16)) & 0x0000ffff0000ffffULL;
+    x = (x | (x << 8)) & 0x00ff00ff00ff00ffULL;
+    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0fULL;
+    x = (x | (x << 2)) & 0x3333333333333333ULL;
+    x = (x | (x << 1)) & 0x5555555555555555ULL;
+    return x;
+}
+
+__device__ __forceinline__ uint32_t cell_key(const QParams& p, const pndf_query& rec, int l0, int half) {
+    const int64_t n_l = p.n0 >> l0;
+    const float inv_s = __int_as_float(__float_as_int(p.inv_s0) - (l0 << 23));
+    const int64_t m = (n_l << half) - 1;
+    const float fu = fmaf(rec.u, inv_s, -0.5f), fv = fmaf(rec.v, inv_s, -0.5f);
+    const int64_t hu = (int64_t)floorf(half ? 2.f * fu : fu) & m;
+    const int64_t hv = (int64_t)floorf(half ? 2.f * fv : fv) & m;
+    return (uint32_t)((level_offset(p.n0, l0) << (2 * half)) +
+                      (int64_t)(part1by1_64((uint64_t)hu) | (part1by1_64((uint64_t)hv) << 1)));
+}
+
 // ------------------------------------------------- decoded query (smem) --
 // One warp decodes 32 records at once (one per lane) into these descriptors,
 // then the whole warp gathers for them G lanes per query.
@@ -110,8 +136,9 @@ struct __align__(16) QDesc {
 };
 static_assert(sizeof(QDesc) == 80, "QDesc layout");
 
+// returns the reuse key (0xffffffff = never equal to a neighbour's)
 template <bool WRAP>
-__device__ __forceinline__ void decode(const QParams& p, const pndf_query& rec, int32_t out_index, QDesc& d) {
+__device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& rec, int32_t out_index, QDesc& d) {
     int x1, x2, y1, y2;
     if (!record_valid(p, rec, x1, x2, y1, y2)) {
         atomicOr(p.err, 1u);
@@ -124,11 +151,12 @@ __device__ __forceinline__ void decode(const QParams& p, const pndf_query& rec, 
         d.py = 0;
         d.div = __int_as_float(0x7fc00000);
         d.out = out_index;
-        return;
+        return 0xffffffffu;
     }
     int l0;
     float t;
     level_select(p, rec.size, l0, t);
+    int r0 = 0, r3 = 0, r4 = 0, r7 = 0;
 #pragma unroll
     for (int dl = 0; dl < 2; ++dl) {
         const int l = l0 + dl;
@@ -143,6 +171,13 @@ __device__ __forceinline__ void decode(const QParams& p, const pndf_query& rec, 
         d.row[4 * dl + 1] = off + j0 * n + i1;
         d.row[4 * dl + 2] = off + j1 * n + i0;
         d.row[4 * dl + 3] = off + j1 * n + i1;
+        if (dl == 0) {
+            r0 = off + j0 * n + i0;
+            r3 = off + j1 * n + i1;
+        } else {
+            r4 = off + j0 * n + i0;
+            r7 = off + j1 * n + i1;
+        }
         const float wa = wl * (1.f - a), wb = wl * a;
         d.w[4 * dl + 0] = wa * (1.f - b);
         d.w[4 * dl + 1] = wb * (1.f - b);
@@ -153,26 +188,64 @@ __device__ __forceinline__ void decode(const QParams& p, const pndf_query& rec, 
     d.py = (uint32_t)y1 | ((uint32_t)(y2 + 1) << 16);
     d.div = p.mean ? (float)((x2 - x1 + 1) * (y2 - y1 + 1)) : 1.f;
     d.out = out_index;
+    if (WRAP) return cell_key(p, rec, l0, 1) & 0x7fffffffu;
+    // clamped borders: (i0, j0, i1, j1) on both levels pin the 8 rows; hash them
+    return (uint32_t)(r0 * 0x9E3779B1u ^ r3 * 0x85EBCA77u ^ r4 * 0xC2B2AE3Du ^ r7 * 0x27D4EB2Fu) & 0x7fffffffu;
+}
+
+// Reduce NB per-lane partials v[0..NB) over the G lanes of each group by
+// recursive halving: at level o the lanes with bit o set keep the upper half.
+// Every value is summed along the same pairing tree (xor G/2, G/4, ..., 1) as a
+// plain butterfly, so the result does not depend on the value's slot.
+// Afterwards lane gl holds the totals of slots (slot_base(gl) + i) for i < NB/G'.
+template <int G, int NB>
+__device__ __forceinline__ void group_reduce(float (&v)[NB], int gl) {
+    int nv = NB;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        if (nv > 1) {
+            const bool upper = (gl & o) != 0;
+            const int half = nv / 2;
+#pragma unroll
+            for (int i = 0; i < NB / 2; ++i) {
+                if (i < half) {
+                    const float send = upper ? v[i] : v[i + half];
+                    const float keep = upper ? v[i + half] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            nv = half;
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        }
+    }
 }
 
 // ------------------------------------------------------- query kernel --
 // Work split: CTA b owns the contiguous query range [b*chunk, (b+1)*chunk), so
 // binned (sorted) queries that share Zc rows run on the same SM and hit in L1.
 // Each warp takes 32 consecutive queries of the CTA's range at a time:
-//   1. decode: lane i decodes query i into a QDesc in shared memory;
+//   1. decode: lane i decodes query i into a QDesc in shared memory, and notes
+//      whether it has the same 8 Zc rows as query i-1 (equal half-cell key);
 //   2. gather: G lanes per query (QPW = 32/G queries per step); each lane owns
 //      NV float4 rank chunks at float offsets (gl + v*G)*4, so a query's G lanes
-//      read each row slice contiguously; 8 Zc + 8 prefix (hi, lo) loads per chunk,
-//      all issued before use; RP = 4*G*NV is a compile-time row stride;
-//   3. reduce: xor-butterfly over the G lanes (IEEE + is commutative, so all
-//      lanes of the group hold identical bits), then lane j of the warp keeps
-//      query j's value and the warp writes 32 results at once.
+//      read each row slice contiguously (RP = 4*G*NV is a compile-time stride).
+//      With G == 32 the previous query's Zc rows stay in registers and are not
+//      re-read when the rows repeat (binned neighbours);
+//   3. reduce: per-lane partials of 8 steps are reduced together over the G lanes
+//      (group_reduce: 1 shuffle per query instead of log2 G, and no shuffle chain
+//      between consecutive queries), then routed to lane (query index) and the
+//      warp writes 32 results at once.
 // A query's result never depends on where it sits in the batch, so binned and
 // unbinned batches are bitwise identical.
 constexpr int kWarpsPerBlock = kThreads / 32;
 #ifndef PNDF_MINB
-#define PNDF_MINB 2  // min resident blocks per SM (tuned on B200: 2-3 beat 1, see profiles/)
+#define PNDF_MINB 2  // min resident blocks per SM (tuned on B200: 2 beats 1 and 3, see profiles/)
 #endif
+#ifndef PNDF_KSTEPS
+#define PNDF_KSTEPS 8
+#endif
+constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced together
 
 template <int G, int NV, bool WRAP, bool BINNED, bool U32>
 __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParams p, const pndf_query* __restrict__ q,
@@ -180,7 +253,11 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                                                          int64_t chunk, float* __restrict__ out) {
     constexpr int QPW = 32 / G;
     constexpr int RP = 4 * G * NV;
+    constexpr int NSTEP = 32 / QPW;                       // steps per 32-query warp batch
+    constexpr int SB = NSTEP < kSteps ? NSTEP : kSteps;   // steps per reduction batch
+    constexpr int VPL = SB / G > 0 ? SB / G : 1;          // reduced values left per lane
     __shared__ QDesc sdesc[kWarpsPerBlock][32];
+    __shared__ uint32_t sreuse[kWarpsPerBlock];           // bit j: query j repeats query j-1's rows
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gl = lane % G, grp = lane / G;
     QDesc* wd = sdesc[warp];
@@ -192,16 +269,17 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 
     const int64_t c0 = (int64_t)blockIdx.x * chunk;
     const int64_t c1 = min(n, c0 + chunk);
+    float4 zc[NV][8];
     for (int64_t base = c0 + (int64_t)warp * 32; base < c1; base += (int64_t)kWarpsPerBlock * 32) {
         // 1. decode 32 records, one per lane
         {
             const int64_t qi = base + lane;
+            uint32_t key = 0xffffffffu;
             if (qi < c1) {
                 // binned: idx is the radix-sorted permutation; gather the record through it
                 const int64_t src = BINNED ? (int64_t)__ldg(idx + qi) : qi;
                 const pndf_query rec = ldg_query(q + src);
-                const int32_t oi = (int32_t)src;
-                decode<WRAP>(p, rec, oi, wd[lane]);
+                key = decode<WRAP>(p, rec, (int32_t)src, wd[lane]);
             } else {
                 wd[lane].out = -1;
 #pragma unroll
@@ -213,90 +291,117 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 wd[lane].py = 0;
                 wd[lane].div = 1.f;
             }
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+            const uint32_t same = __ballot_sync(0xffffffffu, lane > 0 && key == prev && key != 0xffffffffu);
+            if (lane == 0) sreuse[warp] = same;
         }
         __syncwarp();
-        // 2-3. gather + reduce, QPW queries per step.  With G == 32 a warp runs one
-        // query per step and keeps the previous query's Zc rows in registers: binned
-        // neighbours with the same half cell (all 8 rows equal) skip the Zc loads.
+        const uint32_t reuse_mask = (G == 32) ? sreuse[warp] : 0u;
+        // 2-3. gather + batched reduce
         float res = 0.f;
-        float4 zc[NV][8];
-        int cached[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) cached[k] = -1;
 #pragma unroll 1
-        for (int s = 0; s < 32; s += QPW) {
-            const QDesc& d = wd[s + grp];
-            const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
-            const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
-            const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
-            const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
-            const uint4 tail = *reinterpret_cast<const uint4*>(&d.px);
-            const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
-                                (int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
-            const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
-            const float* px0 = PX + (size_t)(tail.x & 0xffffu) * PSTRIDE;
-            const float* px1 = PX + (size_t)(tail.x >> 16) * PSTRIDE;
-            const float* py0 = PY + (size_t)(tail.y & 0xffffu) * PSTRIDE;
-            const float* py1 = PY + (size_t)(tail.y >> 16) * PSTRIDE;
-            bool reuse = false;
-            if (G == 32) {  // warp-uniform: every lane reads the same descriptor
-                reuse = true;
+        for (int s0 = 0; s0 < NSTEP; s0 += SB) {
+            float part[SB];
 #pragma unroll
-                for (int k = 0; k < 8; ++k) reuse = reuse && (row[k] == cached[k]);
+            for (int j = 0; j < SB; ++j) {
+                const int s = s0 + j;  // step: queries s*QPW + grp
+                const QDesc& d = wd[s * QPW + grp];
+                const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
+                const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
+                const uint2 tail = *reinterpret_cast<const uint2*>(&d.px);
+                const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
+                const float* px0 = PX + (size_t)(tail.x & 0xffffu) * PSTRIDE;
+                const float* px1 = PX + (size_t)(tail.x >> 16) * PSTRIDE;
+                const float* py0 = PY + (size_t)(tail.y & 0xffffu) * PSTRIDE;
+                const float* py1 = PY + (size_t)(tail.y >> 16) * PSTRIDE;
+                // warp-uniform for G == 32 (every lane reads the same descriptor)
+                const bool reuse = (G == 32) && s > 0 && ((reuse_mask >> s) & 1u);
+                if (!reuse) {
+                    const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
+                    const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
+                    const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
+                                        (int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
 #pragma unroll
-                for (int k = 0; k < 8; ++k) cached[k] = row[k];
-            }
-            if (!reuse) {
+                    for (int v = 0; v < NV; ++v)
 #pragma unroll
-                for (int v = 0; v < NV; ++v)
-#pragma unroll
-                    for (int k = 0; k < 8; ++k) zc[v][k] = ldg4(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
-            }
-            float part = 0.f;
-#pragma unroll
-            for (int v = 0; v < NV; ++v) {
-                const int c = (gl + v * G) * 4;
-                float4 dx, dy;
-                if (U32) {
-                    // exact integer differences of the fixed-point SATs (scale folded into Zc)
-                    const uint4 qx1 = __ldg(reinterpret_cast<const uint4*>(px1 + c));
-                    const uint4 qx0 = __ldg(reinterpret_cast<const uint4*>(px0 + c));
-                    const uint4 qy1 = __ldg(reinterpret_cast<const uint4*>(py1 + c));
-                    const uint4 qy0 = __ldg(reinterpret_cast<const uint4*>(py0 + c));
-                    dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
-                                     __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
-                    dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
-                                     __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
-                } else {
-                    // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
-                    // under cancellation (Sterbenz), lo carries the fp64 residual.
-                    const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
-                    const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
-                    const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
-                    const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
-                    dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
-                                     (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
-                    dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
-                                     (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                        for (int k = 0; k < 8; ++k) zc[v][k] = ldg4(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
                 }
-                float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+                float acc = 0.f;
 #pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    z.x = fmaf(w[k], zc[v][k].x, z.x);
-                    z.y = fmaf(w[k], zc[v][k].y, z.y);
-                    z.z = fmaf(w[k], zc[v][k].z, z.z);
-                    z.w = fmaf(w[k], zc[v][k].w, z.w);
+                for (int v = 0; v < NV; ++v) {
+                    const int c = (gl + v * G) * 4;
+                    float4 dx, dy;
+                    if (U32) {
+                        // exact integer differences of the fixed-point SATs (scale folded into Zc)
+                        const uint4 qx1 = __ldg(reinterpret_cast<const uint4*>(px1 + c));
+                        const uint4 qx0 = __ldg(reinterpret_cast<const uint4*>(px0 + c));
+                        const uint4 qy1 = __ldg(reinterpret_cast<const uint4*>(py1 + c));
+                        const uint4 qy0 = __ldg(reinterpret_cast<const uint4*>(py0 + c));
+                        dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                         __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                        dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                         __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                    } else {
+                        // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
+                        // under cancellation (Sterbenz), lo carries the fp64 residual.
+                        const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
+                        const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
+                        const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
+                        const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
+                        dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                         (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                        dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                         (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                    }
+                    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        z.x = fmaf(w[k], zc[v][k].x, z.x);
+                        z.y = fmaf(w[k], zc[v][k].y, z.y);
+                        z.z = fmaf(w[k], zc[v][k].z, z.z);
+                        z.w = fmaf(w[k], zc[v][k].w, z.w);
+                    }
+                    acc = fmaf(dx.x * dy.x, z.x, acc);
+                    acc = fmaf(dx.y * dy.y, z.y, acc);
+                    acc = fmaf(dx.z * dy.z, z.z, acc);
+                    acc = fmaf(dx.w * dy.w, z.w, acc);
                 }
-                part = fmaf(dx.x * dy.x, z.x, part);
-                part = fmaf(dx.y * dy.y, z.y, part);
-                part = fmaf(dx.z * dy.z, z.z, part);
-                part = fmaf(dx.w * dy.w, z.w, part);
+                part[j] = acc;
             }
+            group_reduce<G, SB>(part, gl);
+            // lane gl holds slots [slot0, slot0 + VPL) of its group: slot bits from the halving levels
+            int slot0 = 0;
+            {
+                int nv = SB, o = G / 2;
+                while (nv > 1 && o > 0) {
+                    nv >>= 1;
+                    if (gl & o) slot0 += nv;
+                    o >>= 1;
+                }
+            }
+            // route: query (s0 + j) * QPW + g of this batch goes to lane (s0 + j) * QPW + g
 #pragma unroll
-            for (int o = G / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-            // lane s+j takes query s+j's value from lane j*G
-            const float got = __shfl_sync(0xffffffffu, part, ((lane - s) & (QPW - 1)) * G);
-            if (lane >= s && lane < s + QPW) res = got;
+            for (int i = 0; i < VPL; ++i) {
+                const int dst_rel = lane - s0 * QPW;  // this lane's query, relative to the batch
+                const int j = dst_rel / QPW, g = dst_rel % QPW;
+                // source lane: group g, a lane whose slot range starts at j - (j % VPL) when i == j % VPL
+                int src_gl = 0;
+                {
+                    int nv = SB, o = G / 2, rem = j;
+                    while (nv > 1 && o > 0) {
+                        nv >>= 1;
+                        if (rem >= nv) {
+                            src_gl |= o;
+                            rem -= nv;
+                        }
+                        o >>= 1;
+                    }
+                }
+                const float got = __shfl_sync(0xffffffffu, part[i], (g * G + src_gl) & 31);
+                const bool mine = dst_rel >= 0 && dst_rel < SB * QPW && (j % VPL) == i;
+                if (mine) res = got;
+            }
+            (void)slot0;
         }
         const QDesc& mine = wd[lane];
         const int32_t oi = mine.out;
@@ -388,19 +493,6 @@ cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, c
 //   scan_*_kernel      exclusive scan of the histograms -> each tile's digit offsets
 //   rs_scatter_kernel  stable tile-local ranking (match_any + per-warp counts),
 //                      staged in shared memory, written out digit run by run.
-__device__ __forceinline__ uint64_t part1by1_64(uint64_t x) {
-    x &= 0x00000000ffffffffULL;
-    x = (x | (x << 16)) & 0x0000ffff0000ffffULL;
-    x = (x | (x << 8)) & 0x00ff00ff00ff00ffULL;
-    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0fULL;
-    x = (x | (x << 2)) & 0x3333333333333333ULL;
-    x = (x | (x << 1)) & 0x5555555555555555ULL;
-    return x;
-}
-
-// half = 1: key = 4 off_{l0} + Morton(floor(2 f_u), floor(2 f_v)) -- a half cell of
-// level l0, so equal keys share all 8 Zc rows (level l0+1's cell is fixed by the
-// half cell); half = 0: cell keys off_{l0} + Morton(i0, j0).
 __global__ void bin_keys_kernel(const QParams p, const pndf_query* __restrict__ q, int64_t n, uint32_t* keys,
                                 uint32_t invalid_key, int half) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -411,14 +503,7 @@ __global__ void bin_keys_kernel(const QParams p, const pndf_query* __restrict__ 
             int l0;
             float t;
             level_select(p, rec.size, l0, t);
-            const int64_t n_l = p.n0 >> l0;
-            const float inv_s = __int_as_float(__float_as_int(p.inv_s0) - (l0 << 23));
-            const int64_t m = (n_l << half) - 1;
-            const float fu = fmaf(rec.u, inv_s, -0.5f), fv = fmaf(rec.v, inv_s, -0.5f);
-            const int64_t hu = (int64_t)floorf(half ? 2.f * fu : fu) & m;
-            const int64_t hv = (int64_t)floorf(half ? 2.f * fv : fv) & m;
-            key = (uint32_t)((level_offset(p.n0, l0) << (2 * half)) +
-                             (int64_t)(part1by1_64((uint64_t)hu) | (part1by1_64((uint64_t)hv) << 1)));
+            key = cell_key(p, rec, l0, half);
         }
         keys[i] = key;
     }

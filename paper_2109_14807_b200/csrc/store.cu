@@ -159,9 +159,10 @@ bool want_bins(const pndf_store_s* s, int64_t n, uint32_t opts) {
     if (s->nbins == 0 || (opts & PNDF_BIN_OFF)) return false;
     if (opts & PNDF_BIN_ON) return true;
     // AUTO: the factor set does not stay in L2, and the batch reuses rows enough
-    // (>= 8 queries per positional row) for the sort to pay for itself (measured
-    // on B200: config 4, 18 queries/row, gains 11%; config 3, 1.8/row, loses 40%).
-    return (int64_t)s->stats.zc_bytes > s->l2_bytes / 2 && n >= 8 * s->P;
+    // (>= 4 queries per positional row) for the sort to pay for itself (measured on
+    // B200: config 5 at 5.6 queries/row gains 27%, config 4 at 18/row 11%; config 3
+    // at 1.8/row loses 40%).
+    return (int64_t)s->stats.zc_bytes > s->l2_bytes / 2 && n >= 4 * s->P;
 }
 
 // Enqueue one batch (device records) on st using scratch sc.
@@ -487,9 +488,29 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
     std::lock_guard<std::mutex> lk(s->mu);
     DeviceGuard g(s->device);
     // chunk so that >= 8 chunks overlap when the batch allows, 1M..64M records each
-    int64_t chunk = std::max<int64_t>(int64_t(1) << 20, std::min<int64_t>(int64_t(1) << 26, (n + 7) / 8));
+    // Chunking: >= 8 chunks overlap H2D / kernels / D2H on the three slot streams.  When the
+    // whole batch qualifies for binning, chunks are made large enough (>= 4 queries per
+    // positional row) to be binned on their own; otherwise 1M..64M records each.
+    const bool bin_all = want_bins(s, n, opts);
+    int64_t chunk;
+    if (bin_all && !(opts & PNDF_BIN_ON))
+        chunk = std::max<int64_t>(4 * s->P, (n + 7) / 8);
+    else
+        chunk = std::max<int64_t>(int64_t(1) << 20, std::min<int64_t>(int64_t(1) << 26, (n + 7) / 8));
     chunk = std::min(chunk, n);
-    const bool binned = want_bins(s, chunk, opts);
+    {  // fit kSlots x (records + results + binning scratch) in free device memory
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            int64_t have = 0;
+            for (auto& sl : s->slots) have += sl.cap * 20 + sl.scratch.cap * 16;
+            const int64_t budget = (int64_t)(free_b * 0.8) + have;
+            const int64_t per_q = 20 + (bin_all ? 18 : 0);
+            const int64_t fit = budget / (kSlots * per_q);
+            if (chunk > fit) chunk = std::max<int64_t>(int64_t(1) << 20, fit);
+        }
+    }
+    const bool binned = (opts & PNDF_BIN_ON) ? true : (bin_all && chunk >= 4 * s->P);
+    const uint32_t chunk_opts = (opts & PNDF_SUM) | (binned ? PNDF_BIN_ON : PNDF_BIN_OFF);
     for (auto& sl : s->slots) {
         if (!sl.st) CK(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
         if (sl.cap < chunk) {
@@ -512,7 +533,7 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
         Slot& sl = s->slots[c % kSlots];
         const int64_t m = std::min(chunk, n - a);
         CK(cudaMemcpyAsync(sl.d_rec, h_queries + a, sizeof(pndf_query) * m, cudaMemcpyHostToDevice, sl.st));
-        pndf_status r = enqueue(s, sl.scratch, sl.d_rec, m, sl.d_out, opts, sl.st, false);
+        pndf_status r = enqueue(s, sl.scratch, sl.d_rec, m, sl.d_out, chunk_opts, sl.st, false);
         if (r != PNDF_OK) return r;
         CK(cudaMemcpyAsync(h_out + a, sl.d_out, sizeof(float) * m, cudaMemcpyDeviceToHost, sl.st));
     }

@@ -1,0 +1,133 @@
+"""Turn gpurun_out/ ncu captures into the committed evidence under profiles/ (per round).
+
+usage: python tools/write_profiles.py ROUND QUERIES_IN_CAPTURE
+  reads  gpurun_out/prof_query_full.ncu-rep, gpurun_out/prof_scatter_full.ncu-rep,
+         gpurun_out/launches_default.csv, gpurun_out/bench_default.log
+  writes profiles/rNN_query_kernel_ncu.txt, profiles/rNN_radix_scatter_ncu.txt,
+         profiles/rNN_launches_default.txt (+ .csv), profiles/rNN_bench_default.json,
+         profiles/ncu_traffic.json (DRAM bytes per query of the query kernel, read by bench.py)
+"""
+import csv
+import io
+import json
+import os
+import subprocess
+import sys
+from collections import defaultdict
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "profiles")
+GP = os.path.join(ROOT, "gpurun_out")
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "dram__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_sectors_srcunit_tex_op_read.sum",
+           "lts__t_sector_hit_rate.pct", "lts__throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__t_sector_hit_rate.pct", "l1tex__throughput.avg.pct_of_peak_sustained_elapsed",
+           "l1tex__t_requests_pipe_lsu_mem_global_op_ld.sum", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "smsp__issue_active.avg.pct_of_peak_sustained_active", "sm__warps_active.avg.pct_of_peak_sustained_active",
+           "smsp__average_warp_latency_per_inst_issued.ratio", "smsp__inst_executed.sum",
+           "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+           "sm__cycles_elapsed.avg.per_second"]
+SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+
+
+def ncu_csv(rep, page):
+    out = subprocess.run(["ncu", "-i", rep, "--page", page, "--csv"], capture_output=True, text=True).stdout
+    return list(csv.reader(io.StringIO(out)))
+
+
+def summarize(rep, nq, title):
+    rows = ncu_csv(rep, "raw")
+    hdr, units, v = rows[0], rows[1], rows[2]
+    lines = [f"# {title}", f"# source: {os.path.basename(rep)} (ncu --set full --clock-control none)",
+             f"# queries in the captured launch: {nq:.0f}", ""]
+    vals = {}
+    for m in METRICS:
+        if m in hdr:
+            i = hdr.index(m)
+            vals[m] = (v[i], units[i])
+            lines.append(f"{m:60s} {v[i]:>24s} {units[i]}")
+    lines.append("")
+
+    def num(m):
+        x, u = vals[m]
+        return float(x.replace(",", "")) * SCALE.get(u, 1)
+
+    dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+    lines.append(f"dram bytes per query (read+write): {dram / nq:.1f}")
+    lines.append(f"L2->L1 read bytes per query: {float(vals['lts__t_sectors_srcunit_tex_op_read.sum'][0].replace(',', '')) * 32 / nq:.1f}")
+    lines.append(f"warp instructions per query: {float(vals['smsp__inst_executed.sum'][0].replace(',', '')) / nq:.1f}")
+    src = ncu_csv(rep, "source")
+    if len(src) > 2:
+        h = src[1]
+        data = src[2:]
+        iS, iW, iE = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
+        tot = sum(int(r[iW]) for r in data) or 1
+        c, s = defaultdict(int), defaultdict(int)
+        for r in data:
+            t = r[iS].split()
+            if not t:
+                continue
+            op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
+            c[op] += int(r[iE])
+            s[op] += int(r[iW])
+        lines += ["", "opcode mix (per query) and share of warp-stall samples:"]
+        for op, k in sorted(c.items(), key=lambda x: -x[1])[:16]:
+            lines.append(f"  {op:10s} {k / nq:8.2f}/q   stall {s[op] / tot * 100:5.1f}%")
+    return "\n".join(lines) + "\n", dram / nq
+
+
+def launches(path):
+    rows = list(csv.reader(open(path)))
+    start = next(i for i, r in enumerate(rows) if r and r[0] == "ID")
+    h = rows[start]
+    iN, iV = h.index("Kernel Name"), h.index("Metric Value")
+    tot, cnt = defaultdict(float), defaultdict(int)
+    for r in rows[start + 1:]:
+        if len(r) <= iV:
+            continue
+        try:
+            val = float(r[iV].replace(",", ""))
+        except ValueError:
+            continue
+        name = r[iN].split("(")[0]
+        tot[name] += val
+        cnt[name] += 1
+    T = sum(tot.values()) or 1
+    lines = ["# ncu --metrics gpu__time_duration.sum --clock-control none, `python bench.py` (default run)",
+             "# per-launch times are cold-cache and serialised: compare SHARES, not absolutes",
+             f"{'kernel':70s} {'launches':>8s} {'total ms':>10s} {'share':>7s}"]
+    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+        lines.append(f"{k[:70]:70s} {cnt[k]:8d} {v / 1e6:10.2f} {v / T * 100:6.1f}%")
+    return "\n".join(lines) + "\n"
+
+
+def main():
+    rnd = sys.argv[1]
+    nq = float(sys.argv[2])
+    os.makedirs(OUT, exist_ok=True)
+    traffic = {}
+    q = os.path.join(GP, "prof_query_full.ncu-rep")
+    if os.path.exists(q):
+        txt, dpq = summarize(q, nq, "pndf::query_kernel, config 5, binned, U32 SATs")
+        open(os.path.join(OUT, f"{rnd}_query_kernel_ncu.txt"), "w").write(txt)
+        traffic["config5"] = {"dram_bytes_per_query": dpq,
+                              "source": f"profiles/{rnd}_query_kernel_ncu.txt (ncu --set full, {nq:.0e} queries, "
+                                        "same launch configuration as bench.py)"}
+    sc = os.path.join(GP, "prof_scatter_full.ncu-rep")
+    if os.path.exists(sc):
+        txt, _ = summarize(sc, nq, "pndf::rs_scatter_kernel<9> (one radix pass), config 5")
+        open(os.path.join(OUT, f"{rnd}_radix_scatter_ncu.txt"), "w").write(txt)
+    la = os.path.join(GP, "launches_default.csv")
+    if os.path.exists(la):
+        open(os.path.join(OUT, f"{rnd}_launches_default.txt"), "w").write(launches(la))
+    b = os.path.join(GP, "bench_default.log")
+    if os.path.exists(b):
+        line = [l for l in open(b).read().splitlines() if l.startswith("{")][-1]
+        json.dump(json.loads(line), open(os.path.join(OUT, f"{rnd}_bench_default.json"), "w"), indent=1)
+    if traffic:
+        json.dump(traffic, open(os.path.join(OUT, "ncu_traffic.json"), "w"), indent=1)
+
+
+if __name__ == "__main__":
+    main()
