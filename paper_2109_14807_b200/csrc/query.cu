@@ -31,6 +31,34 @@ __device__ __forceinline__ pndf_query ldg_query(const pndf_query* q) {
     return r;
 }
 
+// --------------------------------------------- TMA bulk copy + mbarrier --
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+// one contiguous global -> shared copy on the TMA engine, completion counted on bar
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+
 // off_l = sum_{m<l} (n0 >> m)^2 = 4 n_l^2 (4^l - 1)/3 for power-of-two n0, and
 // (4^l - 1)/3 = 0x5555... (l bit pairs): exact, no division.
 __device__ __forceinline__ int64_t level_offset(int64_t n0, int l) {
@@ -247,25 +275,73 @@ constexpr int kWarpsPerBlock = kThreads / 32;
 #endif
 constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced together
 
+#ifndef PNDF_TMA
+#define PNDF_TMA 0  // 1: stage SAT rows of the next query in smem with TMA bulk copies (measured slower on B200)
+#endif
+constexpr int kSlots = 2;  // per-warp SAT staging slots (prefetch distance 1)
+
+// SAT rows are staged by TMA when a warp runs one query per step (G == 32) and a
+// slot (4 rows) is at most 4 KB, so 8 warps x 2 slots fit beside the descriptors.
+template <int G, int NV, bool U32>
+struct QLayout {
+    static constexpr int RP = 4 * G * NV;
+    static constexpr int PSTRIDE = U32 ? RP : 2 * RP;  // floats (or uint32) per SAT entry row
+    static constexpr bool TMA = PNDF_TMA && G == 32 && PSTRIDE <= 256;
+    static constexpr int ROW_BYTES = PSTRIDE * 4;
+    static constexpr size_t DESC = sizeof(QDesc) * kWarpsPerBlock * 32;
+    static constexpr size_t REUSE = 128;
+    static constexpr size_t BARS = TMA ? 128 : 0;
+    static constexpr size_t SLOTS = TMA ? (size_t)kWarpsPerBlock * kSlots * 4 * ROW_BYTES : 0;
+    static constexpr size_t BYTES = DESC + REUSE + BARS + SLOTS;
+};
+
 template <int G, int NV, bool WRAP, bool BINNED, bool U32>
 __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParams p, const pndf_query* __restrict__ q,
                                                          const uint32_t* __restrict__ idx, int64_t n,
                                                          int64_t chunk, float* __restrict__ out) {
+    using LY = QLayout<G, NV, U32>;
     constexpr int QPW = 32 / G;
-    constexpr int RP = 4 * G * NV;
+    constexpr int RP = LY::RP;
     constexpr int NSTEP = 32 / QPW;                       // steps per 32-query warp batch
     constexpr int SB = NSTEP < kSteps ? NSTEP : kSteps;   // steps per reduction batch
     constexpr int VPL = SB / G > 0 ? SB / G : 1;          // reduced values left per lane
-    __shared__ QDesc sdesc[kWarpsPerBlock][32];
-    __shared__ uint32_t sreuse[kWarpsPerBlock];           // bit j: query j repeats query j-1's rows
+    constexpr bool TMA = LY::TMA;
+    extern __shared__ __align__(128) unsigned char qsmem[];
+    QDesc(*sdesc)[32] = reinterpret_cast<QDesc(*)[32]>(qsmem);
+    uint32_t* sreuse = reinterpret_cast<uint32_t*>(qsmem + LY::DESC);  // bit j: query j repeats j-1's rows
+    uint64_t* sbar = reinterpret_cast<uint64_t*>(qsmem + LY::DESC + LY::REUSE);
+    uint32_t* sslot = reinterpret_cast<uint32_t*>(qsmem + LY::DESC + LY::REUSE + LY::BARS);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int gl = lane % G, grp = lane / G;
     QDesc* wd = sdesc[warp];
     const float* __restrict__ Zc = p.Zc;
     // SAT rows: HILO = [hi row | lo row] per entry (stride 2*RP floats), U32 = one uint32 row
-    constexpr int PSTRIDE = U32 ? RP : 2 * RP;
+    constexpr int PSTRIDE = LY::PSTRIDE;
     const float* __restrict__ PX = p.PXY;
     const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * PSTRIDE;
+    uint64_t* wbar = sbar + warp * kSlots;
+    uint32_t* wslot = sslot + (size_t)warp * kSlots * 4 * PSTRIDE;
+    uint32_t phase = 0;  // bit k: parity of slot k's next completion
+    if (TMA) {
+        if (lane == 0)
+            for (int k = 0; k < kSlots; ++k) mbar_init(wbar + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+    }
+    // lane 0: TMA the 4 SAT rows (x1, x2+1, y1, y2+1) of warp-batch query s into slot s % kSlots
+    auto issue_sat = [&](int s) {
+        if (lane == 0) {
+            const QDesc& d = wd[s];
+            const int k = s % kSlots;
+            uint32_t* dst = wslot + (size_t)k * 4 * PSTRIDE;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot was last read by the generic proxy
+            mbar_arrive_expect_tx(wbar + k, 4 * LY::ROW_BYTES);
+            tma_load_1d(dst + 0 * PSTRIDE, PX + (size_t)(d.px & 0xffffu) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+            tma_load_1d(dst + 1 * PSTRIDE, PX + (size_t)(d.px >> 16) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+            tma_load_1d(dst + 2 * PSTRIDE, PY + (size_t)(d.py & 0xffffu) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+            tma_load_1d(dst + 3 * PSTRIDE, PY + (size_t)(d.py >> 16) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+        }
+    };
 
     const int64_t c0 = (int64_t)blockIdx.x * chunk;
     const int64_t c1 = min(n, c0 + chunk);
@@ -297,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
         }
         __syncwarp();
         const uint32_t reuse_mask = (G == 32) ? sreuse[warp] : 0u;
+        if (TMA) issue_sat(0);
         // 2-3. gather + batched reduce
         float res = 0.f;
 #pragma unroll 1
@@ -306,6 +383,13 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
             for (int j = 0; j < SB; ++j) {
                 const int s = s0 + j;  // step: queries s*QPW + grp
                 const QDesc& d = wd[s * QPW + grp];
+                if (TMA) {
+                    if (s + 1 < NSTEP) issue_sat(s + 1);  // prefetch the next query's SAT rows
+                    const int k = s % kSlots;
+                    while (!mbar_try_wait(wbar + k, (phase >> k) & 1u)) {
+                    }
+                    phase ^= 1u << k;
+                }
                 const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
                 const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
                 const uint2 tail = *reinterpret_cast<const uint2*>(&d.px);
@@ -331,7 +415,31 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 for (int v = 0; v < NV; ++v) {
                     const int c = (gl + v * G) * 4;
                     float4 dx, dy;
-                    if (U32) {
+                    const uint32_t* sl = wslot + (size_t)(s % kSlots) * 4 * PSTRIDE;
+                    if (TMA && U32) {
+                        const uint4 qx0 = *reinterpret_cast<const uint4*>(sl + 0 * PSTRIDE + c);
+                        const uint4 qx1 = *reinterpret_cast<const uint4*>(sl + 1 * PSTRIDE + c);
+                        const uint4 qy0 = *reinterpret_cast<const uint4*>(sl + 2 * PSTRIDE + c);
+                        const uint4 qy1 = *reinterpret_cast<const uint4*>(sl + 3 * PSTRIDE + c);
+                        dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                         __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                        dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                         __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                    } else if (TMA) {
+                        const float* sf = reinterpret_cast<const float*>(sl);
+                        const float4 xh0 = *reinterpret_cast<const float4*>(sf + 0 * PSTRIDE + c);
+                        const float4 xl0 = *reinterpret_cast<const float4*>(sf + 0 * PSTRIDE + RP + c);
+                        const float4 xh1 = *reinterpret_cast<const float4*>(sf + 1 * PSTRIDE + c);
+                        const float4 xl1 = *reinterpret_cast<const float4*>(sf + 1 * PSTRIDE + RP + c);
+                        const float4 yh0 = *reinterpret_cast<const float4*>(sf + 2 * PSTRIDE + c);
+                        const float4 yl0 = *reinterpret_cast<const float4*>(sf + 2 * PSTRIDE + RP + c);
+                        const float4 yh1 = *reinterpret_cast<const float4*>(sf + 3 * PSTRIDE + c);
+                        const float4 yl1 = *reinterpret_cast<const float4*>(sf + 3 * PSTRIDE + RP + c);
+                        dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                         (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                        dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                         (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                    } else if (U32) {
                         // exact integer differences of the fixed-point SATs (scale folded into Zc)
                         const uint4 qx1 = __ldg(reinterpret_cast<const uint4*>(px1 + c));
                         const uint4 qx0 = __ldg(reinterpret_cast<const uint4*>(px0 + c));
@@ -367,6 +475,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                     acc = fmaf(dx.w * dy.w, z.w, acc);
                 }
                 part[j] = acc;
+                if (TMA) __syncwarp();  // every lane is done with this slot before it is refilled
             }
             group_reduce<G, SB>(part, gl);
             // lane gl holds slots [slot0, slot0 + VPL) of its group: slot bits from the halving levels
@@ -415,9 +524,11 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 template <int G, int NV, bool W, bool B, bool U>
 static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
                             int num_sms, cudaStream_t st) {
+    constexpr size_t smem = QLayout<G, NV, U>::BYTES;
+    cudaFuncSetAttribute(query_kernel<G, NV, W, B, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     static int occ = -1;
     if (occ < 0) {
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, query_kernel<G, NV, W, B, U>, kThreads, 0) !=
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, query_kernel<G, NV, W, B, U>, kThreads, smem) !=
                 cudaSuccess ||
             occ < 1)
             occ = 1;
@@ -429,7 +540,7 @@ static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_
     int64_t chunk = (n + grid - 1) / grid;
     chunk = (chunk + 31) / 32 * 32;
     grid = (n + chunk - 1) / chunk;
-    query_kernel<G, NV, W, B, U><<<(unsigned)grid, kThreads, 0, st>>>(p, q, idx, n, chunk, out);
+    query_kernel<G, NV, W, B, U><<<(unsigned)grid, kThreads, smem, st>>>(p, q, idx, n, chunk, out);
     return cudaGetLastError();
 }
 
