@@ -51,6 +51,7 @@ def lib():
         L.oracle_query_batch.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, P, ctypes.c_int64, ctypes.c_int, P,
                                          ctypes.c_int]
         L.oracle_neighbours_batch.argtypes = [ctypes.POINTER(Desc), P, ctypes.c_int64, P, P]
+        L.oracle_sample_batch.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, P, P, ctypes.c_int64, P, P, P, P]
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -90,6 +91,31 @@ def query_batch(desc: Desc, C, X, Y, Z, records: np.ndarray, mean: bool = True, 
     lib().oracle_query_batch(ctypes.byref(desc), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(zmap), _ptr(recs),
                              recs.shape[0], 1 if mean else 0, _ptr(out), threads)
     return out
+
+
+def sample_batch(desc: Desc, C, X, Y, Z, records: np.ndarray, xi: np.ndarray, zmap=None):
+    """Hierarchical importance sampling (Sec. 5.2), fp64.
+    xi: float32 [n, 10] variates (8 descent levels + 2 jitter).  Returns dict of
+    pixel int32 [n, 2] (-1 = no sample), prob float64 [n] (pixel mass / domain mass),
+    h float64 [n, 2] (projected half vector), margin float64 [n] (min relative distance
+    of a variate to a decision boundary)."""
+    C = np.ascontiguousarray(C, np.float32)
+    X = np.ascontiguousarray(X, np.float32)
+    Y = np.ascontiguousarray(Y, np.float32)
+    Z = np.ascontiguousarray(Z, np.float32)
+    recs = np.ascontiguousarray(records)
+    xi = np.ascontiguousarray(xi, np.float32)
+    n = recs.shape[0]
+    assert xi.shape == (n, 10)
+    if zmap is not None:
+        zmap = np.ascontiguousarray(zmap, np.int64)
+    pix = np.empty((n, 2), np.int32)
+    prob = np.empty(n, np.float64)
+    h = np.empty((n, 2), np.float64)
+    mg = np.empty(n, np.float64)
+    lib().oracle_sample_batch(ctypes.byref(desc), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(zmap), _ptr(recs),
+                              _ptr(xi), n, _ptr(pix), _ptr(prob), _ptr(h), _ptr(mg))
+    return dict(pixel=pix, prob=prob, h=h, margin=mg)
 
 
 def neighbours(desc: Desc, records: np.ndarray):

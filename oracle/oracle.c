@@ -33,6 +33,7 @@
 #include <math.h>
 #include <stdint.h>
 #include <stddef.h>
+#include <stdlib.h>
 #include <omp.h>
 
 #define EXPORT __attribute__((visibility("default")))
@@ -185,6 +186,106 @@ EXPORT void oracle_neighbours_batch(const oracle_desc* d, const oracle_rec* q, i
     for (int64_t i = 0; i < n; ++i)
         if (!oracle_neighbours(d, &q[i], rows + 8 * i, w + 8 * i))
             for (int k = 0; k < 8; ++k) { rows[8 * i + k] = -1; w[8 * i + k] = NAN; }
+}
+
+/* ------------------------------------------------------------------------
+ * Hierarchical importance sampling (Sec. 5.2), one global group.
+ * "We start from the entire NDF image, and subdivide it evenly into four
+ * quads ... acquire the average values in these four quads ... use the four
+ * average values as relative probabilities, and randomly choose one quad to
+ * proceed ... until reaching the bottom level, i.e. a pixel"; "when we
+ * reach a pixel, we uniformly perturb the sample location inside it".
+ * Readings: the descent starts from the record's rectangle (the
+ * whole A x A image for plain sampling -- with one global group there is no
+ * separate block choice); a range of width w splits into ceil(w/2) | floor(w/2)
+ * (equal halves for the power-of-two grids of the configs); the relative
+ * probabilities are the quads' SUMS (= averages x area, identical to the
+ * paper's averages for equal quads, and exact for unequal ones); quad order
+ * (x-low,y-low), (x-high,y-low), (x-low,y-high), (x-high,y-high); one variate
+ * per level, xi[l] in [0,1), t = xi[l] * total, first quad with t < cumulative
+ * sum (a zero quad is never chosen; if rounding leaves t >= all sums, the last
+ * nonzero quad); xi[8], xi[9] jitter the pixel.  Outputs the pixel, its
+ * probability mass / domain mass (the sampling pmf: "the PDF ... is
+ * exactly the same as the evaluated NDF value") and the smallest relative
+ * distance of a variate to a decision boundary (for tests).
+ */
+typedef struct {
+    double xs[4096], ys[4096];
+} oracle_scratch;
+
+/* Eq. 6 SUM over [xa, xb) x [ya, yb) blended over the 8 neighbours */
+static double oracle_rect_sum(const oracle_desc* d, const float* C, const float* X, const float* Y, const float* Z,
+                              const int64_t* zmap, const int64_t* zk, const double* wk, int xa, int xb, int ya,
+                              int yb, oracle_scratch* sc) {
+    if (xb <= xa || yb <= ya) return 0.0;
+    const int R = d->R;
+    for (int r = 0; r < R; ++r) { sc->xs[r] = 0.0; sc->ys[r] = 0.0; }
+    for (int x = xa; x < xb; ++x)
+        for (int r = 0; r < R; ++r) sc->xs[r] += (double)X[(int64_t)x * R + r];
+    for (int y = ya; y < yb; ++y)
+        for (int r = 0; r < R; ++r) sc->ys[r] += (double)Y[(int64_t)y * R + r];
+    double sum = 0.0;
+    for (int k = 0; k < 8; ++k) {
+        int64_t z = zmap ? zmap[zk[k]] : zk[k];
+        if (z < 0) return NAN;
+        sum += wk[k] * oracle_range_sum(d, C, sc->xs, sc->ys, Z + z * (int64_t)R);
+    }
+    return sum;
+}
+
+EXPORT void oracle_sample_batch(const oracle_desc* d, const float* C, const float* X, const float* Y, const float* Z,
+                                const int64_t* zmap, const oracle_rec* q, const float* xi /* [n][10] */, int64_t n,
+                                int32_t* pixel /* [n][2] */, double* prob, double* hxy /* [n][2] */,
+                                double* margin) {
+#pragma omp parallel
+    {
+        oracle_scratch* sc = (oracle_scratch*)malloc(sizeof(oracle_scratch));
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            int64_t zk[8];
+            double wk[8];
+            pixel[2 * i] = pixel[2 * i + 1] = -1;
+            prob[i] = NAN;
+            hxy[2 * i] = hxy[2 * i + 1] = NAN;
+            margin[i] = INFINITY;
+            if (!oracle_neighbours(d, &q[i], zk, wk)) continue;
+            int xa = (int)(q[i].rect & 255u), xb = (int)((q[i].rect >> 8) & 255u) + 1;
+            int ya = (int)((q[i].rect >> 16) & 255u), yb = (int)(q[i].rect >> 24) + 1;
+            const double root = oracle_rect_sum(d, C, X, Y, Z, zmap, zk, wk, xa, xb, ya, yb, sc);
+            if (!(root > 0.0)) { prob[i] = 0.0; continue; }
+            double last = root, mg = INFINITY;
+            for (int l = 0; xb - xa > 1 || yb - ya > 1; ++l) {
+                const int xm = xa + (xb - xa + 1) / 2, ym = ya + (yb - ya + 1) / 2;
+                const double Q[4] = {oracle_rect_sum(d, C, X, Y, Z, zmap, zk, wk, xa, xm, ya, ym, sc),
+                                     oracle_rect_sum(d, C, X, Y, Z, zmap, zk, wk, xm, xb, ya, ym, sc),
+                                     oracle_rect_sum(d, C, X, Y, Z, zmap, zk, wk, xa, xm, ym, yb, sc),
+                                     oracle_rect_sum(d, C, X, Y, Z, zmap, zk, wk, xm, xb, ym, yb, sc)};
+                const double tot = ((Q[0] + Q[1]) + Q[2]) + Q[3];
+                const double t = (double)xi[10 * i + l] * tot;
+                double c = 0.0;
+                int k = -1;
+                for (int j = 0; j < 4; ++j) {
+                    if (Q[j] > 0.0) {
+                        const double dist = fabs(t - c) / tot;  /* distance to this quad's lower edge */
+                        if (c > 0.0 && dist < mg) mg = dist;
+                    }
+                    c += Q[j];
+                    if (k < 0 && t < c) k = j;
+                }
+                if (k < 0) for (int j = 3; j >= 0; --j) if (Q[j] > 0.0) { k = j; break; }
+                if (k & 1) xa = xm; else xb = xm;
+                if (k & 2) ya = ym; else yb = ym;
+                last = Q[k];
+            }
+            pixel[2 * i] = xa;
+            pixel[2 * i + 1] = ya;
+            prob[i] = last / root;
+            hxy[2 * i] = ((double)xa + (double)xi[10 * i + 8]) * 2.0 / d->A - 1.0;
+            hxy[2 * i + 1] = ((double)ya + (double)xi[10 * i + 9]) * 2.0 / d->A - 1.0;
+            margin[i] = mg;
+        }
+        free(sc);
+    }
 }
 
 EXPORT int oracle_max_threads(void) { return omp_get_max_threads(); }
