@@ -42,6 +42,9 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--op", default="query", choices=["query", "sample"],
+                    help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
+                         "importance sampling over the whole A x A image")
     ap.add_argument("--queries", type=int, default=0, help="override the config's total query count")
     ap.add_argument("--bin", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--lanes", type=int, default=0)
@@ -394,6 +397,110 @@ def run_ours(args, cfg, rank, world, local_rank):
     return 0
 
 
+SAMPLE_METRIC = "NDF importance samples/sec (hierarchical quad descent, Sec. 5.2)"
+
+
+def sample_bytes(R: int, A: int) -> int:
+    """Per sample: record 16 + variates 40 + result 16 B, 8 Zc rows, 4 corner + 2 per level SAT rows of R fp32."""
+    levels = max(1, (A - 1).bit_length())
+    return 72 + 4 * R * (8 + 4 + 2 * levels)
+
+
+def run_sample_op(args, cfg, rank, world, local_rank):
+    """--op sample: pndf_sample_batch over the shard (domain = whole image), same timing rules."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    from paper_2109_14807_b200 import pndf
+    from paper_2109_14807_b200.shard import reduce_times_and_checksum, shard_range
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n_total = args.queries or min(cfg.n_queries, 10**8)
+    i0, i1 = shard_range(n_total, rank, world)
+    n = i1 - i0
+    bins, f = host_inputs(cfg)
+    Z = synth.build_z_exact_cuda(cfg, f.info["atom_map"], local_rank) if f.Z is None else f.Z
+    store = pndf.load_factors(pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap), f.C, f.X, f.Y, Z,
+                              device=local_rank)
+    del Z
+    torch.cuda.empty_cache()
+    h_q = torch.empty((n, 4), dtype=torch.int32)
+    recs = h_q.numpy().view(synth.QREC).reshape(-1)
+    synth.gen_queries(cfg, bins, i0, i1, out=recs)
+    recs["rect"] = synth.pack_rect(0, cfg.A - 1, 0, cfg.A - 1)
+    d_q = h_q.to(dev)
+    g = torch.Generator(device=dev)
+    g.manual_seed(1000 + rank)
+    d_xi = torch.rand((n, 10), generator=g, device=dev, dtype=torch.float32)
+    d_out = torch.empty((n, 4), dtype=torch.float32, device=dev)
+    opts = {"auto": pndf.BIN_AUTO, "on": pndf.BIN_ON, "off": pndf.BIN_OFF}[args.bin]
+    for _ in range(args.warmup):
+        store.sample_batch(d_q, d_xi, d_out, opts)
+        store.sync()
+    store.reset_stats()
+    l0 = store.stats()["kernel_launches"]
+    clocks = ClockSampler(bus_id_of(dev))
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        store.sample_batch(d_q, d_xi, d_out, opts | pndf.TIMING)
+        store.sync()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    st = store.stats()
+    ms_rank = e0.elapsed_time(e1) / args.steps
+    k_ms = st["query_ms"] / max(1, st["timed_batches"])
+    (ms_step, k_ms_max), _ = reduce_times_and_checksum([ms_rank, k_ms], 0.0, dev)
+    if rank != 0:
+        store.free()
+        return 0
+    peaks, _ = measured_peaks()
+    Bs = sample_bytes(cfg.R, cfg.A)
+    achieved = Bs * n / (k_ms * 1e-3) / 1e9
+    # parity on a sample of the timed batch (oracle sampler on the same variates)
+    idx = np.unique(np.random.default_rng(3).integers(0, n, min(n, 2000)))
+    rs = recs[idx]
+    xi = d_xi[torch.from_numpy(idx).to(dev)].cpu().numpy()
+    o = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy()
+    pix = o[:, 3].view(np.uint32)
+    d = oracle.desc_of(cfg)
+    rows, _ = oracle.neighbours(d, rs)
+    Zs, zmap = oracle.sparse_z(rows, cfg.P, lambda u: z_rows_for(cfg, f, u))
+    ref = oracle.sample_batch(d, f.C, f.X, f.Y, Zs, rs, xi, zmap=zmap)
+    firm = ref["margin"] > 1e-4
+    same = (pix & 0xffff == ref["pixel"][:, 0]) & (pix >> 16 == ref["pixel"][:, 1])
+    pdf_ref = ref["prob"] * cfg.A * cfg.A / 4.0
+    rel = np.abs(o[:, 2] - pdf_ref) / np.maximum(pdf_ref, 1e-30)
+    t0 = time.perf_counter()
+    ref2 = oracle.sample_batch(d, f.C, f.X, f.Y, Zs, rs, xi, zmap=zmap)
+    cpu_rate = rs.shape[0] / (time.perf_counter() - t0)
+    line = {"metric": SAMPLE_METRIC, "value": n_total / (ms_step * 1e-3), "unit": "samples/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(cfg) + "; importance sampling over the whole A x A image",
+                       "samples_total": n_total, "binned": bool(st["last_binned"]),
+                       "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]]},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "pndf::sample_kernel",
+                         "kernel_ms": k_ms, "bytes_per_sample": Bs},
+            "cpu_baseline": {"value": cpu_rate, "unit": "samples/s", "cores": oracle.max_threads(),
+                             "kind": "oracle", "sample": f"{rs.shape[0]} samples of the timed batch"},
+            "gpu_launches": int(st["kernel_launches"] - l0), "clocks": clk,
+            "parity_sample": {"checked": int(rs.shape[0]), "pixel_match_where_firm": bool(same[firm].all()),
+                              "firm": int(firm.sum()), "pdf_max_rel_err_firm": float(rel[firm].max())},
+            "e2e": None}
+    print(json.dumps(line), flush=True)
+    store.free()
+    return 0
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -408,6 +515,8 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl")
     try:
+        if args.op == "sample":
+            return run_sample_op(args, cfg, rank, world, local_rank)
         return run_ours(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:

@@ -108,6 +108,29 @@ pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float
 pndf_status pndf_query_batch(pndf_store s, const pndf_query* d_queries, int64_t n, float* d_out, uint32_t opts,
                              void* cuda_stream);
 
+/* One importance sample (16 bytes): the projected half vector (hx, hy) in
+ * [-1,1]^2, its density pdf = pmf / (2/A)^2 over the projected-h plane (the
+ * pmf is the sampled pixel's mass over the domain's mass), and the pixel
+ * x | y << 16.  No sample (blank domain, or invalid record): pixel = 0xffffffff,
+ * hx = hy = NaN, pdf = 0 (NaN for an invalid record). */
+typedef struct {
+    float hx, hy, pdf;
+    uint32_t pixel;
+} pndf_sample;
+
+/* Batched hierarchical importance sampling (Sec. 5.2; SURVEY §8(f)
+ * row 1).  For record i (footprint u, v, size; rect = the sampling domain, the
+ * whole A x A image for plain NDF sampling) descend from the domain by quads
+ * chosen with probability proportional to their range sums (Eq. 6), one
+ * variate xi[i][l] per level l (< 8 levels since A <= 256), down to a pixel,
+ * then jitter inside it with xi[i][8], xi[i][9].  d_xi is DEVICE memory
+ * [n][10] fp32 in [0,1), caller-supplied (any RNG); d_out [n] pndf_sample.
+ * opts: PNDF_BIN_* (binning by footprint like pndf_query_batch), PNDF_TIMING.
+ * Enqueued on cuda_stream; complete with pndf_sync.  Invalid records set the
+ * sticky PNDF_EQUERY. */
+pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
+                              pndf_sample* d_out, uint32_t opts, void* cuda_stream);
+
 /* Block until the store's work on cuda_stream is done; returns and clears the
  * sticky per-record error (PNDF_EQUERY) or a CUDA error. */
 pndf_status pndf_sync(pndf_store s, void* cuda_stream);

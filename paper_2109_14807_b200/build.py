@@ -1,10 +1,16 @@
-"""Build libpndf.so in-tree with nvcc for sm_100a (no JIT cache, so it travels with gpurun)."""
+"""Build libpndf.so in-tree with nvcc for sm_100a (no JIT cache, so it travels with gpurun).
+
+Each csrc/*.cu compiles to its own object in parallel (the query and sampling
+kernels are instantiated per SAT format in separate translation units), then
+nvcc links the shared library.  ptxas -v output goes to build/ptxas.log.
+"""
 from __future__ import annotations
 
 import glob
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
@@ -28,15 +34,37 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None, de
     if not force and out is None and not stale():
         return LIB
     nvcc = os.environ.get("NVCC", "nvcc")
-    tmp = target + f".{os.getpid()}.tmp"
-    cmd = [nvcc, "-shared", *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", os.path.join(ROOT, "include"),
-           *SOURCES, "-o", tmp]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    tag = os.path.splitext(os.path.basename(target))[0]
+    objdir = os.path.join(ROOT, "build", "obj", tag)
+    os.makedirs(objdir, exist_ok=True)
+    inc = ["-I", os.path.join(ROOT, "include")]
+    defs = [f"-D{d}" for d in defines]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src) + ".o")
+        cmd = [nvcc, "-c", *NVCC_FLAGS, *defs, *inc, src, "-o", obj]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return src, obj, r, cmd
+
+    with ThreadPoolExecutor(max_workers=max(1, min(len(SOURCES), os.cpu_count() or 4))) as ex:
+        results = list(ex.map(compile_one, SOURCES))
     os.makedirs(os.path.join(ROOT, "build"), exist_ok=True)
+    log = []
+    failed = False
+    for src, obj, r, cmd in results:
+        log.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        failed |= r.returncode != 0
+    tmp = target + f".{os.getpid()}.tmp"
+    if not failed:
+        cmd = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", *[o for _, o, _, _ in results],
+               "-o", tmp]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        log.append(" ".join(cmd) + "\n" + r.stdout + r.stderr)
+        failed = r.returncode != 0
     with open(os.path.join(ROOT, "build", "ptxas.log"), "w") as f:
-        f.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)
-    if r.returncode != 0:
-        sys.stderr.write(r.stderr[-4000:])
+        f.write("\n".join(log))
+    if failed:
+        sys.stderr.write("\n".join(log)[-4000:])
         raise RuntimeError("nvcc failed building libpndf.so (see build/ptxas.log)")
     os.replace(tmp, target)
     if verbose:

@@ -15,6 +15,28 @@ bool lanes_supported(int G, int NV);
 cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,
                          float* out, int num_sms, cudaStream_t st);
 
+// Sampling kernel (sample.cu); idx as for launch_query.
+cudaError_t launch_sample(const QParams& p, int G, int NV, const pndf_query* q, const float* xi, const uint32_t* idx,
+                          int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
+
+// per-variant instantiations (query_<fmt>_<border>.cu, sample_<fmt>_<border>.cu)
+cudaError_t launch_query_u32_wrap(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx,
+                                 int64_t n, float* out, int num_sms, cudaStream_t st);
+cudaError_t launch_sample_u32_wrap(int G, int NV, const QParams& p, const pndf_query* q, const float* xi,
+                                  const uint32_t* idx, int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
+cudaError_t launch_query_u32_clamp(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx,
+                                 int64_t n, float* out, int num_sms, cudaStream_t st);
+cudaError_t launch_sample_u32_clamp(int G, int NV, const QParams& p, const pndf_query* q, const float* xi,
+                                  const uint32_t* idx, int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
+cudaError_t launch_query_hilo_wrap(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx,
+                                 int64_t n, float* out, int num_sms, cudaStream_t st);
+cudaError_t launch_sample_hilo_wrap(int G, int NV, const QParams& p, const pndf_query* q, const float* xi,
+                                  const uint32_t* idx, int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
+cudaError_t launch_query_hilo_clamp(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx,
+                                 int64_t n, float* out, int num_sms, cudaStream_t st);
+cudaError_t launch_sample_hilo_clamp(int G, int NV, const QParams& p, const pndf_query* q, const float* xi,
+                                  const uint32_t* idx, int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
+
 int64_t scan_blocks(int64_t nb);
 int64_t radix_tiles(int64_t n);
 

@@ -1,0 +1,434 @@
+// query_kernel.cuh -- the query kernel template (rows a2-a6) and its launch
+// dispatch; instantiated per SAT format in query_u32.cu / query_hilo.cu so the
+// two halves compile in parallel.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+#include "launch.h"
+
+namespace pndf {
+
+// ------------------------------------------------- decoded query (smem) --
+// One warp decodes 32 records at once (one per lane) into these descriptors,
+// then the whole warp gathers for them G lanes per query.
+struct __align__(16) QDesc {
+    int32_t row[8];  // Zc rows of the 8 neighbours (level l0: (i0,j0),(i1,j0),(i0,j1),(i1,j1); then l0+1)
+    float w[8];      // trilinear weights (1-t)(1-a)(1-b), ...
+    uint32_t px;     // prefix entries x1 | (x2+1) << 16
+    uint32_t py;     // prefix entries y1 | (y2+1) << 16
+    float div;       // rectangle area (MEAN), 1 (SUM), NaN (invalid record)
+    int32_t out;     // output index within the (sub-)batch, -1 = no query
+};
+static_assert(sizeof(QDesc) == 80, "QDesc layout");
+
+// returns the reuse key (0xffffffff = never equal to a neighbour's)
+template <bool WRAP>
+__device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& rec, int32_t out_index, QDesc& d) {
+    int x1, x2, y1, y2;
+    if (!record_valid(p, rec, x1, x2, y1, y2)) {
+        atomicOr(p.err, 1u);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            d.row[k] = 0;
+            d.w[k] = 0.f;
+        }
+        d.px = 0;
+        d.py = 0;
+        d.div = __int_as_float(0x7fc00000);
+        d.out = out_index;
+        return 0xffffffffu;
+    }
+    int l0;
+    float t;
+    level_select(p, rec.size, l0, t);
+    int r0 = 0, r3 = 0, r4 = 0, r7 = 0;
+#pragma unroll
+    for (int dl = 0; dl < 2; ++dl) {
+        const int l = l0 + dl;
+        const float wl = dl ? t : 1.f - t;
+        int i0, i1, j0, j1;
+        float a, b;
+        axis_cells<WRAP>(p, rec.u, l, i0, i1, a);
+        axis_cells<WRAP>(p, rec.v, l, j0, j1, b);
+        const int32_t n = p.n0 >> l;
+        const int32_t off = (int32_t)level_offset(p.n0, l);
+        d.row[4 * dl + 0] = off + j0 * n + i0;
+        d.row[4 * dl + 1] = off + j0 * n + i1;
+        d.row[4 * dl + 2] = off + j1 * n + i0;
+        d.row[4 * dl + 3] = off + j1 * n + i1;
+        if (dl == 0) {
+            r0 = off + j0 * n + i0;
+            r3 = off + j1 * n + i1;
+        } else {
+            r4 = off + j0 * n + i0;
+            r7 = off + j1 * n + i1;
+        }
+        const float wa = wl * (1.f - a), wb = wl * a;
+        d.w[4 * dl + 0] = wa * (1.f - b);
+        d.w[4 * dl + 1] = wb * (1.f - b);
+        d.w[4 * dl + 2] = wa * b;
+        d.w[4 * dl + 3] = wb * b;
+    }
+    d.px = (uint32_t)x1 | ((uint32_t)(x2 + 1) << 16);
+    d.py = (uint32_t)y1 | ((uint32_t)(y2 + 1) << 16);
+    d.div = p.mean ? (float)((x2 - x1 + 1) * (y2 - y1 + 1)) : 1.f;
+    d.out = out_index;
+    if (WRAP) return cell_key(p, rec, l0, 1) & 0x7fffffffu;
+    // clamped borders: (i0, j0, i1, j1) on both levels pin the 8 rows; hash them
+    return (uint32_t)(r0 * 0x9E3779B1u ^ r3 * 0x85EBCA77u ^ r4 * 0xC2B2AE3Du ^ r7 * 0x27D4EB2Fu) & 0x7fffffffu;
+}
+
+// Reduce NB per-lane partials v[0..NB) over the G lanes of each group by
+// recursive halving: at level o the lanes with bit o set keep the upper half.
+// Every value is summed along the same pairing tree (xor G/2, G/4, ..., 1) as a
+// plain butterfly, so the result does not depend on the value's slot.
+// Afterwards lane gl holds the totals of slots (slot_base(gl) + i) for i < NB/G'.
+template <int G, int NB>
+__device__ __forceinline__ void group_reduce(float (&v)[NB], int gl) {
+    int nv = NB;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+        if (nv > 1) {
+            const bool upper = (gl & o) != 0;
+            const int half = nv / 2;
+#pragma unroll
+            for (int i = 0; i < NB / 2; ++i) {
+                if (i < half) {
+                    const float send = upper ? v[i] : v[i + half];
+                    const float keep = upper ? v[i + half] : v[i];
+                    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+                }
+            }
+            nv = half;
+        } else {
+            v[0] += __shfl_xor_sync(0xffffffffu, v[0], o);
+        }
+    }
+}
+
+// ------------------------------------------------------- query kernel --
+// Work split: CTA b owns the contiguous query range [b*chunk, (b+1)*chunk), so
+// binned (sorted) queries that share Zc rows run on the same SM and hit in L1.
+// Each warp takes 32 consecutive queries of the CTA's range at a time:
+//   1. decode: lane i decodes query i into a QDesc in shared memory, and notes
+//      whether it has the same 8 Zc rows as query i-1 (equal half-cell key);
+//   2. gather: G lanes per query (QPW = 32/G queries per step); each lane owns
+//      NV float4 rank chunks at float offsets (gl + v*G)*4, so a query's G lanes
+//      read each row slice contiguously (RP = 4*G*NV is a compile-time stride).
+//      With G == 32 the previous query's Zc rows stay in registers and are not
+//      re-read when the rows repeat (binned neighbours);
+//   3. reduce: per-lane partials of 8 steps are reduced together over the G lanes
+//      (group_reduce: 1 shuffle per query instead of log2 G, and no shuffle chain
+//      between consecutive queries), then routed to lane (query index) and the
+//      warp writes 32 results at once.
+// A query's result never depends on where it sits in the batch, so binned and
+// unbinned batches are bitwise identical.
+constexpr int kWarpsPerBlock = kThreads / 32;
+#ifndef PNDF_MINB
+#define PNDF_MINB 2  // min resident blocks per SM (tuned on B200: 2 beats 1 and 3, see profiles/)
+#endif
+#ifndef PNDF_KSTEPS
+#define PNDF_KSTEPS 8
+#endif
+constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced together
+
+#ifndef PNDF_TMA
+#define PNDF_TMA 0  // 1: stage SAT rows of the next query in smem with TMA bulk copies (measured slower on B200)
+#endif
+constexpr int kSlots = 2;  // per-warp SAT staging slots (prefetch distance 1)
+
+// SAT rows are staged by TMA when a warp runs one query per step (G == 32) and a
+// slot (4 rows) is at most 4 KB, so 8 warps x 2 slots fit beside the descriptors.
+template <int G, int NV, bool U32>
+struct QLayout {
+    static constexpr int RP = 4 * G * NV;
+    static constexpr int PSTRIDE = U32 ? RP : 2 * RP;  // floats (or uint32) per SAT entry row
+    static constexpr bool TMA = PNDF_TMA && G == 32 && PSTRIDE <= 256;
+    static constexpr int ROW_BYTES = PSTRIDE * 4;
+    static constexpr size_t DESC = sizeof(QDesc) * kWarpsPerBlock * 32;
+    static constexpr size_t REUSE = 128;
+    static constexpr size_t BARS = TMA ? 128 : 0;
+    static constexpr size_t SLOTS = TMA ? (size_t)kWarpsPerBlock * kSlots * 4 * ROW_BYTES : 0;
+    static constexpr size_t BYTES = DESC + REUSE + BARS + SLOTS;
+};
+
+template <int G, int NV, bool WRAP, bool BINNED, bool U32>
+__global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParams p, const pndf_query* __restrict__ q,
+                                                         const uint32_t* __restrict__ idx, int64_t n,
+                                                         int64_t chunk, float* __restrict__ out) {
+    using LY = QLayout<G, NV, U32>;
+    constexpr int QPW = 32 / G;
+    constexpr int RP = LY::RP;
+    constexpr int NSTEP = 32 / QPW;                       // steps per 32-query warp batch
+    constexpr int SB = NSTEP < kSteps ? NSTEP : kSteps;   // steps per reduction batch
+    constexpr int VPL = SB / G > 0 ? SB / G : 1;          // reduced values left per lane
+    constexpr bool TMA = LY::TMA;
+    extern __shared__ __align__(128) unsigned char qsmem[];
+    QDesc(*sdesc)[32] = reinterpret_cast<QDesc(*)[32]>(qsmem);
+    uint32_t* sreuse = reinterpret_cast<uint32_t*>(qsmem + LY::DESC);  // bit j: query j repeats j-1's rows
+    uint64_t* sbar = reinterpret_cast<uint64_t*>(qsmem + LY::DESC + LY::REUSE);
+    uint32_t* sslot = reinterpret_cast<uint32_t*>(qsmem + LY::DESC + LY::REUSE + LY::BARS);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int gl = lane % G, grp = lane / G;
+    QDesc* wd = sdesc[warp];
+    const float* __restrict__ Zc = p.Zc;
+    // SAT rows: HILO = [hi row | lo row] per entry (stride 2*RP floats), U32 = one uint32 row
+    constexpr int PSTRIDE = LY::PSTRIDE;
+    const float* __restrict__ PX = p.PXY;
+    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * PSTRIDE;
+    uint64_t* wbar = sbar + warp * kSlots;
+    uint32_t* wslot = sslot + (size_t)warp * kSlots * 4 * PSTRIDE;
+    uint32_t phase = 0;  // bit k: parity of slot k's next completion
+    if (TMA) {
+        if (lane == 0)
+            for (int k = 0; k < kSlots; ++k) mbar_init(wbar + k, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        __syncwarp();
+    }
+    // lane 0: TMA the 4 SAT rows (x1, x2+1, y1, y2+1) of warp-batch query s into slot s % kSlots
+    auto issue_sat = [&](int s) {
+        if (lane == 0) {
+            const QDesc& d = wd[s];
+            const int k = s % kSlots;
+            uint32_t* dst = wslot + (size_t)k * 4 * PSTRIDE;
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot was last read by the generic proxy
+            mbar_arrive_expect_tx(wbar + k, 4 * LY::ROW_BYTES);
+            tma_load_1d(dst + 0 * PSTRIDE, PX + (size_t)(d.px & 0xffffu) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+            tma_load_1d(dst + 1 * PSTRIDE, PX + (size_t)(d.px >> 16) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+            tma_load_1d(dst + 2 * PSTRIDE, PY + (size_t)(d.py & 0xffffu) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+            tma_load_1d(dst + 3 * PSTRIDE, PY + (size_t)(d.py >> 16) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+        }
+    };
+
+    const int64_t c0 = (int64_t)blockIdx.x * chunk;
+    const int64_t c1 = min(n, c0 + chunk);
+    float4 zc[NV][8];
+    for (int64_t base = c0 + (int64_t)warp * 32; base < c1; base += (int64_t)kWarpsPerBlock * 32) {
+        // 1. decode 32 records, one per lane
+        {
+            const int64_t qi = base + lane;
+            uint32_t key = 0xffffffffu;
+            if (qi < c1) {
+                // binned: idx is the radix-sorted permutation; gather the record through it
+                const int64_t src = BINNED ? (int64_t)__ldg(idx + qi) : qi;
+                const pndf_query rec = ldg_query(q + src);
+                key = decode<WRAP>(p, rec, (int32_t)src, wd[lane]);
+            } else {
+                wd[lane].out = -1;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    wd[lane].row[k] = 0;
+                    wd[lane].w[k] = 0.f;
+                }
+                wd[lane].px = 0;
+                wd[lane].py = 0;
+                wd[lane].div = 1.f;
+            }
+            const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
+            const uint32_t same = __ballot_sync(0xffffffffu, lane > 0 && key == prev && key != 0xffffffffu);
+            if (lane == 0) sreuse[warp] = same;
+        }
+        __syncwarp();
+        const uint32_t reuse_mask = (G == 32) ? sreuse[warp] : 0u;
+        if (TMA) issue_sat(0);
+        // 2-3. gather + batched reduce
+        float res = 0.f;
+#pragma unroll 1
+        for (int s0 = 0; s0 < NSTEP; s0 += SB) {
+            float part[SB];
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+                const int s = s0 + j;  // step: queries s*QPW + grp
+                const QDesc& d = wd[s * QPW + grp];
+                if (TMA) {
+                    if (s + 1 < NSTEP) issue_sat(s + 1);  // prefetch the next query's SAT rows
+                    const int k = s % kSlots;
+                    while (!mbar_try_wait(wbar + k, (phase >> k) & 1u)) {
+                    }
+                    phase ^= 1u << k;
+                }
+                const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
+                const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
+                const uint2 tail = *reinterpret_cast<const uint2*>(&d.px);
+                const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
+                const float* px0 = PX + (size_t)(tail.x & 0xffffu) * PSTRIDE;
+                const float* px1 = PX + (size_t)(tail.x >> 16) * PSTRIDE;
+                const float* py0 = PY + (size_t)(tail.y & 0xffffu) * PSTRIDE;
+                const float* py1 = PY + (size_t)(tail.y >> 16) * PSTRIDE;
+                // warp-uniform for G == 32 (every lane reads the same descriptor)
+                const bool reuse = (G == 32) && s > 0 && ((reuse_mask >> s) & 1u);
+                if (!reuse) {
+                    const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
+                    const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
+                    const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
+                                        (int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
+#pragma unroll
+                    for (int v = 0; v < NV; ++v)
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) zc[v][k] = ldg4(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
+                }
+                float acc = 0.f;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const int c = (gl + v * G) * 4;
+                    float4 dx, dy;
+                    const uint32_t* sl = wslot + (size_t)(s % kSlots) * 4 * PSTRIDE;
+                    if (TMA && U32) {
+                        const uint4 qx0 = *reinterpret_cast<const uint4*>(sl + 0 * PSTRIDE + c);
+                        const uint4 qx1 = *reinterpret_cast<const uint4*>(sl + 1 * PSTRIDE + c);
+                        const uint4 qy0 = *reinterpret_cast<const uint4*>(sl + 2 * PSTRIDE + c);
+                        const uint4 qy1 = *reinterpret_cast<const uint4*>(sl + 3 * PSTRIDE + c);
+                        dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                         __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                        dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                         __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                    } else if (TMA) {
+                        const float* sf = reinterpret_cast<const float*>(sl);
+                        const float4 xh0 = *reinterpret_cast<const float4*>(sf + 0 * PSTRIDE + c);
+                        const float4 xl0 = *reinterpret_cast<const float4*>(sf + 0 * PSTRIDE + RP + c);
+                        const float4 xh1 = *reinterpret_cast<const float4*>(sf + 1 * PSTRIDE + c);
+                        const float4 xl1 = *reinterpret_cast<const float4*>(sf + 1 * PSTRIDE + RP + c);
+                        const float4 yh0 = *reinterpret_cast<const float4*>(sf + 2 * PSTRIDE + c);
+                        const float4 yl0 = *reinterpret_cast<const float4*>(sf + 2 * PSTRIDE + RP + c);
+                        const float4 yh1 = *reinterpret_cast<const float4*>(sf + 3 * PSTRIDE + c);
+                        const float4 yl1 = *reinterpret_cast<const float4*>(sf + 3 * PSTRIDE + RP + c);
+                        dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                         (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                        dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                         (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                    } else if (U32) {
+                        // exact integer differences of the fixed-point SATs (scale folded into Zc)
+                        const uint4 qx1 = __ldg(reinterpret_cast<const uint4*>(px1 + c));
+                        const uint4 qx0 = __ldg(reinterpret_cast<const uint4*>(px0 + c));
+                        const uint4 qy1 = __ldg(reinterpret_cast<const uint4*>(py1 + c));
+                        const uint4 qy0 = __ldg(reinterpret_cast<const uint4*>(py0 + c));
+                        dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                         __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                        dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                         __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                    } else {
+                        // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
+                        // under cancellation (Sterbenz), lo carries the fp64 residual.
+                        const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
+                        const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
+                        const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
+                        const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
+                        dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                         (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                        dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                         (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                    }
+                    float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        z.x = fmaf(w[k], zc[v][k].x, z.x);
+                        z.y = fmaf(w[k], zc[v][k].y, z.y);
+                        z.z = fmaf(w[k], zc[v][k].z, z.z);
+                        z.w = fmaf(w[k], zc[v][k].w, z.w);
+                    }
+                    acc = fmaf(dx.x * dy.x, z.x, acc);
+                    acc = fmaf(dx.y * dy.y, z.y, acc);
+                    acc = fmaf(dx.z * dy.z, z.z, acc);
+                    acc = fmaf(dx.w * dy.w, z.w, acc);
+                }
+                part[j] = acc;
+                if (TMA) __syncwarp();  // every lane is done with this slot before it is refilled
+            }
+            group_reduce<G, SB>(part, gl);
+            // lane gl holds slots [slot0, slot0 + VPL) of its group: slot bits from the halving levels
+            int slot0 = 0;
+            {
+                int nv = SB, o = G / 2;
+                while (nv > 1 && o > 0) {
+                    nv >>= 1;
+                    if (gl & o) slot0 += nv;
+                    o >>= 1;
+                }
+            }
+            // route: query (s0 + j) * QPW + g of this batch goes to lane (s0 + j) * QPW + g
+#pragma unroll
+            for (int i = 0; i < VPL; ++i) {
+                const int dst_rel = lane - s0 * QPW;  // this lane's query, relative to the batch
+                const int j = dst_rel / QPW, g = dst_rel % QPW;
+                // source lane: group g, a lane whose slot range starts at j - (j % VPL) when i == j % VPL
+                int src_gl = 0;
+                {
+                    int nv = SB, o = G / 2, rem = j;
+                    while (nv > 1 && o > 0) {
+                        nv >>= 1;
+                        if (rem >= nv) {
+                            src_gl |= o;
+                            rem -= nv;
+                        }
+                        o >>= 1;
+                    }
+                }
+                const float got = __shfl_sync(0xffffffffu, part[i], (g * G + src_gl) & 31);
+                const bool mine = dst_rel >= 0 && dst_rel < SB * QPW && (j % VPL) == i;
+                if (mine) res = got;
+            }
+            (void)slot0;
+        }
+        const QDesc& mine = wd[lane];
+        const int32_t oi = mine.out;
+        const float div = mine.div;
+        __syncwarp();
+        if (oi >= 0) out[oi] = res / div;  // a6: Eq. 6 mean (div = area) or sum (div = 1)
+    }
+}
+
+// ----------------------------------------------------------- launchers --
+template <int G, int NV, bool W, bool B, bool U>
+static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
+                            int num_sms, cudaStream_t st) {
+    constexpr size_t smem = QLayout<G, NV, U>::BYTES;
+    cudaFuncSetAttribute(query_kernel<G, NV, W, B, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    static int occ = -1;
+    if (occ < 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, query_kernel<G, NV, W, B, U>, kThreads, smem) !=
+                cudaSuccess ||
+            occ < 1)
+            occ = 1;
+    }
+    int64_t grid = (int64_t)num_sms * occ;
+    const int64_t need = (n + kThreads - 1) / kThreads;  // at least one query per lane per block
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    int64_t chunk = (n + grid - 1) / grid;
+    chunk = (chunk + 31) / 32 * 32;
+    grid = (n + chunk - 1) / chunk;
+    query_kernel<G, NV, W, B, U><<<(unsigned)grid, kThreads, smem, st>>>(p, q, idx, n, chunk, out);
+    return cudaGetLastError();
+}
+
+template <int G, bool W, bool B, bool U>
+static cudaError_t dispatch_nv(int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
+                               float* out, int num_sms, cudaStream_t st) {
+    switch (NV) {
+        case 1: return launch_q<G, 1, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 2: return launch_q<G, 2, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 3: return launch_q<G, 3, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 4: return launch_q<G, 4, W, B, U>(p, q, idx, n, out, num_sms, st);
+        case 8: return launch_q<G, 8, W, B, U>(p, q, idx, n, out, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool W, bool B, bool U>
+static cudaError_t dispatch_g(int G, int NV, const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n,
+                              float* out, int num_sms, cudaStream_t st) {
+    switch (G) {
+        case 1: return dispatch_nv<1, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 2: return dispatch_nv<2, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 4: return dispatch_nv<4, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 8: return dispatch_nv<8, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 16: return dispatch_nv<16, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        case 32: return dispatch_nv<32, W, B, U>(NV, p, q, idx, n, out, num_sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace pndf

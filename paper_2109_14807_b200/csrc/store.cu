@@ -462,6 +462,45 @@ pndf_status pndf_query_batch(pndf_store s, const pndf_query* d_queries, int64_t 
     return r;
 }
 
+pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
+                              pndf_sample* d_out, uint32_t opts, void* cuda_stream) {
+    if (!s || n < 0 || (n > 0 && (!d_queries || !d_xi || !d_out))) return PNDF_EINVAL;
+    if (opts & ~(PNDF_BIN_ON | PNDF_BIN_OFF | PNDF_TIMING)) return PNDF_EINVAL;
+    if ((opts & PNDF_BIN_ON) && (opts & PNDF_BIN_OFF)) return PNDF_EINVAL;
+    if (n == 0) return PNDF_OK;
+    if ((uintptr_t)d_queries % 16 != 0 || (uintptr_t)d_out % 16 != 0 || (uintptr_t)d_xi % 4 != 0)
+        return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const bool timing = (opts & PNDF_TIMING) != 0;
+    const bool binned = want_bins(s, n, opts);
+    if ((opts & PNDF_BIN_ON) && s->nbins == 0) return PNDF_EINVAL;
+    int launches = 0;
+    if (timing) CK(cudaEventRecord(s->ev[0], st));
+    const int64_t step = int64_t(1) << 30;
+    if (binned) {
+        pndf_status r = ensure_scratch(s->main, std::min(n, step), st);
+        if (r != PNDF_OK) return r;
+    }
+    bool first = true;
+    for (int64_t a = 0; a < n; a += step) {
+        const int64_t m = std::min(step, n - a);
+        const uint32_t* perm = nullptr;
+        if (binned) CK(launch_binning(s->qp, d_queries + a, m, s->P, s->main, s->num_sms, st, &launches, &perm));
+        if (timing && first) CK(cudaEventRecord(s->ev[1], st));
+        CK(launch_sample(s->qp, s->G, s->NV, d_queries + a, d_xi + (size_t)a * 10, perm, m, d_out + a, s->num_sms,
+                         st));
+        launches += 1;
+        first = false;
+    }
+    if (timing) CK(cudaEventRecord(s->ev[2], st));
+    s->stats.kernel_launches += (uint64_t)launches;
+    s->stats.last_binned = binned ? 1 : 0;
+    s->timing_pending = timing;
+    return PNDF_OK;
+}
+
 pndf_status pndf_sync(pndf_store s, void* cuda_stream) {
     if (!s) return PNDF_EINVAL;
     std::lock_guard<std::mutex> lk(s->mu);

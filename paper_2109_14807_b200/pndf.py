@@ -52,7 +52,10 @@ class StoreStats(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
-EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sync", "pndf_query_batch_host", "pndf_free",
+SAMPLE_DTYPE = np.dtype([("hx", "<f4"), ("hy", "<f4"), ("pdf", "<f4"), ("pixel", "<u4")])
+
+EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_sync", "pndf_query_batch_host",
+           "pndf_free",
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes")
 
@@ -72,6 +75,8 @@ def lib():
         L.pndf_load_factors.argtypes = [ctypes.POINTER(Desc), P, P, P, P, ctypes.c_int, P, ctypes.POINTER(P)]
         L.pndf_query_batch.restype = i32
         L.pndf_query_batch.argtypes = [P, P, i64, P, u32, P]
+        L.pndf_sample_batch.restype = i32
+        L.pndf_sample_batch.argtypes = [P, P, P, i64, P, u32, P]
         L.pndf_sync.restype = i32
         L.pndf_sync.argtypes = [P, P]
         L.pndf_query_batch_host.restype = i32
@@ -160,6 +165,14 @@ class Store:
         n = out.shape[0] if n is None else n
         _check(lib().pndf_query_batch(self.handle, _ptr(queries), n, _ptr(out), opts, _stream(stream)),
                "pndf_query_batch")
+
+    def sample_batch(self, queries, xi, out, opts: int = 0, stream=None, n: int | None = None):
+        """Enqueue pndf_sample_batch: queries = device records (rect = sampling domain), xi = device
+        float32 [n, 10] variates in [0,1), out = device buffer of n 16-byte pndf_sample records
+        (e.g. int32/float32 [n, 4])."""
+        n = xi.shape[0] if n is None else n
+        _check(lib().pndf_sample_batch(self.handle, _ptr(queries), _ptr(xi), n, _ptr(out), opts, _stream(stream)),
+               "pndf_sample_batch")
 
     def sync(self, stream=None, raise_on_query_error: bool = True) -> int:
         st = lib().pndf_sync(self.handle, _stream(stream))
