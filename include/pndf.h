@@ -172,6 +172,12 @@ pndf_status pndf_store_stats_reset(pndf_store s);
  * [z0, z1) as [z1-z0][Rp] fp32.  Either pointer may be NULL. */
 pndf_status pndf_store_image(pndf_store s, float* PXY, float* Zc, int64_t z0, int64_t z1);
 
+/* Test support: run only the binning pass (row a1) on n device records and copy
+ * the permutation (query indices in binned order) to d_perm [n] and, if not
+ * NULL, the sorted bin keys to d_keys [n] (device memory).  Synchronous. */
+pndf_status pndf_bin_permutation(pndf_store s, const pndf_query* d_queries, int64_t n, uint32_t* d_perm,
+                                 uint32_t* d_keys);
+
 /* Tuning knob (bench / tests): lanes per query G in {1,2,4,8,16,32} with
  * G*4 dividing Rp; 0 restores the default chosen at load. */
 pndf_status pndf_set_lanes(pndf_store s, int32_t lanes);

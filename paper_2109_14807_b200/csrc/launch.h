@@ -44,7 +44,8 @@ int64_t radix_tiles(int64_t n);
 // *perm receives the device permutation (query indices in binned order).
 // Scratch: keys/vals [cap], counts [radix_tiles(cap)*512], bsum [scan_blocks(that)].
 cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int64_t P, BinScratch& sc,
-                           int num_sms, cudaStream_t st, int* launches, const uint32_t** perm);
+                           int num_sms, cudaStream_t st, int* launches, const uint32_t** perm,
+                           const uint32_t** sorted_keys = nullptr);
 
 // Store build kernels (build.cu).
 cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float* Mdev, float* Zc_dst, int Rp,

@@ -324,7 +324,8 @@ int64_t bin_key_space(int64_t P, int* half) {
 }
 
 cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int64_t P, BinScratch& sc,
-                           int num_sms, cudaStream_t st, int* launches, const uint32_t** perm) {
+                           int num_sms, cudaStream_t st, int* launches, const uint32_t** perm,
+                           const uint32_t** sorted_keys) {
     int half;
     const int64_t nkeys = bin_key_space(P, &half);
     int kbits = 1;
@@ -350,6 +351,7 @@ cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int
         *launches += 5;
     }
     *perm = vals;
+    if (sorted_keys) *sorted_keys = sc.keys[cur];
     return cudaGetLastError();
 }
 

@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 #pragma unroll
                     for (int v = 0; v < NV; ++v)
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) zc[v][k] = ldg4(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
+                        for (int k = 0; k < 8; ++k) zc[v][k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
                 }
                 float acc = 0.f;
 #pragma unroll
@@ -301,10 +301,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                                          (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
                     } else if (U32) {
                         // exact integer differences of the fixed-point SATs (scale folded into Zc)
-                        const uint4 qx1 = __ldg(reinterpret_cast<const uint4*>(px1 + c));
-                        const uint4 qx0 = __ldg(reinterpret_cast<const uint4*>(px0 + c));
-                        const uint4 qy1 = __ldg(reinterpret_cast<const uint4*>(py1 + c));
-                        const uint4 qy0 = __ldg(reinterpret_cast<const uint4*>(py0 + c));
+                        const uint4 qx1 = ldg_sat(px1 + c);
+                        const uint4 qx0 = ldg_sat(px0 + c);
+                        const uint4 qy1 = ldg_sat(py1 + c);
+                        const uint4 qy0 = ldg_sat(py0 + c);
                         dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
                                          __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
                         dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),

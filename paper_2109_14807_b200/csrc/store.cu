@@ -614,6 +614,25 @@ pndf_status pndf_store_image(pndf_store s, float* PXY, float* Zc, int64_t z0, in
     return PNDF_OK;
 }
 
+pndf_status pndf_bin_permutation(pndf_store s, const pndf_query* d_queries, int64_t n, uint32_t* d_perm,
+                                 uint32_t* d_keys) {
+    if (!s || n < 0 || (n > 0 && (!d_queries || !d_perm))) return PNDF_EINVAL;
+    if (n == 0) return PNDF_OK;
+    if (n > (int64_t(1) << 30) || s->nbins == 0) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    pndf_status r = ensure_scratch(s->main, n, nullptr);
+    if (r != PNDF_OK) return r;
+    int launches = 0;
+    const uint32_t *perm = nullptr, *keys = nullptr;
+    CK(launch_binning(s->qp, d_queries, n, s->P, s->main, s->num_sms, nullptr, &launches, &perm, &keys));
+    CK(cudaMemcpyAsync(d_perm, perm, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, nullptr));
+    if (d_keys) CK(cudaMemcpyAsync(d_keys, keys, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, nullptr));
+    CK(cudaStreamSynchronize(nullptr));
+    s->stats.kernel_launches += (uint64_t)launches;
+    return PNDF_OK;
+}
+
 pndf_status pndf_set_lanes(pndf_store s, int32_t lanes) {
     if (!s) return PNDF_EINVAL;
     std::lock_guard<std::mutex> lk(s->mu);

@@ -57,7 +57,7 @@ SAMPLE_DTYPE = np.dtype([("hx", "<f4"), ("hy", "<f4"), ("pdf", "<f4"), ("pixel",
 EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_sync", "pndf_query_batch_host",
            "pndf_free",
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
-           "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes")
+           "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation")
 
 _lib = None
 
@@ -93,6 +93,8 @@ def lib():
         L.pndf_store_stats_reset.argtypes = [P]
         L.pndf_store_image.restype = i32
         L.pndf_store_image.argtypes = [P, P, P, i64, i64]
+        L.pndf_bin_permutation.restype = i32
+        L.pndf_bin_permutation.argtypes = [P, P, i64, P, P]
         L.pndf_set_lanes.restype = i32
         L.pndf_set_lanes.argtypes = [P, i32]
         _lib = L
@@ -210,6 +212,11 @@ class Store:
         zc = np.empty((z1 - z0, Rp), np.float32)
         _check(lib().pndf_store_image(self.handle, _ptr(pxy), _ptr(zc), z0, z1), "pndf_store_image")
         return pxy, zc
+
+    def bin_permutation(self, queries, perm, keys=None):
+        """Test support: binning pass only -> permutation (and sorted keys) in device buffers."""
+        _check(lib().pndf_bin_permutation(self.handle, _ptr(queries), perm.shape[0], _ptr(perm), _ptr(keys)),
+               "pndf_bin_permutation")
 
     def set_lanes(self, lanes: int):
         _check(lib().pndf_set_lanes(self.handle, lanes), "pndf_set_lanes")

@@ -311,3 +311,43 @@ def test_cuda_graph_replay():
         s.synchronize()
     assert out.cpu().numpy().tobytes() == first.cpu().numpy().tobytes()
     st.free()
+
+
+@pytest.mark.parametrize("k", [3, 5])
+def test_binning_sorts_by_half_cell_key(k):
+    """Row a1: the radix sort returns a permutation whose keys are nondecreasing, and each key is the
+    record's half cell on its lower level (recomputed here in numpy from the DESIGN.md definition)."""
+    import math
+    pndf = _pndf()
+    cfg = synth.CONFIGS[k].scaled(N=512) if k == 5 else synth.CONFIGS[k]
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    f = synth.build_factors(cfg, nxy, bins)
+    n = 300_001
+    recs = synth.gen_queries(cfg, bins, 0, n)
+    st = pndf.load_factors(pndf.make_desc(**desc_args(cfg)), f.C, f.X, f.Y, f.Z)
+    perm = torch.empty(n, dtype=torch.int32, device="cuda")
+    keys = torch.empty(n, dtype=torch.int32, device="cuda")
+    st.bin_permutation(torch_records(recs), perm, keys)
+    p = perm.cpu().numpy().view(np.uint32).astype(np.int64)
+    kk = keys.cpu().numpy().view(np.uint32).astype(np.int64)
+    st.free()
+    assert np.array_equal(np.sort(p), np.arange(n))
+    assert (np.diff(kk) >= 0).all()
+    # key of record i: 4*off_l0 + Morton(floor(2 f_u) mod 2n, floor(2 f_v) mod 2n)
+    S = recs["size"].astype(np.float64)
+    l0 = np.clip(np.floor(np.log2(S / cfg.s0)), 0, cfg.L - 2).astype(np.int64)
+    n0 = cfg.N // cfg.s0
+    nl = n0 >> l0
+    off = np.array([sum((n0 >> m) ** 2 for m in range(l)) for l in range(cfg.L)], np.int64)[l0]
+    def half(u):
+        fu = u.astype(np.float64) / (cfg.s0 * (1 << l0).astype(np.float64)) - 0.5
+        return np.floor(2 * fu).astype(np.int64) & (2 * nl - 1)
+    hu, hv = half(recs["u"]), half(recs["v"])
+    def spread(x):
+        out = np.zeros_like(x)
+        for b in range(20):
+            out |= ((x >> b) & 1) << (2 * b)
+        return out
+    want = 4 * off + (spread(hu) | (spread(hv) << 1))
+    assert np.array_equal(kk, want[p])
