@@ -52,6 +52,7 @@ def lib():
                                          ctypes.c_int]
         L.oracle_neighbours_batch.argtypes = [ctypes.POINTER(Desc), P, ctypes.c_int64, P, P]
         L.oracle_sample_batch.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, P, P, ctypes.c_int64, P, P, P, P]
+        L.oracle_sg_rects.argtypes = [P, ctypes.c_int64, ctypes.c_double, ctypes.c_int, P, P, P, P]
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -116,6 +117,21 @@ def sample_batch(desc: Desc, C, X, Y, Z, records: np.ndarray, xi: np.ndarray, zm
     lib().oracle_sample_batch(ctypes.byref(desc), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(zmap), _ptr(recs),
                               _ptr(xi), n, _ptr(pix), _ptr(prob), _ptr(h), _ptr(mg))
     return dict(pixel=pix, prob=prob, h=h, margin=mg)
+
+
+def sg_rects(sg: np.ndarray, A: int, eps: float = 0.3):
+    """Environment prefiltering (Sec. 5.4): compact-eps support angle theta, square side Q and the
+    angular rectangle of each 32-byte SG-light record (u, v, size, hx, hy, lambda, amplitude, pad).
+    Returns dict(theta, Q, rect uint32, q_margin)."""
+    sg = np.ascontiguousarray(sg)
+    assert sg.dtype.itemsize == 32
+    n = sg.shape[0]
+    th = np.empty(n, np.float64)
+    Q = np.empty(n, np.float64)
+    rect = np.empty(n, np.uint32)
+    mg = np.empty(n, np.float64)
+    lib().oracle_sg_rects(_ptr(sg), n, eps, A, _ptr(th), _ptr(Q), _ptr(rect), _ptr(mg))
+    return dict(theta=th, Q=Q, rect=rect, q_margin=mg)
 
 
 def neighbours(desc: Desc, records: np.ndarray):

@@ -288,4 +288,50 @@ EXPORT void oracle_sample_batch(const oracle_desc* d, const float* C, const floa
     }
 }
 
+/* ------------------------------------------------------------------------
+ * Environment prefiltering (Sec. 5.4).  A spherical Gaussian with
+ * amplitude A and bandwidth lambda has compact-eps support
+ *     theta = arccos((ln eps - ln A) / lambda + 1)           (eps = 0.3)
+ * and the NDF is blurred over a square of side
+ *     Q = 256 (theta/2)/pi * 2 = 256 theta / pi             (P:426-428, 256 = NDF resolution)
+ * Readings: the resolution is the store's A (Q = A theta/pi); an
+ * arccos argument below -1 gives theta = pi, above 1 gives theta = 0;
+ * the side is floor(Q + 1/2) clamped to [1, A]; the square is centred on the bin
+ * of the projected half vector (bin = min(floor((h+1)A/2), A-1)) and shifted to
+ * stay inside the grid (x1 = clamp(c - (side-1)/2, 0, A - side)).
+ * Outputs theta, Q and the packed rectangle; q_margin is the distance of Q from
+ * the nearest rounding boundary (x.5), used by tests to accept either side there.
+ */
+typedef struct { float u, v, size, hx, hy, lambda, amplitude, pad; } oracle_sgrec;
+
+static int oracle_bin(double h, int A) {
+    int b = (int)floor((h + 1.0) * 0.5 * A);
+    return b < 0 ? 0 : (b > A - 1 ? A - 1 : b);
+}
+
+EXPORT void oracle_sg_rects(const oracle_sgrec* in, int64_t n, double eps, int A, double* theta, double* Q,
+                            uint32_t* rect, double* q_margin) {
+#pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i) {
+        double arg = (log(eps) - log((double)in[i].amplitude)) / (double)in[i].lambda + 1.0;
+        double th = arg <= -1.0 ? M_PI : (arg >= 1.0 ? 0.0 : acos(arg));
+        double q = (double)A * th / M_PI;
+        int side = (int)floor(q + 0.5);
+        if (side < 1) side = 1;
+        if (side > A) side = A;
+        double fr = q + 0.5 - floor(q + 0.5);
+        q_margin[i] = fr < 1.0 - fr ? fr : 1.0 - fr;
+        int cx = oracle_bin((double)in[i].hx, A), cy = oracle_bin((double)in[i].hy, A);
+        int x1 = cx - (side - 1) / 2, y1 = cy - (side - 1) / 2;
+        if (x1 > A - side) x1 = A - side;
+        if (x1 < 0) x1 = 0;
+        if (y1 > A - side) y1 = A - side;
+        if (y1 < 0) y1 = 0;
+        theta[i] = th;
+        Q[i] = q;
+        rect[i] = (uint32_t)x1 | ((uint32_t)(x1 + side - 1) << 8) | ((uint32_t)y1 << 16) |
+                  ((uint32_t)(y1 + side - 1) << 24);
+    }
+}
+
 EXPORT int oracle_max_threads(void) { return omp_get_max_threads(); }

@@ -74,6 +74,7 @@ def lib():
         L.synth_hist_tensor.argtypes = [i32, P, i32, i32, i32, P]
         L.synth_atom_profiles.argtypes = [i32, i32, P, f64, P, P]
         L.synth_gen_queries.argtypes = [ctypes.POINTER(_QDist), u64, i64, i64, P, P]
+        L.synth_gen_sg_lights.argtypes = [ctypes.POINTER(_QDist), u64, i64, i64, f64, f64, f64, f64, f64, P]
         L.synth_max_threads.restype = i32
         _lib = L
     return _lib
@@ -336,6 +337,24 @@ def gen_queries(cfg: Config, bins: np.ndarray | None, i0: int = 0, i1: int | Non
     assert out.dtype == QREC and out.shape[0] == i1 - i0
     lib().synth_gen_queries(ctypes.byref(qd), seed, i0, i1,
                             None if bins is None else _p(np.ascontiguousarray(bins)), _p(out))
+    return out
+
+
+SGREC = np.dtype([("u", "<f4"), ("v", "<f4"), ("size", "<f4"), ("hx", "<f4"), ("hy", "<f4"),
+                  ("lam", "<f4"), ("amp", "<f4"), ("pad", "<f4")])
+
+
+def gen_sg_lights(cfg: Config, i0: int = 0, i1: int | None = None, seed: int | None = None, alpha_h: float = 0.3,
+                  lam=(10.0, 1000.0), amp=(0.5, 2.0), out: np.ndarray | None = None) -> np.ndarray:
+    """SG-light query inputs for environment prefiltering (Sec. 5.4): footprint as the config's queries,
+    half vector ~ Beckmann(alpha_h), lambda log-uniform in `lam`, amplitude uniform in `amp`."""
+    i1 = cfg.n_queries if i1 is None else i1
+    seed = cfg.query_seed + 1000 if seed is None else seed
+    if out is None:
+        out = np.empty(i1 - i0, SGREC)
+    assert out.dtype == SGREC and out.shape[0] == i1 - i0
+    qd = qdist_struct(cfg)
+    lib().synth_gen_sg_lights(ctypes.byref(qd), seed, i0, i1, alpha_h, lam[0], lam[1], amp[0], amp[1], _p(out))
     return out
 
 

@@ -488,4 +488,30 @@ EXPORT void synth_gen_queries(const synth_qdist* q, uint64_t seed, int64_t i0, i
     }
 }
 
+/* Spherical-Gaussian light samples for environment prefiltering (Sec. 5.4):
+ * footprint (u, v, S) as the config's query stream, the half vector of the
+ * sampled lobe direction ~ Beckmann(alpha_h) projected, bandwidth lambda
+ * log-uniform in [lam_lo, lam_hi], amplitude U[amp_lo, amp_hi]. */
+typedef struct { float u, v, size, hx, hy, lambda, amplitude, pad; } synth_sgrec;
+
+EXPORT void synth_gen_sg_lights(const synth_qdist* q, uint64_t seed, int64_t i0, int64_t i1, double alpha_h,
+                                double lam_lo, double lam_hi, double amp_lo, double amp_hi, synth_sgrec* out) {
+    const int N = q->N;
+    const float fN = (float)N, below = nextafterf(fN, 0.0f);
+#pragma omp parallel for schedule(static)
+    for (int64_t i = i0; i < i1; ++i) {
+        uint64_t g = (uint64_t)i;
+        synth_sgrec r;
+        float u = (float)(N * rng_unit(seed, 0, g)), v = (float)(N * rng_unit(seed, 1, g));
+        r.u = u < fN ? u : below;
+        r.v = v < fN ? v : below;
+        r.size = (float)exp2(q->lg_lo + (q->lg_hi - q->lg_lo) * rng_unit(seed, 3, g));
+        beckmann_nxy(alpha_h, rng_unit(seed, 30, g), rng_unit(seed, 31, g), &r.hx, &r.hy);
+        r.lambda = (float)exp(log(lam_lo) + (log(lam_hi) - log(lam_lo)) * rng_unit(seed, 32, g));
+        r.amplitude = (float)(amp_lo + (amp_hi - amp_lo) * rng_unit(seed, 33, g));
+        r.pad = 0.0f;
+        out[i - i0] = r;
+    }
+}
+
 EXPORT int32_t synth_max_threads(void) { return omp_get_max_threads(); }
