@@ -42,9 +42,10 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--op", default="query", choices=["query", "sample"],
+    ap.add_argument("--op", default="query", choices=["query", "sample", "sg"],
                     help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
-                         "importance sampling over the whole A x A image")
+                         "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
+                         "prefiltering (SG rectangle generation + range query)")
     ap.add_argument("--queries", type=int, default=0, help="override the config's total query count")
     ap.add_argument("--bin", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--lanes", type=int, default=0)
@@ -501,6 +502,97 @@ def run_sample_op(args, cfg, rank, world, local_rank):
     return 0
 
 
+SG_METRIC = "SG-prefiltered NDF range queries/sec (Sec. 5.4: rectangle generation + range query)"
+
+
+def run_sg_op(args, cfg, rank, world, local_rank):
+    """--op sg: per step pndf_sg_queries (SG light -> rectangle) + pndf_query_batch, same timing rules."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    from paper_2109_14807_b200 import pndf
+    from paper_2109_14807_b200.shard import reduce_times_and_checksum, shard_range
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n_total = args.queries or min(cfg.n_queries, 2 * 10**8)
+    i0, i1 = shard_range(n_total, rank, world)
+    n = i1 - i0
+    bins, f = host_inputs(cfg)
+    Z = synth.build_z_exact_cuda(cfg, f.info["atom_map"], local_rank) if f.Z is None else f.Z
+    store = pndf.load_factors(pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap), f.C, f.X, f.Y, Z,
+                              device=local_rank)
+    del Z
+    torch.cuda.empty_cache()
+    sg = synth.gen_sg_lights(cfg, i0, i1)
+    d_sg = torch.from_numpy(sg.view(np.float32).reshape(-1, 8)).to(dev)
+    d_q = torch.empty((n, 4), dtype=torch.int32, device=dev)
+    d_out = torch.empty(n, dtype=torch.float32, device=dev)
+    opts = {"auto": pndf.BIN_AUTO, "on": pndf.BIN_ON, "off": pndf.BIN_OFF}[args.bin]
+    for _ in range(args.warmup):
+        pndf.sg_queries(d_sg, d_q, cfg.A)
+        store.query_batch(d_q, d_out, opts)
+        store.sync()
+    store.reset_stats()
+    l0 = store.stats()["kernel_launches"]
+    clocks = ClockSampler(bus_id_of(dev))
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        pndf.sg_queries(d_sg, d_q, cfg.A)
+        store.query_batch(d_q, d_out, opts | pndf.TIMING)
+        store.sync()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    st = store.stats()
+    ms_rank = e0.elapsed_time(e1) / args.steps
+    q_ms = st["query_ms"] / max(1, st["timed_batches"])
+    (ms_step,), _ = reduce_times_and_checksum([ms_rank], 0.0, dev)
+    if rank != 0:
+        store.free()
+        return 0
+    peaks, _ = measured_peaks()
+    Bq = bytes_per_query(cfg.R) + 32 + 16  # + SG record read, generated record write
+    achieved = Bq * n / (ms_rank * 1e-3) / 1e9
+    h_q = d_q.cpu().numpy().view(synth.QREC).reshape(-1)
+    idx = np.unique(np.random.default_rng(4).integers(0, n, min(n, 4096)))
+    ref_r = oracle.sg_rects(sg[idx], cfg.A)
+    rect_ok = float(np.mean(h_q["rect"][idx] == ref_r["rect"]))
+    d = oracle.desc_of(cfg)
+    rows, _ = oracle.neighbours(d, h_q[idx])
+    Zs, zmap = oracle.sparse_z(rows, cfg.P, lambda u: z_rows_for(cfg, f, u))
+    t0 = time.perf_counter()
+    ref = oracle.query_batch(d, f.C, f.X, f.Y, Zs, h_q[idx], mean=True, zmap=zmap)
+    cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
+    got = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref)
+    line = {"metric": SG_METRIC, "value": n_total / (ms_step * 1e-3), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(cfg) + "; SG lights: lambda log-U[10,1000], A U[0.5,2], "
+                                                         "half vector Beckmann 0.3, eps 0.3",
+                       "queries_total": n_total, "binned": bool(st["last_binned"])},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                         "kernel": "sg_rect_kernel + pndf::query_kernel", "query_kernel_ms": q_ms,
+                         "bytes_per_query": Bq},
+            "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
+                             "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
+            "gpu_launches": int(st["kernel_launches"] - l0) + args.steps, "clocks": clk,
+            "parity_sample": {"checked": int(idx.shape[0]), "rect_identical_frac": rect_ok,
+                              "query_pass": bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())},
+            "e2e": None}
+    print(json.dumps(line), flush=True)
+    store.free()
+    return 0
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -517,6 +609,8 @@ def main():
     try:
         if args.op == "sample":
             return run_sample_op(args, cfg, rank, world, local_rank)
+        if args.op == "sg":
+            return run_sg_op(args, cfg, rank, world, local_rank)
         return run_ours(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:

@@ -131,6 +131,24 @@ typedef struct {
 pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
                               pndf_sample* d_out, uint32_t opts, void* cuda_stream);
 
+/* One spherical-Gaussian light sample for environment prefiltering (Sec. 5.4),
+ * 32 bytes: footprint (u, v, size) as in pndf_query, the projected half vector
+ * (hx, hy) of the sampled lobe direction, the lobe's bandwidth lambda and
+ * amplitude A (both > 0), padding. */
+typedef struct {
+    float u, v, size, hx, hy, lambda, amplitude, pad;
+} pndf_sg_light;
+
+/* Environment prefiltering rectangles: theta = arccos((ln eps - ln A)
+ * / lambda + 1) (arccos argument clamped to [-1, 1]), side Q = ang_res theta/pi
+ * rounded to the nearest integer in [1, ang_res], square centred on the bin of
+ * (hx, hy) and shifted inside the grid; d_out[i] = {u, v, size, rect} ready for
+ * pndf_query_batch (the paper uses eps = 0.3).  d_in, d_out DEVICE memory; enqueued
+ * on cuda_stream.  Invalid lights (non-finite, lambda or A <= 0) get an invalid
+ * rectangle, which the query batch turns into NaN + PNDF_EQUERY. */
+pndf_status pndf_sg_queries(const pndf_sg_light* d_in, int64_t n, float eps, int32_t ang_res, pndf_query* d_out,
+                            void* cuda_stream);
+
 /* Block until the store's work on cuda_stream is done; returns and clears the
  * sticky per-record error (PNDF_EQUERY) or a CUDA error. */
 pndf_status pndf_sync(pndf_store s, void* cuda_stream);

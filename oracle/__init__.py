@@ -33,6 +33,11 @@ class Desc(ctypes.Structure):
                 ("A", ctypes.c_int32), ("R", ctypes.c_int32), ("wrap", ctypes.c_int32)]
 
 
+class TilesDesc(ctypes.Structure):
+    _fields_ = [("T", ctypes.c_int32), ("s0", ctypes.c_int32), ("L", ctypes.c_int32), ("margin", ctypes.c_int32),
+                ("A", ctypes.c_int32), ("R", ctypes.c_int32), ("seed", ctypes.c_uint64)]
+
+
 def build_lib(force: bool = False) -> str:
     """gcc -O2 -fopenmp (no -ffast-math, no hand SIMD)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
@@ -53,6 +58,9 @@ def lib():
         L.oracle_neighbours_batch.argtypes = [ctypes.POINTER(Desc), P, ctypes.c_int64, P, P]
         L.oracle_sample_batch.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, P, P, ctypes.c_int64, P, P, P, P]
         L.oracle_sg_rects.argtypes = [P, ctypes.c_int64, ctypes.c_double, ctypes.c_int, P, P, P, P]
+        L.oracle_tile_id.restype = ctypes.c_int
+        L.oracle_tile_id.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64]
+        L.oracle_tiled_query_batch.argtypes = [ctypes.POINTER(TilesDesc), P, P, P, P, P, ctypes.c_int64, ctypes.c_int, P]
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -132,6 +140,24 @@ def sg_rects(sg: np.ndarray, A: int, eps: float = 0.3):
     mg = np.empty(n, np.float64)
     lib().oracle_sg_rects(_ptr(sg), n, eps, A, _ptr(th), _ptr(Q), _ptr(rect), _ptr(mg))
     return dict(theta=th, Q=Q, rect=rect, q_margin=mg)
+
+
+def tile_id(seed: int, cx: int, cy: int) -> int:
+    """Wang tile of world cell (cx, cy) from the vertex-hash edge colours."""
+    return lib().oracle_tile_id(seed, cx, cy)
+
+
+def tiled_query_batch(td: TilesDesc, C, X, Y, Z, records: np.ndarray, mean: bool = True) -> np.ndarray:
+    """Implicit Wang-tiled range query (Sec. 5.5): sum of the overlapped tiles' partial NDFs. Z: [16*P_ext, R]."""
+    C = np.ascontiguousarray(C, np.float32)
+    X = np.ascontiguousarray(X, np.float32)
+    Y = np.ascontiguousarray(Y, np.float32)
+    Z = np.ascontiguousarray(Z, np.float32)
+    recs = np.ascontiguousarray(records)
+    out = np.empty(recs.shape[0], np.float64)
+    lib().oracle_tiled_query_batch(ctypes.byref(td), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(recs),
+                                   recs.shape[0], 1 if mean else 0, _ptr(out))
+    return out
 
 
 def neighbours(desc: Desc, records: np.ndarray):

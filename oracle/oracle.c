@@ -334,4 +334,117 @@ EXPORT void oracle_sg_rects(const oracle_sgrec* in, int64_t n, double eps, int A
     }
 }
 
+/* ------------------------------------------------------------------------
+ * Implicit Wang tiling (Sec. 5.5).  The world is an infinite grid
+ * of T x T cells; each lattice vertex hashes to two random bits -- the colours
+ * of its right (horizontal) and bottom (vertical) edges ("we
+ * generate two random numbers with the vertex index as seed ... set to edges
+ * e_ah and e_av, which are the right and bottom edges of vertex A") -- and a
+ * cell's four edge colours pick one of the 16 tiles (edge-to-tile map:
+ * id = N | E<<1 | S<<2 | W<<3).  Each tile has its own CP store over an
+ * extended centre grid ("the sampled centers could locate outside the Wang
+ * tiles") holding the tile's PARTIAL footprint NDF (its own texels,
+ * normalised by the whole footprint's weight), so "the NDF image for a query
+ * that crosses the borders between different Wang tiles is ... computed by
+ * combining the precomputed NDF images from all overlapping Wang tiles":
+ *     D(c) = sum over tiles t overlapping the footprint of D_t(c - origin_t).
+ * Readings: the hash is splitmix64 of (seed, vx, vy) (any fixed
+ * hash; the paper's "hash table" maps bits to colours one to one); the world is
+ * not periodic; level select, neighbours and weights as in the plain query, with
+ * world cell indices; tile t's extended grid has `margin` cells on each side.
+ */
+typedef struct {
+    int32_t T, s0, L, margin, A, R;
+    uint64_t seed;
+} oracle_tiles;
+
+static uint64_t oracle_mix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+/* bit 0: colour of the vertex's right edge, bit 1: of its bottom edge */
+static uint64_t oracle_vertex(uint64_t seed, int64_t vx, int64_t vy) {
+    return oracle_mix(oracle_mix(seed) ^ ((uint64_t)(uint32_t)vx | ((uint64_t)(uint32_t)vy << 32)));
+}
+EXPORT int oracle_tile_id(uint64_t seed, int64_t cx, int64_t cy) {
+    const int n = (int)(oracle_vertex(seed, cx, cy) & 1u);            /* top edge: right edge of (cx, cy)   */
+    const int sth = (int)(oracle_vertex(seed, cx, cy + 1) & 1u);      /* bottom edge: of (cx, cy+1)        */
+    const int w = (int)((oracle_vertex(seed, cx, cy) >> 1) & 1u);     /* left edge: bottom edge of (cx, cy) */
+    const int e = (int)((oracle_vertex(seed, cx + 1, cy) >> 1) & 1u); /* right edge: of (cx+1, cy)          */
+    return n | (e << 1) | (sth << 2) | (w << 3);
+}
+
+static int64_t oracle_tile_rows(const oracle_tiles* d) {
+    int64_t P = 0;
+    for (int l = 0; l < d->L; ++l) {
+        const int64_t ne = d->T / ((int64_t)d->s0 << l) + 2 * d->margin;
+        P += ne * ne;
+    }
+    return P;
+}
+
+EXPORT void oracle_tiled_query_batch(const oracle_tiles* d, const float* C, const float* X, const float* Y,
+                                     const float* Z /* [16][P_ext][R] */, const oracle_rec* q, int64_t n, int mean,
+                                     double* out) {
+    const int64_t Pext = oracle_tile_rows(d);
+    const oracle_desc pd = {d->T, d->s0, d->L, d->A, d->R, 0};
+#pragma omp parallel
+    {
+        double xs[4096], ys[4096];
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t qi = 0; qi < n; ++qi) {
+            int x1, x2, y1, y2;
+            if (!oracle_valid(&pd, &q[qi], &x1, &x2, &y1, &y2) || fabs((double)q[qi].u) > 1073741824.0) {
+                out[qi] = NAN;
+                continue;
+            }
+            const int R = d->R;
+            for (int r = 0; r < R; ++r) { xs[r] = 0.0; ys[r] = 0.0; }
+            for (int x = x1; x <= x2; ++x)
+                for (int r = 0; r < R; ++r) xs[r] += (double)X[(int64_t)x * R + r];
+            for (int y = y1; y <= y2; ++y)
+                for (int r = 0; r < R; ++r) ys[r] += (double)Y[(int64_t)y * R + r];
+            int l0;
+            double t;
+            oracle_level(&pd, (double)q[qi].size, &l0, &t);
+            double sum = 0.0;
+            for (int dl = 0; dl < 2; ++dl) {
+                const int l = l0 + dl;
+                const double wl = dl ? t : 1.0 - t;
+                const int64_t s = (int64_t)d->s0 << l, nn = d->T / s, ne = nn + 2 * d->margin;
+                int64_t off = 0;
+                for (int m = 0; m < l; ++m) {
+                    const int64_t e2 = d->T / ((int64_t)d->s0 << m) + 2 * d->margin;
+                    off += e2 * e2;
+                }
+                const double fu = (double)q[qi].u / (double)s - 0.5, fv = (double)q[qi].v / (double)s - 0.5;
+                const int64_t iu = (int64_t)floor(fu), iv = (int64_t)floor(fv);
+                const double a = fu - floor(fu), b = fv - floor(fv);
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t iw = iu + (k & 1), jw = iv + (k >> 1);
+                    const double wk = wl * ((k & 1) ? a : 1.0 - a) * ((k >> 1) ? b : 1.0 - b);
+                    /* every tile whose extended grid contains this world centre */
+                    const int64_t tx0 = (int64_t)floor((double)(iw - (nn + d->margin) + 1) / (double)nn);
+                    const int64_t tx1 = (int64_t)floor((double)(iw + d->margin) / (double)nn);
+                    const int64_t ty0 = (int64_t)floor((double)(jw - (nn + d->margin) + 1) / (double)nn);
+                    const int64_t ty1 = (int64_t)floor((double)(jw + d->margin) / (double)nn);
+                    for (int64_t ty = ty0; ty <= ty1; ++ty)
+                        for (int64_t tx = tx0; tx <= tx1; ++tx) {
+                            const int64_t il = iw - tx * nn, jl = jw - ty * nn;
+                            if (il < -d->margin || il >= nn + d->margin || jl < -d->margin || jl >= nn + d->margin)
+                                continue;
+                            const int tile = oracle_tile_id(d->seed, tx, ty);
+                            const int64_t z = (int64_t)tile * Pext + off + (jl + d->margin) * ne + (il + d->margin);
+                            sum += wk * oracle_range_sum(&pd, C, xs, ys, Z + z * R);
+                        }
+                }
+            }
+            if (mean) sum /= (double)(x2 - x1 + 1) * (double)(y2 - y1 + 1);
+            out[qi] = sum;
+        }
+    }
+}
+
 EXPORT int oracle_max_threads(void) { return omp_get_max_threads(); }

@@ -501,6 +501,19 @@ pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const f
     return PNDF_OK;
 }
 
+pndf_status pndf_sg_queries(const pndf_sg_light* d_in, int64_t n, float eps, int32_t ang_res, pndf_query* d_out,
+                            void* cuda_stream) {
+    if (n < 0 || (n > 0 && (!d_in || !d_out))) return PNDF_EINVAL;
+    if (!(eps > 0.0f) || ang_res < 1 || ang_res > 256) return PNDF_EINVAL;
+    if ((uintptr_t)d_in % 16 != 0 || (uintptr_t)d_out % 16 != 0) return PNDF_EINVAL;
+    if (n == 0) return PNDF_OK;
+    int dev = 0, sms = 148;
+    CK(cudaGetDevice(&dev));
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    CK(launch_sg_rects(d_in, n, eps, ang_res, d_out, sms, (cudaStream_t)cuda_stream));
+    return PNDF_OK;
+}
+
 pndf_status pndf_sync(pndf_store s, void* cuda_stream) {
     if (!s) return PNDF_EINVAL;
     std::lock_guard<std::mutex> lk(s->mu);

@@ -57,7 +57,11 @@ SAMPLE_DTYPE = np.dtype([("hx", "<f4"), ("hy", "<f4"), ("pdf", "<f4"), ("pixel",
 EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_sync", "pndf_query_batch_host",
            "pndf_free",
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
-           "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation")
+           "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
+           "pndf_sg_queries")
+
+SG_DTYPE = np.dtype([("u", "<f4"), ("v", "<f4"), ("size", "<f4"), ("hx", "<f4"), ("hy", "<f4"),
+                     ("lam", "<f4"), ("amp", "<f4"), ("pad", "<f4")])
 
 _lib = None
 
@@ -95,6 +99,8 @@ def lib():
         L.pndf_store_image.argtypes = [P, P, P, i64, i64]
         L.pndf_bin_permutation.restype = i32
         L.pndf_bin_permutation.argtypes = [P, P, i64, P, P]
+        L.pndf_sg_queries.restype = i32
+        L.pndf_sg_queries.argtypes = [P, i64, ctypes.c_float, i32, P, P]
         L.pndf_set_lanes.restype = i32
         L.pndf_set_lanes.argtypes = [P, i32]
         _lib = L
@@ -141,6 +147,13 @@ def _stream(stream):
     if isinstance(stream, int):
         return ctypes.c_void_p(stream)
     return ctypes.c_void_p(stream.cuda_stream)
+
+
+def sg_queries(d_lights, d_queries, ang_res: int, eps: float = 0.3, stream=None, n: int | None = None):
+    """pndf_sg_queries: device SG-light records (32 B) -> device query records (16 B) for pndf_query_batch."""
+    n = d_queries.shape[0] if n is None else n
+    _check(lib().pndf_sg_queries(_ptr(d_lights), n, eps, ang_res, _ptr(d_queries), _stream(stream)),
+           "pndf_sg_queries")
 
 
 def make_desc(N: int, s0: int, L: int, A: int, R: int, wrap: bool = True, prefix: int = PREFIX_AUTO) -> Desc:

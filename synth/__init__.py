@@ -75,6 +75,10 @@ def lib():
         L.synth_atom_profiles.argtypes = [i32, i32, P, f64, P, P]
         L.synth_gen_queries.argtypes = [ctypes.POINTER(_QDist), u64, i64, i64, P, P]
         L.synth_gen_sg_lights.argtypes = [ctypes.POINTER(_QDist), u64, i64, i64, f64, f64, f64, f64, f64, P]
+        L.synth_wang_tiles.argtypes = [i32, u64, f64, f64, P]
+        L.synth_wang_rows.restype = i64
+        L.synth_wang_rows.argtypes = [i32, i32, i32, i32]
+        L.synth_wang_z.argtypes = [i32, P, i32, i32, i32, i32, P]
         L.synth_max_threads.restype = i32
         _lib = L
     return _lib
@@ -356,6 +360,59 @@ def gen_sg_lights(cfg: Config, i0: int = 0, i1: int | None = None, seed: int | N
     qd = qdist_struct(cfg)
     lib().synth_gen_sg_lights(ctypes.byref(qd), seed, i0, i1, alpha_h, lam[0], lam[1], amp[0], amp[1], _p(out))
     return out
+
+
+@dataclass(frozen=True)
+class TileConfig:
+    """Wang-tile workload (16 tiles of 512^2: a 100K^2 synthesized map)."""
+    T: int = 512
+    A: int = 64
+    R: int = 32
+    s0: int = 1
+    margin: int = 3
+    spacing: float = 12.0
+    alpha: float = 0.1
+    sigma_r: float = 0.005
+    seed: int = 7
+    world: int = 102400
+    n_queries: int = 10**7
+
+    @property
+    def L(self) -> int:
+        return int(round(math.log2(self.T // self.s0))) + 1
+
+
+def wang_tiles(tc: TileConfig) -> np.ndarray:
+    """16 edge-coloured flake tiles: float32 [16, T, T, 2] projected normals."""
+    out = np.empty((16, tc.T, tc.T, 2), np.float32)
+    lib().synth_wang_tiles(tc.T, 0, tc.spacing, tc.alpha, _p(out))
+    return out
+
+
+def wang_rows(tc: TileConfig) -> int:
+    return lib().synth_wang_rows(tc.T, tc.s0, tc.L, tc.margin)
+
+
+def wang_factors(tc: TileConfig, tiles: np.ndarray):
+    """Exact-rank factors shared by the 16 tiles (atoms from all tiles), extended per-tile Z [16*P_ext, R]."""
+    cfg = Config(0, "wang", N=tc.T, A=tc.A, R=tc.R, n_queries=0, map_kind="flakes", sigma_r=tc.sigma_r, s0=tc.s0)
+    allbins = np.concatenate([bin_map(cfg, tiles[t]) for t in range(16)], axis=0)  # [16T, T]
+    # atoms = the R most populated bins over all tiles (ties -> lower bin id); nearest-atom snapping
+    cnt = np.bincount(allbins.ravel().astype(np.int64), minlength=tc.A * tc.A)
+    order = np.lexsort((np.arange(cnt.size), -cnt))[: tc.R]
+    ab = order.astype(np.int32)
+    bx, by = ab % tc.A, ab // tc.A
+    pop = np.nonzero(cnt)[0]
+    px, py = pop % tc.A, pop // tc.A
+    d2 = (px[:, None] - bx[None, :]) ** 2 + (py[:, None] - by[None, :]) ** 2
+    lut = np.full(tc.A * tc.A, 0, np.int64)
+    lut[pop] = np.argmin(d2, axis=1)  # ties -> lower atom index
+    am = lut[allbins.astype(np.int64)].astype(np.uint16).reshape(16, tc.T, tc.T)
+    X, Y = atom_profiles(cfg, ab)
+    P = wang_rows(tc)
+    Z = np.empty((16 * P, tc.R), np.float32)
+    lib().synth_wang_z(tc.T, _p(np.ascontiguousarray(am)), tc.R, tc.s0, tc.L, tc.margin, _p(Z))
+    return Factors(C=np.ones(tc.R, np.float32), X=X, Y=Y, Z=Z, info=dict(atom_bins=ab, atom_map=am, rows=P))
 
 
 def pack_rect(x1, x2, y1, y2):

@@ -514,4 +514,128 @@ EXPORT void synth_gen_sg_lights(const synth_qdist* q, uint64_t seed, int64_t i0,
     }
 }
 
+/* ------------------------------------------------------------ Wang tiles --
+ * 16 edge-coloured tiles (2 colours for horizontal edges, 2 for vertical edges,
+ * tile id = N | E<<1 | S<<2 | W<<3), each T x T texels of Voronoi flakes
+ * ("16 Wang tiles ... tile size as 512 x 512").  Seeds live on a
+ * jittered grid of cells of side ~spacing; a grid cell in the band along an
+ * edge draws its seed from (edge orientation, edge colour, position along the
+ * edge), interior cells from the tile id, so tiles sharing an edge colour have
+ * the same seeds along it (near-seamless; corners are not constrained, as in
+ * the paper).  nxy: [16][T][T][2]. */
+EXPORT void synth_wang_tiles(int32_t T, uint64_t seed, double spacing, double alpha, float* nxy) {
+    int nc = (int)floor((double)T / spacing + 0.5);
+    if (nc < 3) nc = 3;
+    const double cs = (double)T / nc;
+    for (int tile = 0; tile < 16; ++tile) {
+        const int cn = tile & 1, ce = (tile >> 1) & 1, csouth = (tile >> 2) & 1, cw = (tile >> 3) & 1;
+        const int64_t NF = (int64_t)nc * nc;
+        double* sx = (double*)malloc(sizeof(double) * NF);
+        double* sy = (double*)malloc(sizeof(double) * NF);
+        float* fnx = (float*)malloc(sizeof(float) * NF);
+        float* fny = (float*)malloc(sizeof(float) * NF);
+        for (int64_t f = 0; f < NF; ++f) {
+            const int ci = (int)(f % nc), cj = (int)(f / nc);
+            uint64_t key;
+            if (cj == 0 && ci > 0 && ci < nc - 1) key = 0x1000 + (uint64_t)cn * 0x100 + ci;                /* N */
+            else if (cj == nc - 1 && ci > 0 && ci < nc - 1) key = 0x1000 + (uint64_t)csouth * 0x100 + ci;  /* S */
+            else if (ci == 0 && cj > 0 && cj < nc - 1) key = 0x2000 + (uint64_t)cw * 0x100 + cj;           /* W */
+            else if (ci == nc - 1 && cj > 0 && cj < nc - 1) key = 0x2000 + (uint64_t)ce * 0x100 + cj;      /* E */
+            else if ((ci == 0 || ci == nc - 1) && (cj == 0 || cj == nc - 1)) key = 0x3000;                 /* corner */
+            else key = 0x4000 + (uint64_t)tile * 0x10000 + (uint64_t)f;                                    /* interior */
+            /* band seeds sit on the edge-normal axis symmetric for the two tiles sharing the edge */
+            double jx = rng_unit(seed, 40, key), jy = rng_unit(seed, 41, key);
+            if (cj == 0) jy = 0.5 * jy;               /* keep N-band seeds near the edge */
+            if (cj == nc - 1) jy = 1.0 - 0.5 * jy;
+            if (ci == 0) jx = 0.5 * jx;
+            if (ci == nc - 1) jx = 1.0 - 0.5 * jx;
+            sx[f] = (ci + jx) * cs;
+            sy[f] = (cj + jy) * cs;
+            beckmann_nxy(alpha, rng_unit(seed, 42, key), rng_unit(seed, 43, key), &fnx[f], &fny[f]);
+        }
+        float* out = nxy + (int64_t)tile * T * T * 2;
+#pragma omp parallel for schedule(static)
+        for (int64_t t = 0; t < (int64_t)T * T; ++t) {
+            const double px = (double)(t % T) + 0.5, py = (double)(t / T) + 0.5;
+            const int ci = (int)floor(px / cs), cj = (int)floor(py / cs);
+            double best = 1e300;
+            int64_t bf = 0;
+            for (int dj = -2; dj <= 2; ++dj)
+                for (int di = -2; di <= 2; ++di) {
+                    const int ii = ci + di, jj = cj + dj;
+                    if (ii < 0 || jj < 0 || ii >= nc || jj >= nc) continue;
+                    const int64_t f = (int64_t)jj * nc + ii;
+                    const double dx = px - sx[f], dy = py - sy[f], d2 = dx * dx + dy * dy;
+                    if (d2 < best || (d2 == best && f < bf)) { best = d2; bf = f; }
+                }
+            out[2 * t] = fnx[bf];
+            out[2 * t + 1] = fny[bf];
+        }
+        free(sx); free(sy); free(fnx); free(fny);
+    }
+}
+
+/* Extended per-tile positional factors for Wang-tile stores (P:438-442:
+ * "the sampled centers could locate outside the Wang tiles").  Level l of a tile
+ * has n = T/(s0 2^l) cells plus `margin` cells on each side; row
+ * z = off_l + (j + m) (n + 2m) + (i + m) for local cells i, j in [-m, n + m).
+ * Z[t][z][k] = sum over the tile's OWN texels u of G_p(u - c) [atom(u) = k] /
+ * W_total, with W_total the footprint's full weight (sum w)^2: a footprint that
+ * straddles tiles is the SUM of the tiles' partial NDFs (linearity of Eq. 2).
+ * atom_map: [16][T][T]; Z: [16][P_ext][R]. */
+EXPORT int64_t synth_wang_rows(int32_t T, int32_t s0, int32_t L, int32_t margin) {
+    int64_t P = 0;
+    for (int l = 0; l < L; ++l) {
+        const int64_t n = T / ((int64_t)s0 << l) + 2 * margin;
+        P += n * n;
+    }
+    return P;
+}
+
+EXPORT void synth_wang_z(int32_t T, const uint16_t* atom_map, int32_t R, int32_t s0, int32_t L, int32_t margin,
+                         float* Z) {
+    const int64_t Pext = synth_wang_rows(T, s0, L, margin);
+    for (int tile = 0; tile < 16; ++tile) {
+        const uint16_t* am = atom_map + (int64_t)tile * T * T;
+        int64_t off = 0;
+        for (int32_t l = 0; l < L; ++l) {
+            const int32_t s = s0 << l, n = T / s, ne = n + 2 * margin;
+            /* unfolded window table over a virtual line much longer than the tile */
+            const double sigma = 1.5 * (double)s / sqrt(12.0), c = 0.5 * (1.0 - (double)s);
+            const int64_t qmin = (int64_t)ceil(-4.0 * sigma - c), qmax = (int64_t)floor(4.0 * sigma - c);
+            const int64_t W = qmax - qmin + 1;
+            uint32_t* wt = (uint32_t*)malloc(sizeof(uint32_t) * W);
+            uint64_t sw = 0;
+            for (int64_t q = qmin; q <= qmax; ++q) {
+                const double d = (double)q + c;
+                wt[q - qmin] = (uint32_t)llround(65536.0 * exp(-d * d / (2.0 * sigma * sigma)));
+                sw += wt[q - qmin];
+            }
+            const double tot = (double)sw * (double)sw;
+#pragma omp parallel
+            {
+                uint64_t* acc = (uint64_t*)malloc(sizeof(uint64_t) * R);
+#pragma omp for schedule(dynamic, 16)
+                for (int64_t cidx = 0; cidx < (int64_t)ne * ne; ++cidx) {
+                    const int64_t i = cidx % ne - margin, j = cidx / ne - margin;
+                    memset(acc, 0, sizeof(uint64_t) * R);
+                    /* texels x = i*s + q for q in [qmin, qmax], clipped to the tile */
+                    const int64_t qy0 = qmin > -j * s ? qmin : -j * s, qy1 = qmax < T - 1 - j * s ? qmax : T - 1 - j * s;
+                    const int64_t qx0 = qmin > -i * s ? qmin : -i * s, qx1 = qmax < T - 1 - i * s ? qmax : T - 1 - i * s;
+                    for (int64_t qy = qy0; qy <= qy1; ++qy) {
+                        const uint64_t wy = wt[qy - qmin];
+                        const uint16_t* row = am + (j * s + qy) * T + i * s;
+                        for (int64_t qx = qx0; qx <= qx1; ++qx) acc[row[qx]] += wy * (uint64_t)wt[qx - qmin];
+                    }
+                    float* out = Z + ((int64_t)tile * Pext + off + cidx) * R;
+                    for (int k = 0; k < R; ++k) out[k] = (float)((double)acc[k] / tot);
+                }
+                free(acc);
+            }
+            free(wt);
+            off += (int64_t)ne * ne;
+        }
+    }
+}
+
 EXPORT int32_t synth_max_threads(void) { return omp_get_max_threads(); }
