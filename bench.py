@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--op", default="query", choices=["query", "sample", "sg"],
+    ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang"],
                     help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
                          "prefiltering (SG rectangle generation + range query)")
@@ -593,6 +593,93 @@ def run_sg_op(args, cfg, rank, world, local_rank):
     return 0
 
 
+WANG_METRIC = "Wang-tiled NDF range queries/sec (Sec. 5.5: implicit 16-tile map, 100K^2 texels)"
+
+
+def run_wang_op(args, cfg, rank, world, local_rank):
+    """--op wang: range queries on an implicitly Wang-tiled 102400^2 map (16 tiles of 512^2, A=64, R=32)."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    from paper_2109_14807_b200 import pndf
+    from paper_2109_14807_b200.shard import reduce_times_and_checksum, shard_range
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    tc = synth.TileConfig()
+    n_total = args.queries or tc.n_queries
+    i0, i1 = shard_range(n_total, rank, world)
+    n = i1 - i0
+    tiles = synth.wang_tiles(tc)
+    f = synth.wang_factors(tc, tiles)
+    store = pndf.load_tiles(pndf.make_tile_desc(tc.T, tc.s0, tc.L, tc.margin, tc.A, tc.R, tc.seed), f.C, f.X, f.Y,
+                            f.Z, device=local_rank)
+    # queries: world positions uniform, sizes log-uniform in [1, T], config-2-like rectangles
+    rng = np.random.default_rng(500 + rank)
+    A = tc.A
+    w = rng.uniform(0.5, 4.0, (n, 2))
+    side = np.maximum(1, np.floor(2 * w + 0.5)).astype(np.int64)
+    x1 = rng.integers(0, A - side[:, 0] + 1)
+    y1 = rng.integers(0, A - side[:, 1] + 1)
+    recs = synth.make_records(rng.uniform(0, tc.world, n), rng.uniform(0, tc.world, n),
+                              np.exp2(rng.uniform(0, np.log2(tc.T), n)), x1, x1 + side[:, 0] - 1, y1,
+                              y1 + side[:, 1] - 1)
+    d_q = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).to(dev)
+    d_out = torch.empty(n, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        store.query_batch(d_q, d_out, 0)
+        store.sync()
+    store.reset_stats()
+    clocks = ClockSampler(bus_id_of(dev))
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        store.query_batch(d_q, d_out, pndf.TIMING)
+        store.sync()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    st = store.stats()
+    ms_rank = e0.elapsed_time(e1) / args.steps
+    (ms_step,), _ = reduce_times_and_checksum([ms_rank], 0.0, dev)
+    if rank != 0:
+        store.free()
+        return 0
+    idx = np.unique(np.random.default_rng(5).integers(0, n, min(n, 20000)))
+    td_o = oracle.TilesDesc(T=tc.T, s0=tc.s0, L=tc.L, margin=tc.margin, A=tc.A, R=tc.R, seed=tc.seed)
+    t0 = time.perf_counter()
+    ref = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, recs[idx])
+    cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
+    got = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref)
+    line = {"metric": WANG_METRIC, "value": n_total / (ms_step * 1e-3), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"16 Wang tiles of {tc.T}^2 flakes (spacing {tc.spacing}, alpha {tc.alpha}), "
+                                   f"A={tc.A}, R={tc.R}, margin {tc.margin}, world {tc.world}^2, S log-U[1,{tc.T}]",
+                       "queries_total": n_total, "rows": int(st["rows"]),
+                       "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]]},
+            "roofline": {"bound": "hbm", "achieved": None, "peak": measured_peaks()[0]["hbm_gbs"], "unit": "GB/s",
+                         "frac": None, "traffic": None, "kernel": "pndf::tiled_query_kernel",
+                         "kernel_ms": st["query_ms"] / max(1, st["timed_batches"]),
+                         "note": "tiles' Zc (%.0f MB) is L2-resident; rows per query vary with the footprint" %
+                                 (st["zc_bytes"] / 1e6)},
+            "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
+                             "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
+            "gpu_launches": args.steps, "clocks": clk,
+            "parity_sample": {"checked": int(idx.shape[0]),
+                              "pass": bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())},
+            "e2e": None}
+    print(json.dumps(line), flush=True)
+    store.free()
+    return 0
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -611,6 +698,8 @@ def main():
             return run_sample_op(args, cfg, rank, world, local_rank)
         if args.op == "sg":
             return run_sg_op(args, cfg, rank, world, local_rank)
+        if args.op == "wang":
+            return run_wang_op(args, cfg, rank, world, local_rank)
         return run_ours(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:

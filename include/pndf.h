@@ -190,6 +190,38 @@ pndf_status pndf_store_stats_reset(pndf_store s);
  * [z0, z1) as [z1-z0][Rp] fp32.  Either pointer may be NULL. */
 pndf_status pndf_store_image(pndf_store s, float* PXY, float* Zc, int64_t z0, int64_t z1);
 
+/* Implicit Wang tiling (Sec. 5.5).  16 tiles of
+ * T x T texels share the angular factors X, Y (and C); tile t has its own
+ * positional factors over an EXTENDED centre grid: level l has n_l = T/(s0 2^l)
+ * cells plus `margin` cells on each side (centres outside the tile), rows
+ * z = t*P_ext + off_l + (j+margin)(n_l+2 margin) + (i+margin), off_l the sum of the
+ * earlier levels' (n+2 margin)^2, P_ext the per-tile total; each row holds the
+ * tile's PARTIAL footprint NDF (its own texels, normalised by the footprint's full
+ * weight).  World cell (cx, cy) uses the tile whose edge colours come from the
+ * vertex hash splitmix64(splitmix64(seed) ^ (uint32 vx | uint32 vy << 32)) --
+ * bit 0 = colour of the vertex's right edge, bit 1 = of its bottom edge; tile id =
+ * N | E<<1 | S<<2 | W<<3.  A query on a tiled store sums the
+ * contributions of every tile whose extended grid holds each of its 8 neighbours
+ * ("combining the precomputed NDF images from all overlapping Wang tiles",
+ * P:440).  World coordinates are not periodic; |u|,|v| <= 2^22. */
+typedef struct {
+    uint32_t abi_version; /* = PNDF_ABI_VERSION                                    */
+    int32_t tile_size;    /* T, power of two                                       */
+    int32_t base_stride;  /* s0, power of two dividing T                           */
+    int32_t num_levels;   /* L, 2 <= L <= log2(T/s0) + 1                           */
+    int32_t margin;       /* extended cells per side, >= 2 (covers the +-4 sigma support) */
+    int32_t ang_res;      /* A                                                     */
+    int32_t rank;         /* R                                                     */
+    uint32_t flags;       /* PNDF_PREFIX_* (border flags ignored)                  */
+    uint64_t seed;        /* vertex-hash seed                                      */
+} pndf_tile_desc;
+
+/* Build a tiled store (Z = [16 * P_ext][R], other arguments as pndf_load_factors).
+ * pndf_query_batch / pndf_query_batch_host answer world-space queries on it
+ * (never binned); pndf_sample_batch returns PNDF_EINVAL for tiled stores. */
+pndf_status pndf_load_tiles(const pndf_tile_desc* desc, const float* C, const float* X, const float* Y,
+                            const float* Z, int device, void* cuda_stream, pndf_store* out);
+
 /* Test support: run only the binning pass (row a1) on n device records and copy
  * the permutation (query indices in binned order) to d_perm [n] and, if not
  * NULL, the sorted bin keys to d_keys [n] (device memory).  Synchronous. */

@@ -36,6 +36,14 @@ struct QParams {
     uint32_t mean;                 // 1 = divide by the rectangle area
 };
 
+// Implicit Wang tiling (tiles.cu).
+struct TileParams {
+    int32_t T;        // tile size (texels)
+    int32_t margin;   // extended cells per side
+    int64_t p_ext;    // rows per tile
+    uint64_t seed;    // vertex-hash seed
+};
+
 // Device scratch of one in-flight binned batch (radix sort double buffers).
 struct BinScratch {
     uint32_t* keys[2] = {nullptr, nullptr};

@@ -37,6 +37,10 @@ cudaError_t launch_query_hilo_clamp(int G, int NV, const QParams& p, const pndf_
 cudaError_t launch_sample_hilo_clamp(int G, int NV, const QParams& p, const pndf_query* q, const float* xi,
                                   const uint32_t* idx, int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
 
+// Wang-tiled query (tiles.cu).
+cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q, int64_t n,
+                               float* out, int num_sms, cudaStream_t st);
+
 // Environment-prefiltering rectangles (sg.cu).
 cudaError_t launch_sg_rects(const pndf_sg_light* in, int64_t n, float eps, int A, pndf_query* out, int num_sms,
                             cudaStream_t st);

@@ -92,6 +92,8 @@ struct pndf_store_s {
     int64_t P = 0;
     int Rp = 0, G0 = 0, NV0 = 0, G = 0, NV = 0;
     int64_t nbins = 0;  // P + 1 (last = invalid records); 0 if binning infeasible
+    bool tiled = false;  // Wang-tile store (pndf_load_tiles)
+    TileParams tp{};
     QParams qp{};
     float* Zc = nullptr;
     float* PXY = nullptr;
@@ -170,6 +172,16 @@ pndf_status enqueue(pndf_store_s* s, Scratch& sc, const pndf_query* q, int64_t n
                     cudaStream_t st, bool timing) {
     QParams p = s->qp;
     p.mean = (opts & PNDF_SUM) ? 0u : 1u;
+    if (s->tiled) {  // Wang-tiled world queries: one kernel, never binned
+        if (opts & PNDF_BIN_ON) return PNDF_EINVAL;
+        if (timing) CK(cudaEventRecord(s->ev[0], st));
+        if (timing) CK(cudaEventRecord(s->ev[1], st));
+        CK(launch_tiled_query(p, s->tp, s->G, s->NV, q, n, out, s->num_sms, st));
+        if (timing) CK(cudaEventRecord(s->ev[2], st));
+        s->stats.kernel_launches += 1;
+        s->stats.last_binned = 0;
+        return PNDF_OK;
+    }
     const bool binned = want_bins(s, n, opts);
     if ((opts & PNDF_BIN_ON) && s->nbins == 0) return PNDF_EINVAL;
     int launches = 0;
@@ -246,12 +258,58 @@ const char* pndf_error_string(pndf_status st) {
 
 const char* pndf_last_cuda_error(void) { return g_cuda_err; }
 
+static pndf_status load_impl(const pndf_desc* desc, int64_t P_override, const float* C, const float* X,
+                             const float* Y, const float* Z, int device, void* cuda_stream, pndf_store* out);
+
 pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float* X, const float* Y, const float* Z,
                               int device, void* cuda_stream, pndf_store* out) {
-    if (!out || !X || !Y || !Z) return PNDF_EINVAL;
+    if (!out) return PNDF_EINVAL;
     *out = nullptr;
     pndf_status r = validate_desc(desc);
     if (r != PNDF_OK) return r;
+    return load_impl(desc, 0, C, X, Y, Z, device, cuda_stream, out);
+}
+
+pndf_status pndf_load_tiles(const pndf_tile_desc* td, const float* C, const float* X, const float* Y, const float* Z,
+                            int device, void* cuda_stream, pndf_store* out) {
+    if (!out || !td) return PNDF_EINVAL;
+    *out = nullptr;
+    if (td->abi_version != PNDF_ABI_VERSION) return PNDF_EFORMAT;
+    if (!is_pow2(td->tile_size) || td->tile_size > (1 << 16) || td->margin < 2 || td->margin > 64) return PNDF_EINVAL;
+    pndf_desc d;
+    d.abi_version = PNDF_ABI_VERSION;
+    d.map_size = td->tile_size;
+    d.base_stride = td->base_stride;
+    d.num_levels = td->num_levels;
+    d.ang_res = td->ang_res;
+    d.rank = td->rank;
+    d.flags = td->flags & PNDF_PREFIX_MASK;
+    pndf_status r = validate_desc(&d);
+    if (r != PNDF_OK) return r;
+    int64_t pext = 0;
+    const int64_t n0 = td->tile_size / td->base_stride;
+    for (int l = 0; l < td->num_levels; ++l) {
+        const int64_t ne = (n0 >> l) + 2 * td->margin;
+        pext += ne * ne;
+    }
+    if (16 * pext >= (int64_t(1) << 31)) return PNDF_EINVAL;
+    r = load_impl(&d, 16 * pext, C, X, Y, Z, device, cuda_stream, out);
+    if (r != PNDF_OK) return r;
+    pndf_store_s* s = *out;
+    s->tiled = true;
+    s->nbins = 0;  // tiled queries are not binned
+    s->tp.T = td->tile_size;
+    s->tp.margin = td->margin;
+    s->tp.p_ext = pext;
+    s->tp.seed = td->seed;
+    s->qp.wrap = 0;
+    return PNDF_OK;
+}
+
+static pndf_status load_impl(const pndf_desc* desc, int64_t P_override, const float* C, const float* X,
+                             const float* Y, const float* Z, int device, void* cuda_stream, pndf_store* out) {
+    if (!out || !X || !Y || !Z) return PNDF_EINVAL;
+    *out = nullptr;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
     if (device < 0 || device >= ndev) return PNDF_EINVAL;
@@ -266,6 +324,7 @@ pndf_status pndf_load_factors(const pndf_desc* desc, const float* C, const float
               R = desc->rank;
     const int64_t n0 = N / s0;
     for (int l = 0; l < L; ++l) s->P += (n0 >> l) * (n0 >> l);
+    if (P_override > 0) s->P = P_override;
     choose_lanes(R, &s->G0, &s->NV0);
     s->G = s->G0;
     s->NV = s->NV0;
@@ -470,6 +529,7 @@ pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const f
     if (n == 0) return PNDF_OK;
     if ((uintptr_t)d_queries % 16 != 0 || (uintptr_t)d_out % 16 != 0 || (uintptr_t)d_xi % 4 != 0)
         return PNDF_EINVAL;
+    if (s->tiled) return PNDF_EINVAL;  // sampling a tiled store is not supported
     std::lock_guard<std::mutex> lk(s->mu);
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)cuda_stream;

@@ -1,0 +1,196 @@
+// tiles.cu -- range queries on an implicitly Wang-tiled normal map (Sec. 5.5,
+// P:438-454).  Each of the 8 trilinear neighbours (world
+// cell centres) gathers the Zc row of every tile whose extended grid holds it
+// (the tiles' partial NDFs add up to the footprint's NDF); the tile of a
+// world cell comes from the edge colours hashed at its corner vertices (P:444,
+// P:450-451).  X, Y are shared by the tiles, so Z-hat = sum_k w_k sum_tiles Zc
+// is accumulated first and the SAT product runs once, as in query_kernel.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "device.cuh"
+#include "launch.h"
+
+namespace pndf {
+
+__device__ __forceinline__ uint64_t tile_mix(uint64_t z) {
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t tile_vertex(uint64_t seed_mixed, int64_t vx, int64_t vy) {
+    return tile_mix(seed_mixed ^ ((uint64_t)(uint32_t)vx | ((uint64_t)(uint32_t)vy << 32)));
+}
+// tile id = N | E<<1 | S<<2 | W<<3 from the corner vertices' edge colours
+__device__ __forceinline__ int tile_of(uint64_t seed_mixed, int64_t cx, int64_t cy) {
+    const uint64_t a = tile_vertex(seed_mixed, cx, cy);
+    const int n = (int)(a & 1u), w = (int)((a >> 1) & 1u);
+    const int sth = (int)(tile_vertex(seed_mixed, cx, cy + 1) & 1u);
+    const int e = (int)((tile_vertex(seed_mixed, cx + 1, cy) >> 1) & 1u);
+    return n | (e << 1) | (sth << 2) | (w << 3);
+}
+
+template <int G, int NV, bool U32>
+__global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const TileParams tp,
+                                                          const pndf_query* __restrict__ q, int64_t n,
+                                                          float* __restrict__ out) {
+    constexpr int QPW = 32 / G;
+    constexpr int RP = 4 * G * NV;
+    constexpr int PSTRIDE = U32 ? RP : 2 * RP;
+    const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
+    const float* __restrict__ PX = p.PXY;
+    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * PSTRIDE;
+    const uint64_t seed_mixed = tile_mix(tp.seed);
+    const int M = tp.margin;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = gw * QPW; base < n; base += nw * QPW) {
+        const int64_t qi = base + grp;
+        const bool active = qi < n;
+        const pndf_query rec = ldg_query(q + (active ? qi : 0));
+        int x1, x2, y1, y2;
+        const bool valid = active && record_valid(p, rec, x1, x2, y1, y2);
+        float4 zh[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) zh[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (valid) {
+            int l0;
+            float t;
+            level_select(p, rec.size, l0, t);
+            for (int dl = 0; dl < 2; ++dl) {
+                const int l = l0 + dl;
+                const float wl = dl ? t : 1.f - t;
+                const int sh = __ffs(p.n0 >> l) - 1;  // log2 n_l
+                const int64_t nl = (int64_t)1 << sh, ne = nl + 2 * M;
+                int64_t off = 0;
+                for (int m = 0; m < l; ++m) {
+                    const int64_t e2 = (int64_t)(p.n0 >> m) + 2 * M;
+                    off += e2 * e2;
+                }
+                const float inv_s = __int_as_float(__float_as_int(p.inv_s0) - (l << 23));
+                const float fu = fmaf(rec.u, inv_s, -0.5f), fv = fmaf(rec.v, inv_s, -0.5f);
+                const float flu = floorf(fu), flv = floorf(fv);
+                const float a = fu - flu, b = fv - flv;
+                const int64_t iu = (int64_t)flu, iv = (int64_t)flv;
+                const float wa = wl * (1.f - a), wb = wl * a;
+                const float wk4[4] = {wa * (1.f - b), wb * (1.f - b), wa * b, wb * b};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int64_t iw = iu + (k & 1), jw = iv + (k >> 1);
+                    const float wk = wk4[k];
+                    // tiles whose extended grid [-M, nl + M) holds this world cell (floor division by nl = 2^sh)
+                    const int64_t tx0 = (iw - (nl + M) + 1) >> sh, tx1 = (iw + M) >> sh;
+                    const int64_t ty0 = (jw - (nl + M) + 1) >> sh, ty1 = (jw + M) >> sh;
+                    for (int64_t ty = ty0; ty <= ty1; ++ty)
+                        for (int64_t tx = tx0; tx <= tx1; ++tx) {
+                            const int64_t il = iw - (tx << sh), jl = jw - (ty << sh);
+                            if (il < -M || il >= nl + M || jl < -M || jl >= nl + M) continue;
+                            const int tile = tile_of(seed_mixed, tx, ty);
+                            const int64_t row = (int64_t)tile * tp.p_ext + off + (jl + M) * ne + (il + M);
+#pragma unroll
+                            for (int v = 0; v < NV; ++v) {
+                                const float4 zr = ldg4(p.Zc + (size_t)row * RP + (gl + v * G) * 4);
+                                zh[v].x = fmaf(wk, zr.x, zh[v].x);
+                                zh[v].y = fmaf(wk, zr.y, zh[v].y);
+                                zh[v].z = fmaf(wk, zr.z, zh[v].z);
+                                zh[v].w = fmaf(wk, zr.w, zh[v].w);
+                            }
+                        }
+                }
+            }
+        }
+        float part = 0.f;
+        if (valid) {
+            const float* px0 = PX + (size_t)x1 * PSTRIDE;
+            const float* px1 = PX + (size_t)(x2 + 1) * PSTRIDE;
+            const float* py0 = PY + (size_t)y1 * PSTRIDE;
+            const float* py1 = PY + (size_t)(y2 + 1) * PSTRIDE;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const int c = (gl + v * G) * 4;
+                float4 dx, dy;
+                if (U32) {
+                    const uint4 qx1 = __ldg(reinterpret_cast<const uint4*>(px1 + c));
+                    const uint4 qx0 = __ldg(reinterpret_cast<const uint4*>(px0 + c));
+                    const uint4 qy1 = __ldg(reinterpret_cast<const uint4*>(py1 + c));
+                    const uint4 qy0 = __ldg(reinterpret_cast<const uint4*>(py0 + c));
+                    dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                     __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                    dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                     __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                } else {
+                    const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
+                    const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
+                    const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
+                    const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
+                    dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                     (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                    dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                     (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                }
+                part = fmaf(dx.x * dy.x, zh[v].x, part);
+                part = fmaf(dx.y * dy.y, zh[v].y, part);
+                part = fmaf(dx.z * dy.z, zh[v].z, part);
+                part = fmaf(dx.w * dy.w, zh[v].w, part);
+            }
+        }
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (active && gl == 0) {
+            if (!valid) {
+                out[qi] = __int_as_float(0x7fc00000);
+                atomicOr(p.err, 1u);
+            } else {
+                out[qi] = p.mean ? part / (float)((x2 - x1 + 1) * (y2 - y1 + 1)) : part;
+            }
+        }
+    }
+}
+
+template <int G, int NV, bool U>
+static cudaError_t launch_t(const QParams& p, const TileParams& tp, const pndf_query* q, int64_t n, float* out,
+                            int num_sms, cudaStream_t st) {
+    const int64_t qpb = 8 * (32 / G);
+    int64_t grid = (n + qpb - 1) / qpb;
+    if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
+    if (grid < 1) grid = 1;
+    tiled_query_kernel<G, NV, U><<<(unsigned)grid, 256, 0, st>>>(p, tp, q, n, out);
+    return cudaGetLastError();
+}
+
+template <int G, bool U>
+static cudaError_t t_nv(int NV, const QParams& p, const TileParams& tp, const pndf_query* q, int64_t n, float* out,
+                        int sms, cudaStream_t st) {
+    switch (NV) {
+        case 1: return launch_t<G, 1, U>(p, tp, q, n, out, sms, st);
+        case 2: return launch_t<G, 2, U>(p, tp, q, n, out, sms, st);
+        case 3: return launch_t<G, 3, U>(p, tp, q, n, out, sms, st);
+        case 4: return launch_t<G, 4, U>(p, tp, q, n, out, sms, st);
+        case 8: return launch_t<G, 8, U>(p, tp, q, n, out, sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool U>
+static cudaError_t t_g(int G, int NV, const QParams& p, const TileParams& tp, const pndf_query* q, int64_t n,
+                       float* out, int sms, cudaStream_t st) {
+    switch (G) {
+        case 1: return t_nv<1, U>(NV, p, tp, q, n, out, sms, st);
+        case 2: return t_nv<2, U>(NV, p, tp, q, n, out, sms, st);
+        case 4: return t_nv<4, U>(NV, p, tp, q, n, out, sms, st);
+        case 8: return t_nv<8, U>(NV, p, tp, q, n, out, sms, st);
+        case 16: return t_nv<16, U>(NV, p, tp, q, n, out, sms, st);
+        case 32: return t_nv<32, U>(NV, p, tp, q, n, out, sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q, int64_t n,
+                               float* out, int num_sms, cudaStream_t st) {
+    if (4 * G * NV != p.Rp) return cudaErrorInvalidValue;
+    if (p.prefix_u32) return t_g<true>(G, NV, p, tp, q, n, out, num_sms, st);
+    return t_g<false>(G, NV, p, tp, q, n, out, num_sms, st);
+}
+
+}  // namespace pndf

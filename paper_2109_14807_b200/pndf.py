@@ -41,6 +41,12 @@ class Desc(ctypes.Structure):
                 ("flags", ctypes.c_uint32)]
 
 
+class TileDesc(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_uint32), ("tile_size", ctypes.c_int32), ("base_stride", ctypes.c_int32),
+                ("num_levels", ctypes.c_int32), ("margin", ctypes.c_int32), ("ang_res", ctypes.c_int32),
+                ("rank", ctypes.c_int32), ("flags", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
+
+
 class StoreStats(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("rank_padded", ctypes.c_int32), ("lanes_per_query", ctypes.c_int32),
                 ("zc_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
@@ -58,7 +64,7 @@ EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_s
            "pndf_free",
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
-           "pndf_sg_queries")
+           "pndf_sg_queries", "pndf_load_tiles")
 
 SG_DTYPE = np.dtype([("u", "<f4"), ("v", "<f4"), ("size", "<f4"), ("hx", "<f4"), ("hy", "<f4"),
                      ("lam", "<f4"), ("amp", "<f4"), ("pad", "<f4")])
@@ -99,6 +105,8 @@ def lib():
         L.pndf_store_image.argtypes = [P, P, P, i64, i64]
         L.pndf_bin_permutation.restype = i32
         L.pndf_bin_permutation.argtypes = [P, P, i64, P, P]
+        L.pndf_load_tiles.restype = i32
+        L.pndf_load_tiles.argtypes = [ctypes.POINTER(TileDesc), P, P, P, P, ctypes.c_int, P, ctypes.POINTER(P)]
         L.pndf_sg_queries.restype = i32
         L.pndf_sg_queries.argtypes = [P, i64, ctypes.c_float, i32, P, P]
         L.pndf_set_lanes.restype = i32
@@ -153,7 +161,7 @@ def sg_queries(d_lights, d_queries, ang_res: int, eps: float = 0.3, stream=None,
     """pndf_sg_queries: device SG-light records (32 B) -> device query records (16 B) for pndf_query_batch."""
     n = d_queries.shape[0] if n is None else n
     _check(lib().pndf_sg_queries(_ptr(d_lights), n, eps, ang_res, _ptr(d_queries), _stream(stream)),
-           "pndf_sg_queries")
+           "pndf_sg_queries", "pndf_load_tiles")
 
 
 def make_desc(N: int, s0: int, L: int, A: int, R: int, wrap: bool = True, prefix: int = PREFIX_AUTO) -> Desc:
@@ -252,3 +260,17 @@ def load_factors(desc: Desc, C, X, Y, Z, device: int = 0, stream=None) -> Store:
     _check(lib().pndf_load_factors(ctypes.byref(desc), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), device, _stream(stream),
                                    ctypes.byref(h)), "pndf_load_factors")
     return Store(h, desc)
+
+
+def make_tile_desc(T: int, s0: int, L: int, margin: int, A: int, R: int, seed: int, prefix: int = PREFIX_AUTO):
+    return TileDesc(abi_version=ABI_VERSION, tile_size=T, base_stride=s0, num_levels=L, margin=margin, ang_res=A,
+                    rank=R, flags=prefix, seed=seed)
+
+
+def load_tiles(td: TileDesc, C, X, Y, Z, device: int = 0, stream=None) -> Store:
+    """pndf_load_tiles: 16 Wang tiles sharing X, Y; Z = [16 * P_ext, R] extended per-tile factors."""
+    h = ctypes.c_void_p()
+    _check(lib().pndf_load_tiles(ctypes.byref(td), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), device, _stream(stream),
+                                 ctypes.byref(h)), "pndf_load_tiles")
+    d = make_desc(td.tile_size, td.base_stride, td.num_levels, td.ang_res, td.rank, False)
+    return Store(h, d)
