@@ -118,13 +118,20 @@ def main():
     if os.path.exists(sc):
         txt, _ = summarize(sc, nq, "pndf::rs_scatter_kernel<9> (one radix pass), config 5")
         open(os.path.join(OUT, f"{rnd}_radix_scatter_ncu.txt"), "w").write(txt)
+    sp = os.path.join(GP, "prof_sample.ncu-rep")
+    if os.path.exists(sp):
+        txt, _ = summarize(sp, 1e8, "pndf::sample_kernel, config 5, 1e8 samples (bench --op sample)")
+        open(os.path.join(OUT, f"{rnd}_sample_kernel_ncu.txt"), "w").write(txt)
     la = os.path.join(GP, "launches_default.csv")
     if os.path.exists(la):
         open(os.path.join(OUT, f"{rnd}_launches_default.txt"), "w").write(launches(la))
-    b = os.path.join(GP, "bench_default.log")
-    if os.path.exists(b):
-        line = [l for l in open(b).read().splitlines() if l.startswith("{")][-1]
-        json.dump(json.loads(line), open(os.path.join(OUT, f"{rnd}_bench_default.json"), "w"), indent=1)
+    for name in ("bench_default", "bench_c1", "bench_c2", "bench_c3", "bench_c4", "bench_sample", "bench_sg",
+                 "bench_wang"):
+        b = os.path.join(GP, name + ".log")
+        if os.path.exists(b):
+            lines = [l for l in open(b).read().splitlines() if l.startswith("{")]
+            if lines:
+                json.dump(json.loads(lines[-1]), open(os.path.join(OUT, f"{rnd}_{name}.json"), "w"), indent=1)
     if traffic:
         json.dump(traffic, open(os.path.join(OUT, "ncu_traffic.json"), "w"), indent=1)
 
