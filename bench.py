@@ -667,8 +667,8 @@ def run_wang_op(args, cfg, rank, world, local_rank):
             "roofline": {"bound": "hbm", "achieved": None, "peak": measured_peaks()[0]["hbm_gbs"], "unit": "GB/s",
                          "frac": None, "traffic": None, "kernel": "pndf::tiled_query_kernel",
                          "kernel_ms": st["query_ms"] / max(1, st["timed_batches"]),
-                         "note": "tiles' Zc (%.0f MB) is L2-resident; rows per query vary with the footprint" %
-                                 (st["zc_bytes"] / 1e6)},
+                         "note": "16 tiles' Zc %.0f MB; Zc rows per query grow with the footprint (tiles overlapped)"
+                                 % (st["zc_bytes"] / 1e6)},
             "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
                              "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
             "gpu_launches": args.steps, "clocks": clk,

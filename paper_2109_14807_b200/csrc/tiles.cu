@@ -79,13 +79,16 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
                 for (int k = 0; k < 4; ++k) {
                     const int64_t iw = iu + (k & 1), jw = iv + (k >> 1);
                     const float wk = wk4[k];
-                    // tiles whose extended grid [-M, nl + M) holds this world cell (floor division by nl = 2^sh)
-                    const int64_t tx0 = (iw - (nl + M) + 1) >> sh, tx1 = (iw + M) >> sh;
-                    const int64_t ty0 = (jw - (nl + M) + 1) >> sh, ty1 = (jw + M) >> sh;
+                    // tiles whose texels this centre's footprint reaches: local cell il in [-2, nl + 1]
+                    // (support +-4 sigma = +-1.73 cells around the centre at (il + 1/2) cells); rows
+                    // further out in the extended grid are zero and skipped (exact: they add +0)
+                    const int64_t MA = M < 2 ? M : 2;
+                    const int64_t tx0 = (iw - (nl + MA) + 1) >> sh, tx1 = (iw + MA) >> sh;
+                    const int64_t ty0 = (jw - (nl + MA) + 1) >> sh, ty1 = (jw + MA) >> sh;
                     for (int64_t ty = ty0; ty <= ty1; ++ty)
                         for (int64_t tx = tx0; tx <= tx1; ++tx) {
                             const int64_t il = iw - (tx << sh), jl = jw - (ty << sh);
-                            if (il < -M || il >= nl + M || jl < -M || jl >= nl + M) continue;
+                            if (il < -MA || il >= nl + MA || jl < -MA || jl >= nl + MA) continue;
                             const int tile = tile_of(seed_mixed, tx, ty);
                             const int64_t row = (int64_t)tile * tp.p_ext + off + (jl + M) * ne + (il + M);
 #pragma unroll

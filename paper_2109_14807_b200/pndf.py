@@ -161,7 +161,7 @@ def sg_queries(d_lights, d_queries, ang_res: int, eps: float = 0.3, stream=None,
     """pndf_sg_queries: device SG-light records (32 B) -> device query records (16 B) for pndf_query_batch."""
     n = d_queries.shape[0] if n is None else n
     _check(lib().pndf_sg_queries(_ptr(d_lights), n, eps, ang_res, _ptr(d_queries), _stream(stream)),
-           "pndf_sg_queries", "pndf_load_tiles")
+           "pndf_sg_queries")
 
 
 def make_desc(N: int, s0: int, L: int, A: int, R: int, wrap: bool = True, prefix: int = PREFIX_AUTO) -> Desc:
