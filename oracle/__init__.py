@@ -38,6 +38,11 @@ class TilesDesc(ctypes.Structure):
                 ("A", ctypes.c_int32), ("R", ctypes.c_int32), ("seed", ctypes.c_uint64)]
 
 
+class BlockedDesc(ctypes.Structure):
+    _fields_ = [("N", ctypes.c_int32), ("s0", ctypes.c_int32), ("L", ctypes.c_int32), ("A", ctypes.c_int32),
+                ("t", ctypes.c_int32), ("region", ctypes.c_int32), ("R", ctypes.c_int32), ("wrap", ctypes.c_int32)]
+
+
 def build_lib(force: bool = False) -> str:
     """gcc -O2 -fopenmp (no -ffast-math, no hand SIMD)."""
     if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
@@ -61,6 +66,8 @@ def lib():
         L.oracle_tile_id.restype = ctypes.c_int
         L.oracle_tile_id.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64]
         L.oracle_tiled_query_batch.argtypes = [ctypes.POINTER(TilesDesc), P, P, P, P, P, ctypes.c_int64, ctypes.c_int, P]
+        L.oracle_blocked_query_batch.argtypes = [ctypes.POINTER(BlockedDesc), P, P, P, P, P, P, P, ctypes.c_int64,
+                                                 ctypes.c_int, P]
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -157,6 +164,21 @@ def tiled_query_batch(td: TilesDesc, C, X, Y, Z, records: np.ndarray, mean: bool
     out = np.empty(recs.shape[0], np.float64)
     lib().oracle_tiled_query_batch(ctypes.byref(td), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(recs),
                                    recs.shape[0], 1 if mean else 0, _ptr(out))
+    return out
+
+
+def blocked_query_batch(cfg, bs, records: np.ndarray, mean: bool = True) -> np.ndarray:
+    """Blocked / clustered store query (Sec. 4.2 + P:353): per neighbour, per overlapped angular block, the
+    group's Eq. 6 on the sub-rectangle.  cfg: pyramid geometry (N, s0, L, A, wrap); bs: synth.BlockedStore."""
+    d = BlockedDesc(N=cfg.N, s0=cfg.s0, L=cfg.L, A=cfg.A, t=bs.t, region=bs.region, R=bs.R,
+                    wrap=1 if cfg.wrap else 0)
+    recs = np.ascontiguousarray(records)
+    out = np.empty(recs.shape[0], np.float64)
+    arr = [np.ascontiguousarray(a, dt) for a, dt in ((bs.C, np.float32), (bs.X, np.float32), (bs.Y, np.float32),
+                                                    (bs.group_set, np.int32), (bs.slab_ptr, np.int64),
+                                                    (bs.Z, np.float32))]
+    lib().oracle_blocked_query_batch(ctypes.byref(d), *[_ptr(a) for a in arr], _ptr(recs), recs.shape[0],
+                                     1 if mean else 0, _ptr(out))
     return out
 
 

@@ -447,4 +447,78 @@ EXPORT void oracle_tiled_query_batch(const oracle_tiles* d, const float* C, cons
     }
 }
 
+/* ------------------------------------------------------------------------
+ * Blocked / clustered store (Sec. 4.2; range splitting P:353).
+ * Each NDF image is cut into t x t angular blocks; blocks of footprints centred
+ * in the same spatial region (side `region` texels) form a group with its own
+ * CP factors (Eq. 5 per group); all-blank blocks are dropped
+ * (P:294).  A query evaluates, for each of its 8 trilinear neighbours,
+ * every block the rectangle overlaps -- "when the angular range happen to
+ * overlap multiple image blocks, we subdivide it into smaller ones according to
+ * the boundary of the image blocks" -- with that block's group factors
+ * (Eq. 6 on the sub-rectangle), and sums.  Readings: a centre
+ * ((i+1/2)s, (j+1/2)s) belongs to region (floor(cx/region), floor(cy/region));
+ * group g = region * nb^2 + block; group_set[g] names the group's factor set
+ * (C, X, Y), slab_ptr[z][block] its slab (-1 = blank).  The sum over the
+ * sub-rectangles is the SUM over the whole rectangle; MEAN divides by its area.
+ */
+typedef struct {
+    int32_t N, s0, L, A, t, region, R, wrap;
+} oracle_blocked;
+
+EXPORT void oracle_blocked_query_batch(const oracle_blocked* d, const float* C, const float* X, const float* Y,
+                                       const int32_t* group_set, const int64_t* slab_ptr, const float* Z,
+                                       const oracle_rec* q, int64_t n, int mean, double* out) {
+    const oracle_desc pd = {d->N, d->s0, d->L, d->A, d->R, d->wrap};
+    const int t = d->t, nb = d->A / d->t, R = d->R;
+    const int64_t nr = d->N / d->region;
+#pragma omp parallel
+    {
+        double xs[4096], ys[4096];
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t qi = 0; qi < n; ++qi) {
+            int64_t rows[8];
+            double w[8];
+            int x1, x2, y1, y2;
+            if (!oracle_valid(&pd, &q[qi], &x1, &x2, &y1, &y2) || !oracle_neighbours(&pd, &q[qi], rows, w)) {
+                out[qi] = NAN;
+                continue;
+            }
+            double sum = 0.0;
+            for (int k = 0; k < 8; ++k) {
+                /* level, cell and region of row z */
+                int64_t z = rows[k], off = 0;
+                int l = 0;
+                for (;; ++l) {
+                    const int64_t nn = d->N / ((int64_t)d->s0 << l);
+                    if (z < off + nn * nn) break;
+                    off += nn * nn;
+                }
+                const int64_t s = (int64_t)d->s0 << l, nn = d->N / s, c = z - off, i = c % nn, j = c / nn;
+                const int64_t reg = (((2 * j + 1) * s) / (2 * d->region)) * nr + ((2 * i + 1) * s) / (2 * d->region);
+                for (int byb = y1 / t; byb <= y2 / t; ++byb)
+                    for (int bxb = x1 / t; bxb <= x2 / t; ++bxb) {
+                        const int b = byb * nb + bxb;
+                        const int64_t slab = slab_ptr[z * nb * nb + b];
+                        if (slab < 0) continue; /* blank block */
+                        const int set = group_set[reg * nb * nb + b];
+                        if (set < 0) continue;
+                        const int lx1 = (x1 > bxb * t ? x1 : bxb * t) - bxb * t;
+                        const int lx2 = (x2 < bxb * t + t - 1 ? x2 : bxb * t + t - 1) - bxb * t;
+                        const int ly1 = (y1 > byb * t ? y1 : byb * t) - byb * t;
+                        const int ly2 = (y2 < byb * t + t - 1 ? y2 : byb * t + t - 1) - byb * t;
+                        for (int r = 0; r < R; ++r) { xs[r] = 0.0; ys[r] = 0.0; }
+                        for (int x = lx1; x <= lx2; ++x)
+                            for (int r = 0; r < R; ++r) xs[r] += (double)X[((int64_t)set * t + x) * R + r];
+                        for (int y = ly1; y <= ly2; ++y)
+                            for (int r = 0; r < R; ++r) ys[r] += (double)Y[((int64_t)set * t + y) * R + r];
+                        sum += w[k] * oracle_range_sum(&pd, C + (int64_t)set * R, xs, ys, Z + slab * R);
+                    }
+            }
+            if (mean) sum /= (double)(x2 - x1 + 1) * (double)(y2 - y1 + 1);
+            out[qi] = sum;
+        }
+    }
+}
+
 EXPORT int oracle_max_threads(void) { return omp_get_max_threads(); }

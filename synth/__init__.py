@@ -415,6 +415,122 @@ def wang_factors(tc: TileConfig, tiles: np.ndarray):
     return Factors(C=np.ones(tc.R, np.float32), X=X, Y=Y, Z=Z, info=dict(atom_bins=ab, atom_map=am, rows=P))
 
 
+@dataclass
+class BlockedStore:
+    """Paper-faithful blocked / clustered store inputs."""
+    t: int                    # angular block side
+    region: int               # spatial region side (texels) of the footprint centres
+    R: int                    # rank per group
+    C: np.ndarray             # [n_sets, R]
+    X: np.ndarray             # [n_sets, t, R]
+    Y: np.ndarray             # [n_sets, t, R]
+    group_set: np.ndarray     # [n_groups] int32 factor set of the group (-1 = empty group)
+    slab_ptr: np.ndarray      # [P, nb*nb] int64 global slab index or -1 (blank block)
+    Z: np.ndarray             # [n_slabs, R]
+    info: dict = field(default_factory=dict)
+
+
+def _block_profiles(A, t, R, atom_bins_local, sigma_b):
+    """Atom profiles truncated to the atom's block and renormalised (so the block holds all the mass)."""
+    Xb = np.zeros((t, R), np.float32)
+    Yb = np.zeros((t, R), np.float32)
+    from math import erf, sqrt
+    for k, (cx, cy) in enumerate(atom_bins_local):
+        if cx < 0:
+            continue
+        for F, c in ((Xb, cx), (Yb, cy)):
+            col = np.zeros(t)
+            if sigma_b <= 0:
+                col[c] = 1.0
+            else:
+                T = int(np.ceil(4 * sigma_b))
+                for x in range(max(0, c - T), min(t, c + T + 1)):
+                    lo, hi = (x - (c + 0.5)) / sigma_b, (x + 1 - (c + 0.5)) / sigma_b
+                    col[x] = 0.5 * (erf(hi / sqrt(2)) - erf(lo / sqrt(2)))
+            F[:, k] = (col / col.sum()).astype(np.float32)
+    return Xb, Yb
+
+
+def build_blocked(cfg: Config, nxy: np.ndarray | None = None, bins: np.ndarray | None = None, t: int = 16,
+                  region: int = 8, sigma_b: float | None = None) -> tuple:
+    """Exact-rank blocked store: per angular block b the R most populated bins of b are its atoms, every texel
+    snaps to the nearest atom of its own block, and group (region, b) holds the slabs of all footprints centred
+    in the region whose block b is not blank (blank blocks pruned).  Returns (BlockedStore,
+    global_factors) -- the second is the same tensor as ONE global CP store (rank nb^2 R) for cross-checks."""
+    assert cfg.A % t == 0
+    if bins is None:
+        bins = bin_map(cfg, make_map(cfg) if nxy is None else nxy)
+    A, R, nb = cfg.A, cfg.R, cfg.A // t
+    sigma_b = cfg.sigma_r * A / 2.0 if sigma_b is None else sigma_b
+    bx, by = bins.astype(np.int64) % A, bins.astype(np.int64) // A
+    blk = (by // t) * nb + (bx // t)
+    cnt = np.bincount(bins.ravel().astype(np.int64), minlength=A * A)
+    atom_local = -np.ones((nb * nb, R, 2), np.int64)
+    lut = np.zeros(A * A, np.int64)  # bin -> global atom id b*R + k
+    for b in range(nb * nb):
+        ox, oy = (b % nb) * t, (b // nb) * t
+        ids = np.array([(oy + y) * A + ox + x for y in range(t) for x in range(t)])
+        c = cnt[ids]
+        pop = ids[c > 0]
+        if pop.size == 0:
+            continue
+        order = np.lexsort((pop, -cnt[pop]))[:R]
+        ab = pop[order]
+        atom_local[b, :ab.size, 0] = ab % A - ox
+        atom_local[b, :ab.size, 1] = ab // A - oy
+        axx, ayy = ab % A, ab // A
+        px, py = pop % A, pop // A
+        d2 = (px[:, None] - axx[None, :]) ** 2 + (py[:, None] - ayy[None, :]) ** 2
+        lut[pop] = b * R + np.argmin(d2, axis=1)
+    am = lut[bins.astype(np.int64)].astype(np.uint16)
+    Rt = nb * nb * R
+    assert Rt <= 65535
+    gcfg = cfg.scaled(R=Rt)
+    Zg = build_z_exact(gcfg, np.ascontiguousarray(am))            # [P, nb^2 R]
+    sets_X = np.zeros((nb * nb, t, R), np.float32)
+    sets_Y = np.zeros((nb * nb, t, R), np.float32)
+    for b in range(nb * nb):
+        sets_X[b], sets_Y[b] = _block_profiles(A, t, R, atom_local[b], sigma_b)
+    # groups: (region of the footprint centre, block)
+    nr = cfg.N // region
+    P = cfg.P
+    zr = np.zeros(P, np.int64)
+    off = 0
+    for l in range(cfg.L):
+        s = cfg.s0 << l
+        n = cfg.N // s
+        j, i = np.divmod(np.arange(n * n), n)
+        rx = ((2 * i + 1) * s) // (2 * region)
+        ry = ((2 * j + 1) * s) // (2 * region)
+        zr[off:off + n * n] = ry * nr + rx
+        off += n * n
+    mass = Zg.reshape(P, nb * nb, R).sum(axis=2)                  # per (row, block)
+    nonblank = mass > 0
+    slab_ptr = -np.ones((P, nb * nb), np.int64)
+    # slabs grouped by (region, block): sort (group, row) pairs
+    rows, blocks = np.nonzero(nonblank)
+    groups = zr[rows] * (nb * nb) + blocks
+    order = np.lexsort((rows, groups))
+    rows, blocks = rows[order], blocks[order]
+    slab_ptr[rows, blocks] = np.arange(rows.size)
+    Zs = Zg.reshape(P, nb * nb, R)[rows, blocks]                  # [S, R]
+    group_set = -np.ones(nr * nr * nb * nb, np.int32)
+    group_set[np.unique(groups)] = (np.unique(groups) % (nb * nb)).astype(np.int32)
+    store = BlockedStore(t=t, region=region, R=R, C=np.ones((nb * nb, R), np.float32), X=sets_X, Y=sets_Y,
+                         group_set=group_set, slab_ptr=slab_ptr, Z=np.ascontiguousarray(Zs, np.float32),
+                         info=dict(n_slabs=int(rows.size), blank_fraction=float(1 - nonblank.mean()),
+                                   n_groups=int(np.unique(groups).size)))
+    # the same tensor as one global CP store: profiles embedded in the full grid
+    Xg = np.zeros((A, Rt), np.float32)
+    Yg = np.zeros((A, Rt), np.float32)
+    for b in range(nb * nb):
+        ox, oy = (b % nb) * t, (b // nb) * t
+        Xg[ox:ox + t, b * R:(b + 1) * R] = sets_X[b]
+        Yg[oy:oy + t, b * R:(b + 1) * R] = sets_Y[b]
+    glob = Factors(C=np.ones(Rt, np.float32), X=Xg, Y=Yg, Z=Zg, info=dict(R=Rt))
+    return store, glob
+
+
 def pack_rect(x1, x2, y1, y2):
     x1, x2, y1, y2 = (np.asarray(a, np.uint32) for a in (x1, x2, y1, y2))
     return x1 | (x2 << 8) | (y1 << 16) | (y2 << 24)
