@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang"],
+    ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang", "blocked"],
                     help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
                          "prefiltering (SG rectangle generation + range query)")
@@ -141,12 +141,17 @@ class ClockSampler:
             if self.bus_id:
                 cmd += ["-i", self.bus_id]
             self.proc = subprocess.Popen(cmd, stdout=self.f, stderr=subprocess.DEVNULL)
+            # wait (<= 3 s) until the sampler is live, so even a timed region of a few ms is covered
+            t0 = time.time()
+            while time.time() - t0 < 3.0 and self.proc.poll() is None and os.path.getsize(self.f.name) == 0:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
 
     def stop(self):
         if not self.proc:
             return None
+        time.sleep(0.25)  # one more sample at the end of the region (short regions)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -680,6 +685,94 @@ def run_wang_op(args, cfg, rank, world, local_rank):
     return 0
 
 
+BLOCKED_METRIC = "NDF range queries/sec on the blocked/clustered store (Sec. 4.2: t=16 blocks, 8x8-texel regions)"
+
+
+def blocked_roofline(cfg, n, k_ms):
+    """Algorithmic bytes of the blocked query: record + result, and per bilinear neighbour of both levels one
+    block's slab pointer + group set (8 B), its Zc row (4R) and 8 HILO prefix rows (32R).  Counts one
+    non-blank block per neighbour: rectangles that cross block borders read more, blank blocks less."""
+    peaks, src = measured_peaks()
+    Bq = 20 + 8 * (8 + 36 * cfg.R)
+    achieved = Bq * n / (k_ms * 1e-3) / 1e9
+    return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "pndf::blocked_query_kernel",
+            "kernel_ms": k_ms, "bytes_per_query": Bq, "peak_source": src,
+            "note": blocked_roofline.__doc__.split("\n")[0].strip()}
+
+
+def run_blocked_op(args, cfg, rank, world, local_rank):
+    """--op blocked: the config's queries on the paper-faithful blocked / clustered store (exact-rank groups)."""
+    import torch
+    import torch.distributed as dist
+    import oracle
+    from paper_2109_14807_b200 import pndf
+    from paper_2109_14807_b200.shard import reduce_times_and_checksum, shard_range
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n_total = args.queries or cfg.n_queries
+    i0, i1 = shard_range(n_total, rank, world)
+    n = i1 - i0
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    bs, _ = synth.build_blocked(cfg, nxy, bins, t=16, region=8)
+    store = pndf.load_blocked(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.wrap, bs, device=local_rank)
+    recs = synth.gen_queries(cfg, bins, i0, i1)
+    d_q = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).to(dev)
+    d_out = torch.empty(n, dtype=torch.float32, device=dev)
+    for _ in range(args.warmup):
+        store.query_batch(d_q, d_out, 0)
+        store.sync()
+    store.reset_stats()
+    clocks = ClockSampler(bus_id_of(dev))
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        store.query_batch(d_q, d_out, pndf.TIMING)
+        store.sync()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    st = store.stats()
+    ms_rank = e0.elapsed_time(e1) / args.steps
+    (ms_step,), _ = reduce_times_and_checksum([ms_rank], 0.0, dev)
+    if rank != 0:
+        store.free()
+        return 0
+    idx = np.unique(np.random.default_rng(6).integers(0, n, min(n, 20000)))
+    t0 = time.perf_counter()
+    ref = oracle.blocked_query_batch(cfg, bs, recs[idx])
+    cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
+    got = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref)
+    nb = cfg.A // 16
+    raw = cfg.P * cfg.A * cfg.A * 4
+    comp = st["zc_bytes"] + st["prefix_bytes"] + cfg.P * nb * nb * 4 + bs.group_set.size * 4
+    line = {"metric": BLOCKED_METRIC, "value": n_total / (ms_step * 1e-3), "unit": "queries/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(cfg) + "; blocked store t=16, 8-texel regions",
+                       "queries_total": n_total, "slabs": bs.info["n_slabs"], "groups": bs.info["n_groups"],
+                       "blank_block_fraction": bs.info["blank_fraction"],
+                       "storage_vs_raw_pyramid": comp / raw},
+            "roofline": blocked_roofline(cfg, n, st["query_ms"] / max(1, st["timed_batches"])),
+            "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
+                             "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
+            "gpu_launches": args.steps, "clocks": clk,
+            "parity_sample": {"checked": int(idx.shape[0]),
+                              "pass": bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())},
+            "e2e": None}
+    print(json.dumps(line), flush=True)
+    store.free()
+    return 0
+
+
 def main():
     args = parse()
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -700,6 +793,8 @@ def main():
             return run_sg_op(args, cfg, rank, world, local_rank)
         if args.op == "wang":
             return run_wang_op(args, cfg, rank, world, local_rank)
+        if args.op == "blocked":
+            return run_blocked_op(args, cfg, rank, world, local_rank)
         return run_ours(args, cfg, rank, world, local_rank)
     finally:
         if world > 1:

@@ -222,6 +222,40 @@ typedef struct {
 pndf_status pndf_load_tiles(const pndf_tile_desc* desc, const float* C, const float* X, const float* Y,
                             const float* Z, int device, void* cuda_stream, pndf_store* out);
 
+/* Blocked / clustered store (Sec. 4.2).  Each
+ * A x A NDF image is cut into t x t angular blocks; the blocks of footprints
+ * centred in the same spatial region (side `region` texels: centre
+ * ((i+1/2)s, (j+1/2)s) is in region (floor(cx/region), floor(cy/region)))
+ * form a group g = region_index * nb^2 + block (nb = A/t) with its own CP
+ * factors; blank blocks are pruned.  A query sums,
+ * over its 8 trilinear neighbours and over every block its rectangle overlaps
+ * (the range is split on block boundaries), Eq. 6 on the sub-rectangle
+ * with that block's group factors -- so the angular SAT rows are fetched per
+ * neighbour, as in the paper.  Inputs (host or device, copied):
+ *   C [num_sets][R], X [num_sets][t][R], Y [num_sets][t][R]  factor sets
+ *   group_set [(N/region)^2 * nb^2] int32   factor set of each group (-1 = empty)
+ *   slab_ptr  [P][nb^2] int64               Z row of (positional row, block), -1 = blank
+ *   Z [num_slabs][R]                          per-slab positional factors
+ * SATs are stored in the HILO format.  pndf_query_batch answers queries on it
+ * (never binned); pndf_sample_batch returns PNDF_EINVAL. */
+typedef struct {
+    uint32_t abi_version; /* = PNDF_ABI_VERSION                                   */
+    int32_t map_size;     /* N                                                    */
+    int32_t base_stride;  /* s0                                                   */
+    int32_t num_levels;   /* L                                                    */
+    int32_t ang_res;      /* A, a multiple of block                              */
+    int32_t block;        /* t, 1 <= t <= 64                                      */
+    int32_t region;       /* spatial region side in texels, power of two, <= N   */
+    int32_t rank;         /* R (per group)                                        */
+    uint32_t flags;       /* PNDF_WRAP or PNDF_CLAMP                             */
+    int32_t num_sets;     /* factor sets                                          */
+    int64_t num_slabs;    /* rows of Z, < 2^31                                    */
+} pndf_block_desc;
+
+pndf_status pndf_load_blocked(const pndf_block_desc* desc, const float* C, const float* X, const float* Y,
+                              const int32_t* group_set, const int64_t* slab_ptr, const float* Z, int device,
+                              void* cuda_stream, pndf_store* out);
+
 /* Test support: run only the binning pass (row a1) on n device records and copy
  * the permutation (query indices in binned order) to d_perm [n] and, if not
  * NULL, the sorted bin keys to d_keys [n] (device memory).  Synchronous. */

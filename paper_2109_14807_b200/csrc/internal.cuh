@@ -44,6 +44,16 @@ struct TileParams {
     uint64_t seed;    // vertex-hash seed
 };
 
+// Blocked / clustered store (blocks.cu).
+struct BlockParams {
+    int32_t t;                  // angular block side
+    int32_t nb;                 // blocks per axis (A / t)
+    int32_t region;             // spatial region side (texels)
+    int32_t nr;                 // regions per axis (N / region)
+    const int32_t* slab_ptr;    // [P][nb^2] Zc row or -1
+    const int32_t* group_set;   // [nr^2 * nb^2] factor set or -1
+};
+
 // Device scratch of one in-flight binned batch (radix sort double buffers).
 struct BinScratch {
     uint32_t* keys[2] = {nullptr, nullptr};

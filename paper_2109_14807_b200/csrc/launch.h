@@ -41,6 +41,13 @@ cudaError_t launch_sample_hilo_clamp(int G, int NV, const QParams& p, const pndf
 cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q, int64_t n,
                                float* out, int num_sms, cudaStream_t st);
 
+// Blocked / clustered store (blocks.cu).
+cudaError_t launch_blocked_query(const QParams& p, const BlockParams& bp, int G, int NV, const pndf_query* q,
+                                 int64_t n, float* out, int num_sms, cudaStream_t st);
+cudaError_t launch_block_build(const float* X, const float* Y, int sets, int t, int R, int Rp, float* pool,
+                               const float* Z, int64_t slabs, const float* C, const int32_t* slab_set, float* Zc,
+                               uint32_t* flags, int num_sms, cudaStream_t st);
+
 // Environment-prefiltering rectangles (sg.cu).
 cudaError_t launch_sg_rects(const pndf_sg_light* in, int64_t n, float eps, int A, pndf_query* out, int num_sms,
                             cudaStream_t st);

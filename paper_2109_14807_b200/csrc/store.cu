@@ -94,6 +94,10 @@ struct pndf_store_s {
     int64_t nbins = 0;  // P + 1 (last = invalid records); 0 if binning infeasible
     bool tiled = false;  // Wang-tile store (pndf_load_tiles)
     TileParams tp{};
+    bool blocked = false;  // blocked / clustered store (pndf_load_blocked)
+    BlockParams bp{};
+    int32_t* d_slab_ptr = nullptr;
+    int32_t* d_group_set = nullptr;
     QParams qp{};
     float* Zc = nullptr;
     float* PXY = nullptr;
@@ -172,6 +176,16 @@ pndf_status enqueue(pndf_store_s* s, Scratch& sc, const pndf_query* q, int64_t n
                     cudaStream_t st, bool timing) {
     QParams p = s->qp;
     p.mean = (opts & PNDF_SUM) ? 0u : 1u;
+    if (s->blocked) {  // blocked / clustered store: one kernel, never binned
+        if (opts & PNDF_BIN_ON) return PNDF_EINVAL;
+        if (timing) CK(cudaEventRecord(s->ev[0], st));
+        if (timing) CK(cudaEventRecord(s->ev[1], st));
+        CK(launch_blocked_query(p, s->bp, s->G, s->NV, q, n, out, s->num_sms, st));
+        if (timing) CK(cudaEventRecord(s->ev[2], st));
+        s->stats.kernel_launches += 1;
+        s->stats.last_binned = 0;
+        return PNDF_OK;
+    }
     if (s->tiled) {  // Wang-tiled world queries: one kernel, never binned
         if (opts & PNDF_BIN_ON) return PNDF_EINVAL;
         if (timing) CK(cudaEventRecord(s->ev[0], st));
@@ -230,6 +244,8 @@ void destroy(pndf_store_s* s) {
     cudaFree(s->Zc);
     cudaFree(s->PXY);
     cudaFree(s->err);
+    cudaFree(s->d_slab_ptr);
+    cudaFree(s->d_group_set);
     s->main.release();
     for (auto& sl : s->slots) sl.release();
     for (auto& e : s->ev)
@@ -303,6 +319,164 @@ pndf_status pndf_load_tiles(const pndf_tile_desc* td, const float* C, const floa
     s->tp.p_ext = pext;
     s->tp.seed = td->seed;
     s->qp.wrap = 0;
+    return PNDF_OK;
+}
+
+pndf_status pndf_load_blocked(const pndf_block_desc* bd, const float* C, const float* X, const float* Y,
+                              const int32_t* group_set, const int64_t* slab_ptr, const float* Z, int device,
+                              void* cuda_stream, pndf_store* out) {
+    if (!out || !bd || !C || !X || !Y || !group_set || !slab_ptr || (bd->num_slabs > 0 && !Z)) return PNDF_EINVAL;
+    *out = nullptr;
+    if (bd->abi_version != PNDF_ABI_VERSION) return PNDF_EFORMAT;
+    pndf_desc d;
+    d.abi_version = PNDF_ABI_VERSION;
+    d.map_size = bd->map_size;
+    d.base_stride = bd->base_stride;
+    d.num_levels = bd->num_levels;
+    d.ang_res = bd->ang_res;
+    d.rank = bd->rank;
+    d.flags = bd->flags & PNDF_WRAP;
+    pndf_status r = validate_desc(&d);
+    if (r != PNDF_OK) return r;
+    const int t = bd->block, A = bd->ang_res, R = bd->rank;
+    if (t < 1 || t > 64 || A % t != 0) return PNDF_EINVAL;
+    if (!is_pow2(bd->region) || bd->region > bd->map_size) return PNDF_EINVAL;
+    if (bd->num_sets < 1 || bd->num_slabs < 0 || bd->num_slabs >= (int64_t(1) << 31)) return PNDF_EINVAL;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return PNDF_EINVAL;
+    DeviceGuard guard(device);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const int nb = A / t, nb2 = nb * nb;
+    const int64_t nr = bd->map_size / bd->region, n0 = bd->map_size / bd->base_stride;
+    int64_t P = 0;
+    for (int l = 0; l < bd->num_levels; ++l) P += (n0 >> l) * (n0 >> l);
+    const int64_t G = nr * nr * nb2, S = bd->num_slabs, sets = bd->num_sets;
+    // host copies of the index tables; per-slab factor set for the fold
+    std::vector<int32_t> hg(G);
+    std::vector<int64_t> hs(P * nb2);
+    CK(cudaMemcpy(hg.data(), group_set, sizeof(int32_t) * G, cudaMemcpyDefault));
+    CK(cudaMemcpy(hs.data(), slab_ptr, sizeof(int64_t) * P * nb2, cudaMemcpyDefault));
+    std::vector<int32_t> hs32(P * nb2), slab_set(S, -1);
+    {
+        int64_t off = 0;
+        for (int l = 0; l < bd->num_levels; ++l) {
+            const int64_t nl = n0 >> l, sl = (int64_t)bd->base_stride << l;
+            for (int64_t c = 0; c < nl * nl; ++c) {
+                const int64_t i = c % nl, j = c / nl;
+                const int64_t reg = (((2 * j + 1) * sl) / (2 * bd->region)) * nr + ((2 * i + 1) * sl) / (2 * bd->region);
+                for (int b = 0; b < nb2; ++b) {
+                    const int64_t slab = hs[(off + c) * nb2 + b];
+                    if (slab < -1 || slab >= S) return PNDF_EINVAL;
+                    hs32[(off + c) * nb2 + b] = (int32_t)slab;
+                    if (slab < 0) continue;
+                    const int32_t set = hg[reg * nb2 + b];
+                    if (set < 0 || set >= sets) return PNDF_EINVAL;  // a slab without factors
+                    slab_set[slab] = set;
+                }
+            }
+            off += nl * nl;
+        }
+    }
+    for (int64_t sl = 0; sl < S; ++sl)
+        if (slab_set[sl] < 0) slab_set[sl] = 0;  // unreferenced slab: any valid set
+    for (int64_t g = 0; g < G; ++g)
+        if (hg[g] < -1 || hg[g] >= sets) return PNDF_EINVAL;
+
+    pndf_store_s* s = new (std::nothrow) pndf_store_s();
+    if (!s) return PNDF_ENOMEM;
+    s->d = d;
+    s->device = device;
+    s->P = S;
+    choose_lanes(R, &s->G0, &s->NV0);
+    s->G = s->G0;
+    s->NV = s->NV0;
+    s->Rp = 4 * s->G0 * s->NV0;
+    const int Rp = s->Rp;
+    int v = 0;
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device);
+    s->num_sms = v > 0 ? v : 148;
+    cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device);
+    s->l2_bytes = v;
+    s->nbins = 0;
+    auto fail = [&](pndf_status e) {
+        destroy(s);
+        return e;
+    };
+    const size_t zc_bytes = sizeof(float) * (size_t)std::max<int64_t>(S, 1) * Rp;
+    const size_t pool_bytes = sizeof(float) * (size_t)sets * 2 * (t + 1) * 2 * Rp;
+    float *dC = nullptr, *dX = nullptr, *dY = nullptr, *dZ = nullptr;
+    int32_t* dset = nullptr;
+    auto free_tmp = [&]() {
+        cudaFree(dC);
+        cudaFree(dX);
+        cudaFree(dY);
+        cudaFree(dZ);
+        cudaFree(dset);
+    };
+    cudaError_t e = cudaSuccess;
+    auto ok = [&](cudaError_t ce) {
+        if (e == cudaSuccess) e = ce;
+        return e == cudaSuccess;
+    };
+    ok(cudaMalloc(&s->Zc, zc_bytes));
+    ok(cudaMalloc(&s->PXY, pool_bytes));
+    ok(cudaMalloc(&s->err, 2 * sizeof(uint32_t)));
+    ok(cudaMalloc(&s->d_slab_ptr, sizeof(int32_t) * P * nb2));
+    ok(cudaMalloc(&s->d_group_set, sizeof(int32_t) * G));
+    ok(cudaMalloc(&dC, sizeof(float) * sets * R));
+    ok(cudaMalloc(&dX, sizeof(float) * sets * t * R));
+    ok(cudaMalloc(&dY, sizeof(float) * sets * t * R));
+    ok(cudaMalloc(&dZ, sizeof(float) * std::max<int64_t>(S, 1) * R));
+    ok(cudaMalloc(&dset, sizeof(int32_t) * std::max<int64_t>(S, 1)));
+    for (auto& ev : s->ev) ok(cudaEventCreate(&ev));
+    if (e != cudaSuccess) {
+        free_tmp();
+        return fail(cuda_fail(e, "cudaMalloc(blocked store)"));
+    }
+    ok(cudaMemsetAsync(s->err, 0, 2 * sizeof(uint32_t), st));
+    ok(cudaMemcpy(dC, C, sizeof(float) * sets * R, cudaMemcpyDefault));
+    ok(cudaMemcpy(dX, X, sizeof(float) * sets * t * R, cudaMemcpyDefault));
+    ok(cudaMemcpy(dY, Y, sizeof(float) * sets * t * R, cudaMemcpyDefault));
+    if (S > 0) ok(cudaMemcpy(dZ, Z, sizeof(float) * S * R, cudaMemcpyDefault));
+    if (S > 0) ok(cudaMemcpy(dset, slab_set.data(), sizeof(int32_t) * S, cudaMemcpyHostToDevice));
+    ok(cudaMemcpy(s->d_slab_ptr, hs32.data(), sizeof(int32_t) * P * nb2, cudaMemcpyHostToDevice));
+    ok(cudaMemcpy(s->d_group_set, hg.data(), sizeof(int32_t) * G, cudaMemcpyHostToDevice));
+    ok(launch_block_build(dX, dY, (int)sets, t, R, Rp, s->PXY, dZ, S, dC, dset, s->Zc, s->err + 1, s->num_sms, st));
+    ok(cudaStreamSynchronize(st));
+    uint32_t hflags = 0;
+    ok(cudaMemcpy(&hflags, s->err + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost));
+    free_tmp();
+    if (e != cudaSuccess) return fail(cuda_fail(e, "blocked store build"));
+    if (hflags & 1u) return fail(PNDF_EINVAL);
+    s->stats.kernel_launches += 2;
+    QParams& p = s->qp;
+    p.Zc = s->Zc;
+    p.PXY = s->PXY;
+    p.err = s->err;
+    p.N = d.map_size;
+    p.n0 = (int32_t)n0;
+    p.L = d.num_levels;
+    p.A = A;
+    p.Rp = Rp;
+    p.wrap = (d.flags & PNDF_WRAP) ? 1 : 0;
+    p.prefix_u32 = 0;
+    p.inv_s0 = 1.0f / (float)d.base_stride;
+    p.mean = 1;
+    s->blocked = true;
+    s->bp.t = t;
+    s->bp.nb = nb;
+    s->bp.region = bd->region;
+    s->bp.nr = (int32_t)nr;
+    s->bp.slab_ptr = s->d_slab_ptr;
+    s->bp.group_set = s->d_group_set;
+    s->stats.rows = S;
+    s->stats.rank_padded = Rp;
+    s->stats.lanes_per_query = s->G;
+    s->stats.zc_bytes = (int64_t)zc_bytes;
+    s->stats.prefix_bytes = (int64_t)pool_bytes;
+    s->stats.prefix_format = 0;
+    *out = s;
     return PNDF_OK;
 }
 
@@ -529,7 +703,7 @@ pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const f
     if (n == 0) return PNDF_OK;
     if ((uintptr_t)d_queries % 16 != 0 || (uintptr_t)d_out % 16 != 0 || (uintptr_t)d_xi % 4 != 0)
         return PNDF_EINVAL;
-    if (s->tiled) return PNDF_EINVAL;  // sampling a tiled store is not supported
+    if (s->tiled || s->blocked) return PNDF_EINVAL;  // sampling: one-group stores only
     std::lock_guard<std::mutex> lk(s->mu);
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)cuda_stream;
@@ -691,7 +865,7 @@ pndf_status pndf_bin_permutation(pndf_store s, const pndf_query* d_queries, int6
                                  uint32_t* d_keys) {
     if (!s || n < 0 || (n > 0 && (!d_queries || !d_perm))) return PNDF_EINVAL;
     if (n == 0) return PNDF_OK;
-    if (n > (int64_t(1) << 30) || s->nbins == 0) return PNDF_EINVAL;
+    if (n > (int64_t(1) << 30) || s->nbins == 0 || s->tiled || s->blocked) return PNDF_EINVAL;
     std::lock_guard<std::mutex> lk(s->mu);
     DeviceGuard g(s->device);
     pndf_status r = ensure_scratch(s->main, n, nullptr);

@@ -47,6 +47,13 @@ class TileDesc(ctypes.Structure):
                 ("rank", ctypes.c_int32), ("flags", ctypes.c_uint32), ("seed", ctypes.c_uint64)]
 
 
+class BlockDesc(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_uint32), ("map_size", ctypes.c_int32), ("base_stride", ctypes.c_int32),
+                ("num_levels", ctypes.c_int32), ("ang_res", ctypes.c_int32), ("block", ctypes.c_int32),
+                ("region", ctypes.c_int32), ("rank", ctypes.c_int32), ("flags", ctypes.c_uint32),
+                ("num_sets", ctypes.c_int32), ("num_slabs", ctypes.c_int64)]
+
+
 class StoreStats(ctypes.Structure):
     _fields_ = [("rows", ctypes.c_int64), ("rank_padded", ctypes.c_int32), ("lanes_per_query", ctypes.c_int32),
                 ("zc_bytes", ctypes.c_int64), ("prefix_bytes", ctypes.c_int64),
@@ -64,7 +71,7 @@ EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_s
            "pndf_free",
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
-           "pndf_sg_queries", "pndf_load_tiles")
+           "pndf_sg_queries", "pndf_load_tiles", "pndf_load_blocked")
 
 SG_DTYPE = np.dtype([("u", "<f4"), ("v", "<f4"), ("size", "<f4"), ("hx", "<f4"), ("hy", "<f4"),
                      ("lam", "<f4"), ("amp", "<f4"), ("pad", "<f4")])
@@ -107,6 +114,9 @@ def lib():
         L.pndf_bin_permutation.argtypes = [P, P, i64, P, P]
         L.pndf_load_tiles.restype = i32
         L.pndf_load_tiles.argtypes = [ctypes.POINTER(TileDesc), P, P, P, P, ctypes.c_int, P, ctypes.POINTER(P)]
+        L.pndf_load_blocked.restype = i32
+        L.pndf_load_blocked.argtypes = [ctypes.POINTER(BlockDesc), P, P, P, P, P, P, ctypes.c_int, P,
+                                        ctypes.POINTER(P)]
         L.pndf_sg_queries.restype = i32
         L.pndf_sg_queries.argtypes = [P, i64, ctypes.c_float, i32, P, P]
         L.pndf_set_lanes.restype = i32
@@ -274,3 +284,18 @@ def load_tiles(td: TileDesc, C, X, Y, Z, device: int = 0, stream=None) -> Store:
                                  ctypes.byref(h)), "pndf_load_tiles")
     d = make_desc(td.tile_size, td.base_stride, td.num_levels, td.ang_res, td.rank, False)
     return Store(h, d)
+
+
+def load_blocked(N: int, s0: int, L: int, A: int, wrap: bool, bs, device: int = 0, stream=None) -> Store:
+    """pndf_load_blocked from a synth.BlockedStore-like object (t, region, R, C, X, Y, group_set, slab_ptr, Z)."""
+    arr = dict(C=np.ascontiguousarray(bs.C, np.float32), X=np.ascontiguousarray(bs.X, np.float32),
+               Y=np.ascontiguousarray(bs.Y, np.float32), G=np.ascontiguousarray(bs.group_set, np.int32),
+               S=np.ascontiguousarray(bs.slab_ptr, np.int64), Z=np.ascontiguousarray(bs.Z, np.float32))
+    bd = BlockDesc(abi_version=ABI_VERSION, map_size=N, base_stride=s0, num_levels=L, ang_res=A, block=bs.t,
+                   region=bs.region, rank=bs.R, flags=WRAP if wrap else CLAMP, num_sets=arr["C"].shape[0],
+                   num_slabs=arr["Z"].shape[0])
+    h = ctypes.c_void_p()
+    _check(lib().pndf_load_blocked(ctypes.byref(bd), _ptr(arr["C"]), _ptr(arr["X"]), _ptr(arr["Y"]),
+                                   _ptr(arr["G"]), _ptr(arr["S"]), _ptr(arr["Z"]), device, _stream(stream),
+                                   ctypes.byref(h)), "pndf_load_blocked")
+    return Store(h, make_desc(N, s0, L, A, bs.R, wrap))
