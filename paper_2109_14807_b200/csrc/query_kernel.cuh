@@ -135,6 +135,9 @@ constexpr int kWarpsPerBlock = kThreads / 32;
 #endif
 constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced together
 
+#ifndef PNDF_F2
+#define PNDF_F2 1  // 1: packed fp32 FFMA2/FMUL2 for the interpolation and rank product (sm_100)
+#endif
 #ifndef PNDF_TMA
 #define PNDF_TMA 0  // 1: stage SAT rows of the next query in smem with TMA bulk copies (measured slower on B200)
 #endif
@@ -271,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                         for (int k = 0; k < 8; ++k) zc[v][k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
                 }
                 float acc = 0.f;
+                float2 acc2 = make_float2(0.f, 0.f);
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     const int c = (gl + v * G) * 4;
@@ -321,6 +325,19 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                         dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
                                          (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
                     }
+#if PNDF_F2
+                    // packed fp32 (FFMA2/FMUL2, sm_100): two ranks per instruction, same per-element
+                    // rounding as the scalar chain; the rank sum runs in two interleaved halves
+                    float2 zxy = make_float2(0.f, 0.f), zzw = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int k = 0; k < 8; ++k) {
+                        const float2 wk = make_float2(w[k], w[k]);
+                        zxy = __ffma2_rn(wk, make_float2(zc[v][k].x, zc[v][k].y), zxy);
+                        zzw = __ffma2_rn(wk, make_float2(zc[v][k].z, zc[v][k].w), zzw);
+                    }
+                    acc2 = __ffma2_rn(__fmul2_rn(make_float2(dx.x, dx.y), make_float2(dy.x, dy.y)), zxy, acc2);
+                    acc2 = __ffma2_rn(__fmul2_rn(make_float2(dx.z, dx.w), make_float2(dy.z, dy.w)), zzw, acc2);
+#else
                     float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
                     for (int k = 0; k < 8; ++k) {
@@ -333,8 +350,9 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                     acc = fmaf(dx.y * dy.y, z.y, acc);
                     acc = fmaf(dx.z * dy.z, z.z, acc);
                     acc = fmaf(dx.w * dy.w, z.w, acc);
+#endif
                 }
-                part[j] = acc;
+                part[j] = PNDF_F2 ? acc2.x + acc2.y : acc;
                 if (TMA) __syncwarp();  // every lane is done with this slot before it is refilled
             }
             group_reduce<G, SB>(part, gl);
