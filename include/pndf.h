@@ -266,6 +266,45 @@ pndf_status pndf_bin_permutation(pndf_store s, const pndf_query* d_queries, int6
  * G*4 dividing Rp; 0 restores the default chosen at load. */
 pndf_status pndf_set_lanes(pndf_store s, int32_t lanes);
 
+/* ---- GPU factor builder ----------------------------------------------
+ * The tensor the paper compresses (footprint NDF images stacked along the third dimension) and its
+ * CP decomposition by alternating least squares (Eq. 5: "maximum error 1e-4, maximum
+ * iteration count 500"), for ONE global group (readings 14, 23).  Limits: A a power of two,
+ * 4 <= A <= 128, 1 <= R <= 128, P * A < 2^32.  All pointers are DEVICE memory; calls enqueue on cuda_stream
+ * and pndf_cp_als synchronises once per sweep (to test the stopping rule).
+ *
+ * pndf_hist_tensor: D[z][x][y] = tf32(count / total) -- the footprint-weighted histogram of the map's
+ *   angular bins over footprint z (Eq. 2 with sigma_r -> 0; Gaussian G_p, sigma = 1.5 s_l / sqrt(12),
+ *   truncated at 4 sigma, 16-bit integer weights, exact integer counts: DESIGN.md reading 11), rounded to
+ *   nearest-even at 11 significant bits (reading 23).  Rows z = off_l + j n_l + i (periodic map, PNDF_WRAP
+ *   required).  d_bins [N][N] uint16: bin x + A*y of texel (u, v) at d_bins[v*N + u].  d_D [P][A][A] and
+ *   d_Dt [P][A][A] (= D with x, y swapped; may be NULL) are caller-allocated fp32.
+ * pndf_cp_als: nonnegative CP-ALS (HALS column updates, modes Z, X, Y, per-rank norm balance after each
+ *   sweep) of D from the caller's initial factors (in/out, fp32, >= 0): d_Z [P][R], d_X [A][R], d_Y [A][R].
+ *   Stops after the first sweep whose relative fit-error change is < tol, or after max_sweeps.  With
+ *   PNDF_ALS_NORMALISE the result is normalised (unit-sum X_r, Y_r, max_z Z_r = 1, C_r the weight, every
+ *   row's reconstructed mass 1; reading 16) and d_C [R] is written (else d_C, if not NULL, is set to 1).
+ *   h_err [max_sweeps] (host, may be NULL) receives the fit error ||D - D_hat|| / ||D|| after each sweep;
+ *   *sweeps_out the number of sweeps run.  The MTTKRP of each mode runs on the tensor cores (tcgen05,
+ *   kind::tf32, D exact in tf32, the factor operand split into tf32 hi + lo parts).
+ * pndf_mttkrp (test support): one MTTKRP, mode 0 = Z ([P][R] = D_(z) (X kr Y)), 1 = X ([A][R]),
+ *   2 = Y ([A][R]), into d_M (fp64). */
+#define PNDF_ALS_NORMALISE 1u
+typedef struct {
+    uint32_t abi_version; /* = PNDF_ABI_VERSION                                  */
+    int32_t max_sweeps;   /* >= 1 (500)                                   */
+    double tol;           /* relative change of the fit error (1e-4)      */
+    uint32_t flags;       /* PNDF_ALS_NORMALISE                                  */
+} pndf_als_opts;
+
+pndf_status pndf_hist_tensor(const pndf_desc* desc, const uint16_t* d_bins, float* d_D, float* d_Dt,
+                             void* cuda_stream);
+pndf_status pndf_cp_als(const pndf_desc* desc, const float* d_D, const float* d_Dt, float* d_C, float* d_X,
+                        float* d_Y, float* d_Z, const pndf_als_opts* opts, double* h_err, int32_t* sweeps_out,
+                        void* cuda_stream);
+pndf_status pndf_mttkrp(const pndf_desc* desc, const float* d_D, const float* d_Dt, const float* d_Z,
+                        const float* d_X, const float* d_Y, int32_t mode, double* d_M, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,27 +51,34 @@ def footprint_weights(s: int, N: int):
 def hist_tensor(N: int, s0: int, L: int, A: int, bins: np.ndarray) -> np.ndarray:
     """D[z, x, y] (fp64) for a periodic map; bins[v, u] = x + A*y (uint16) is the angular bin of texel (u, v)."""
     P = sum((N // (s0 << l)) ** 2 for l in range(L))
-    D = np.zeros((P, A, A))
+    return hist_rows(N, s0, L, A, bins, np.arange(P))
+
+
+def hist_rows(N: int, s0: int, L: int, A: int, bins: np.ndarray, rows) -> np.ndarray:
+    """The rows z of hist_tensor (for sampled checks at full size): D[k] = histogram of footprint rows[k]."""
+    rows = np.asarray(rows, np.int64)
     bx = (bins.astype(np.int64) % A)
     by = (bins.astype(np.int64) // A)
     flat = (bx * A + by)  # [v, u] -> x*A + y
-    z = 0
-    for l in range(L):
+    off = np.cumsum([0] + [(N // (s0 << l)) ** 2 for l in range(L)])
+    out = np.zeros((rows.shape[0], A, A))
+    tabs = [footprint_weights(s0 << l, N) for l in range(L)]
+    for k, z in enumerate(rows):
+        l = int(np.searchsorted(off, z, side="right") - 1)
         s = s0 << l
         n = N // s
-        qmin, w = footprint_weights(s, N)
+        c = int(z - off[l])
+        i, j = c % n, c // n
+        qmin, w = tabs[l]
         Wf = w.shape[0]
         tot = float(w.sum()) ** 2
-        for j in range(n):
-            vs = (j * s + qmin + np.arange(Wf)) % N
-            for i in range(n):
-                us = (i * s + qmin + np.arange(Wf)) % N
-                win = flat[np.ix_(vs, us)]                       # [q (v), p (u)]
-                ww = np.outer(w, w).astype(np.float64)           # w_y[q] * w_x[p], exact integers
-                cnt = np.bincount(win.ravel(), weights=ww.ravel(), minlength=A * A)
-                D[z] = (cnt / tot).reshape(A, A)
-                z += 1
-    return D
+        vs = (j * s + qmin + np.arange(Wf)) % N
+        us = (i * s + qmin + np.arange(Wf)) % N
+        win = flat[np.ix_(vs, us)]                       # [q (v), p (u)]
+        ww = np.outer(w, w).astype(np.float64)           # w_y[q] * w_x[p], exact integers
+        cnt = np.bincount(win.ravel(), weights=ww.ravel(), minlength=A * A)
+        out[k] = (cnt / tot).reshape(A, A)
+    return out
 
 
 def tf32_round(x: np.ndarray) -> np.ndarray:

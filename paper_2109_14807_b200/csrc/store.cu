@@ -256,6 +256,10 @@ void destroy(pndf_store_s* s) {
 }  // namespace
 
 // ----------------------------------------------------------------- API --
+namespace pndf {
+void set_last_error(const char* msg) { snprintf(g_cuda_err, sizeof(g_cuda_err), "%s", msg); }
+}  // namespace pndf
+
 extern "C" {
 
 uint32_t pndf_abi_version(void) { return PNDF_ABI_VERSION; }

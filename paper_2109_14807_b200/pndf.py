@@ -71,7 +71,15 @@ EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_s
            "pndf_free",
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
-           "pndf_sg_queries", "pndf_load_tiles", "pndf_load_blocked")
+           "pndf_sg_queries", "pndf_load_tiles", "pndf_load_blocked", "pndf_hist_tensor", "pndf_cp_als",
+           "pndf_mttkrp")
+
+ALS_NORMALISE = 1
+
+
+class AlsOpts(ctypes.Structure):
+    _fields_ = [("abi_version", ctypes.c_uint32), ("max_sweeps", ctypes.c_int32), ("tol", ctypes.c_double),
+                ("flags", ctypes.c_uint32)]
 
 SG_DTYPE = np.dtype([("u", "<f4"), ("v", "<f4"), ("size", "<f4"), ("hx", "<f4"), ("hy", "<f4"),
                      ("lam", "<f4"), ("amp", "<f4"), ("pad", "<f4")])
@@ -121,6 +129,13 @@ def lib():
         L.pndf_sg_queries.argtypes = [P, i64, ctypes.c_float, i32, P, P]
         L.pndf_set_lanes.restype = i32
         L.pndf_set_lanes.argtypes = [P, i32]
+        L.pndf_hist_tensor.restype = i32
+        L.pndf_hist_tensor.argtypes = [ctypes.POINTER(Desc), P, P, P, P]
+        L.pndf_cp_als.restype = i32
+        L.pndf_cp_als.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, P, ctypes.POINTER(AlsOpts), P,
+                                  ctypes.POINTER(i32), P]
+        L.pndf_mttkrp.restype = i32
+        L.pndf_mttkrp.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, i32, P, P]
         _lib = L
     return _lib
 
@@ -299,3 +314,27 @@ def load_blocked(N: int, s0: int, L: int, A: int, wrap: bool, bs, device: int = 
                                    _ptr(arr["G"]), _ptr(arr["S"]), _ptr(arr["Z"]), device, _stream(stream),
                                    ctypes.byref(h)), "pndf_load_blocked")
     return Store(h, make_desc(N, s0, L, A, bs.R, wrap))
+
+
+# ---- GPU factor builder ---------------------------------------------------------
+def hist_tensor(desc: Desc, d_bins, d_D, d_Dt=None, stream=None):
+    """pndf_hist_tensor: D[z][x][y] (and Dt[z][y][x]) = tf32-rounded footprint histograms, device buffers."""
+    _check(lib().pndf_hist_tensor(ctypes.byref(desc), _ptr(d_bins), _ptr(d_D), _ptr(d_Dt), _stream(stream)),
+           "pndf_hist_tensor")
+
+
+def mttkrp(desc: Desc, d_D, d_Dt, d_Z, d_X, d_Y, mode: int, d_M, stream=None):
+    """pndf_mttkrp (test support): mode 0 = Z, 1 = X, 2 = Y, into d_M (fp64, device)."""
+    _check(lib().pndf_mttkrp(ctypes.byref(desc), _ptr(d_D), _ptr(d_Dt), _ptr(d_Z), _ptr(d_X), _ptr(d_Y), mode,
+                             _ptr(d_M), _stream(stream)), "pndf_mttkrp")
+
+
+def cp_als(desc: Desc, d_D, d_Dt, d_Z, d_X, d_Y, d_C=None, max_sweeps: int = 500, tol: float = 1e-4,
+           normalise: bool = False, stream=None):
+    """pndf_cp_als: factors updated in place (device fp32); returns the fit-error history (numpy)."""
+    o = AlsOpts(abi_version=ABI_VERSION, max_sweeps=max_sweeps, tol=tol, flags=ALS_NORMALISE if normalise else 0)
+    err = np.zeros(max_sweeps, np.float64)
+    n = ctypes.c_int32(0)
+    _check(lib().pndf_cp_als(ctypes.byref(desc), _ptr(d_D), _ptr(d_Dt), _ptr(d_C), _ptr(d_X), _ptr(d_Y),
+                             _ptr(d_Z), ctypes.byref(o), _ptr(err), ctypes.byref(n), _stream(stream)), "pndf_cp_als")
+    return err[:n.value].copy()

@@ -36,11 +36,11 @@ def ncu_csv(rep, page):
     return list(csv.reader(io.StringIO(out)))
 
 
-def summarize(rep, nq, title):
+def summarize(rep, nq, title, idx=0, unit="query"):
     rows = ncu_csv(rep, "raw")
-    hdr, units, v = rows[0], rows[1], rows[2]
+    hdr, units, v = rows[0], rows[1], rows[2 + idx]
     lines = [f"# {title}", f"# source: {os.path.basename(rep)} (ncu --set full --clock-control none)",
-             f"# queries in the captured launch: {nq:.0f}", ""]
+             f"# {unit}s in the captured launch: {nq:.0f}", ""]
     vals = {}
     for m in METRICS:
         if m in hdr:
@@ -54,15 +54,25 @@ def summarize(rep, nq, title):
         return float(x.replace(",", "")) * SCALE.get(u, 1)
 
     dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
-    lines.append(f"dram bytes per query (read+write): {dram / nq:.1f}")
-    lines.append(f"L2->L1 read bytes per query: {float(vals['lts__t_sectors_srcunit_tex_op_read.sum'][0].replace(',', '')) * 32 / nq:.1f}")
-    lines.append(f"warp instructions per query: {float(vals['smsp__inst_executed.sum'][0].replace(',', '')) / nq:.1f}")
+    lines.append(f"dram bytes per {unit} (read+write): {dram / nq:.2f}")
+    lines.append(f"L2->L1 read bytes per {unit}: {float(vals['lts__t_sectors_srcunit_tex_op_read.sum'][0].replace(',', '')) * 32 / nq:.2f}")
+    lines.append(f"warp instructions per {unit}: {float(vals['smsp__inst_executed.sum'][0].replace(',', '')) / nq:.3f}")
     src = ncu_csv(rep, "source")
     if len(src) > 2:
         h = src[1]
         data = src[2:]
+        if idx:  # the source page lists the first kernel only
+            data = []
         iS, iW, iE = h.index("Source"), h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
-        tot = sum(int(r[iW]) for r in data) or 1
+        def _i(x):
+            try:
+                return int(x)
+            except ValueError:
+                return 0
+        data = [r for r in data if len(r) > max(iS, iW, iE)]
+        for r in data:
+            r[iW], r[iE] = _i(r[iW]), _i(r[iE])
+        tot = sum(r[iW] for r in data) or 1
         c, s = defaultdict(int), defaultdict(int)
         for r in data:
             t = r[iS].split()
@@ -71,7 +81,7 @@ def summarize(rep, nq, title):
             op = (t[1] if t[0].startswith("@") else t[0]).split(".")[0]
             c[op] += int(r[iE])
             s[op] += int(r[iW])
-        lines += ["", "opcode mix (per query) and share of warp-stall samples:"]
+        lines += ["", f"opcode mix (per {unit}) and share of warp-stall samples:"]
         for op, k in sorted(c.items(), key=lambda x: -x[1])[:16]:
             lines.append(f"  {op:10s} {k / nq:8.2f}/q   stall {s[op] / tot * 100:5.1f}%")
     return "\n".join(lines) + "\n", dram / nq
@@ -126,12 +136,26 @@ def main():
     if os.path.exists(la):
         open(os.path.join(OUT, f"{rnd}_launches_default.txt"), "w").write(launches(la))
     for name in ("bench_default", "bench_c1", "bench_c2", "bench_c3", "bench_c4", "bench_sample", "bench_sg",
-                 "bench_wang"):
+                 "bench_wang", "bench_blocked", "bench_als"):
         b = os.path.join(GP, name + ".log")
         if os.path.exists(b):
             lines = [l for l in open(b).read().splitlines() if l.startswith("{")]
             if lines:
                 json.dump(json.loads(lines[-1]), open(os.path.join(OUT, f"{rnd}_{name}.json"), "w"), indent=1)
+    al = os.path.join(GP, "prof_als.ncu-rep")
+    if os.path.exists(al):
+        import synth
+        cfg = synth.CONFIGS[2]
+        n_el = cfg.P * cfg.A * cfg.A
+        txt0, _ = summarize(al, n_el, "pndf::als::mttkrp_gemm_kernel<32, 0> (mode Z: [P x A^2] . [A^2 x 32], "
+                                      "tcgen05 kind::tf32), config 2", 0, "D element")
+        txt1, _ = summarize(al, n_el, "pndf::als::mttkrp_gemm_kernel<32, 1> (mode X: [(P A) x A] . [A x 32], "
+                                      "z-reducing epilogue), config 2", 1, "D element")
+        open(os.path.join(OUT, f"{rnd}_als_gemm_ncu.txt"), "w").write(txt0 + "\n" + txt1)
+    la2 = os.path.join(GP, "launches_als.csv")
+    if os.path.exists(la2):
+        open(os.path.join(OUT, f"{rnd}_launches_als.txt"), "w").write(launches(la2).replace(
+            "`python bench.py` (default run)", "`python bench.py --op als --config 2 --steps 2 --warmup 3`"))
     if traffic:
         json.dump(traffic, open(os.path.join(OUT, "ncu_traffic.json"), "w"), indent=1)
 
