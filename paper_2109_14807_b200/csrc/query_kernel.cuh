@@ -17,12 +17,12 @@ namespace pndf {
 struct __align__(16) QDesc {
     int32_t row[8];  // Zc rows of the 8 neighbours (level l0: (i0,j0),(i1,j0),(i0,j1),(i1,j1); then l0+1)
     float w[8];      // trilinear weights (1-t)(1-a)(1-b), ...
-    uint32_t px;     // prefix entries x1 | (x2+1) << 16
-    uint32_t py;     // prefix entries y1 | (y2+1) << 16
+    int32_t sat[4];  // SAT rows (entries of PXY) x1, x2+1, A+1+y1, A+1+y2+1 (the 4 look-ups)
     float div;       // rectangle area (MEAN), 1 (SUM), NaN (invalid record)
     int32_t out;     // output index within the (sub-)batch, -1 = no query
+    int32_t pad[2];
 };
-static_assert(sizeof(QDesc) == 80, "QDesc layout");
+static_assert(sizeof(QDesc) == 96, "QDesc layout");
 
 // returns the reuse key (0xffffffff = never equal to a neighbour's)
 template <bool WRAP>
@@ -35,8 +35,8 @@ __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& r
             d.row[k] = 0;
             d.w[k] = 0.f;
         }
-        d.px = 0;
-        d.py = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) d.sat[k] = 0;
         d.div = __int_as_float(0x7fc00000);
         d.out = out_index;
         return 0xffffffffu;
@@ -72,8 +72,10 @@ __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& r
         d.w[4 * dl + 2] = wa * b;
         d.w[4 * dl + 3] = wb * b;
     }
-    d.px = (uint32_t)x1 | ((uint32_t)(x2 + 1) << 16);
-    d.py = (uint32_t)y1 | ((uint32_t)(y2 + 1) << 16);
+    d.sat[0] = x1;  // PY follows PX: its entries are rows A+1 ...
+    d.sat[1] = x2 + 1;
+    d.sat[2] = p.A + 1 + y1;
+    d.sat[3] = p.A + 2 + y2;
     d.div = p.mean ? (float)((x2 - x1 + 1) * (y2 - y1 + 1)) : 1.f;
     d.out = out_index;
     if (WRAP) return cell_key(p, rec, l0, 1) & 0x7fffffffu;
@@ -180,8 +182,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
     const float* __restrict__ Zc = p.Zc;
     // SAT rows: HILO = [hi row | lo row] per entry (stride 2*RP floats), U32 = one uint32 row
     constexpr int PSTRIDE = LY::PSTRIDE;
-    const float* __restrict__ PX = p.PXY;
-    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * PSTRIDE;
+    const float* __restrict__ PXl = p.PXY + gl * 4;  // this lane's first rank chunk of SAT row 0
     uint64_t* wbar = sbar + warp * kSlots;
     uint32_t* wslot = sslot + (size_t)warp * kSlots * 4 * PSTRIDE;
     uint32_t phase = 0;  // bit k: parity of slot k's next completion
@@ -199,10 +200,9 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
             uint32_t* dst = wslot + (size_t)k * 4 * PSTRIDE;
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // slot was last read by the generic proxy
             mbar_arrive_expect_tx(wbar + k, 4 * LY::ROW_BYTES);
-            tma_load_1d(dst + 0 * PSTRIDE, PX + (size_t)(d.px & 0xffffu) * PSTRIDE, LY::ROW_BYTES, wbar + k);
-            tma_load_1d(dst + 1 * PSTRIDE, PX + (size_t)(d.px >> 16) * PSTRIDE, LY::ROW_BYTES, wbar + k);
-            tma_load_1d(dst + 2 * PSTRIDE, PY + (size_t)(d.py & 0xffffu) * PSTRIDE, LY::ROW_BYTES, wbar + k);
-            tma_load_1d(dst + 3 * PSTRIDE, PY + (size_t)(d.py >> 16) * PSTRIDE, LY::ROW_BYTES, wbar + k);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                tma_load_1d(dst + e * PSTRIDE, p.PXY + (size_t)d.sat[e] * PSTRIDE, LY::ROW_BYTES, wbar + k);
         }
     };
 
@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                     wd[lane].row[k] = 0;
                     wd[lane].w[k] = 0.f;
                 }
-                wd[lane].px = 0;
-                wd[lane].py = 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) wd[lane].sat[k] = 0;
                 wd[lane].div = 1.f;
             }
             const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
@@ -255,12 +255,12 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 }
                 const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
                 const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
-                const uint2 tail = *reinterpret_cast<const uint2*>(&d.px);
+                const int4 so = *reinterpret_cast<const int4*>(&d.sat[0]);
                 const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
-                const float* px0 = PX + (size_t)(tail.x & 0xffffu) * PSTRIDE;
-                const float* px1 = PX + (size_t)(tail.x >> 16) * PSTRIDE;
-                const float* py0 = PY + (size_t)(tail.y & 0xffffu) * PSTRIDE;
-                const float* py1 = PY + (size_t)(tail.y >> 16) * PSTRIDE;
+                const float* px0 = PXl + (int64_t)so.x * PSTRIDE;  // one IMAD.WIDE each
+                const float* px1 = PXl + (int64_t)so.y * PSTRIDE;
+                const float* py0 = PXl + (int64_t)so.z * PSTRIDE;
+                const float* py1 = PXl + (int64_t)so.w * PSTRIDE;
                 // warp-uniform for G == 32 (every lane reads the same descriptor)
                 const bool reuse = (G == 32) && s > 0 && ((reuse_mask >> s) & 1u);
                 if (!reuse) {
@@ -305,10 +305,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                                          (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
                     } else if (U32) {
                         // exact integer differences of the fixed-point SATs (scale folded into Zc)
-                        const uint4 qx1 = ldg_sat(px1 + c);
-                        const uint4 qx0 = ldg_sat(px0 + c);
-                        const uint4 qy1 = ldg_sat(py1 + c);
-                        const uint4 qy0 = ldg_sat(py0 + c);
+                        const uint4 qx1 = ldg_sat(px1 + v * G * 4);
+                        const uint4 qx0 = ldg_sat(px0 + v * G * 4);
+                        const uint4 qy1 = ldg_sat(py1 + v * G * 4);
+                        const uint4 qy0 = ldg_sat(py0 + v * G * 4);
                         dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
                                          __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
                         dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
@@ -316,10 +316,11 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                     } else {
                         // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
                         // under cancellation (Sterbenz), lo carries the fp64 residual.
-                        const float4 xh1 = ldg4(px1 + c), xh0 = ldg4(px0 + c);
-                        const float4 xl1 = ldg4(px1 + RP + c), xl0 = ldg4(px0 + RP + c);
-                        const float4 yh1 = ldg4(py1 + c), yh0 = ldg4(py0 + c);
-                        const float4 yl1 = ldg4(py1 + RP + c), yl0 = ldg4(py0 + RP + c);
+                        const int cv = v * G * 4;
+                        const float4 xh1 = ldg4(px1 + cv), xh0 = ldg4(px0 + cv);
+                        const float4 xl1 = ldg4(px1 + RP + cv), xl0 = ldg4(px0 + RP + cv);
+                        const float4 yh1 = ldg4(py1 + cv), yh0 = ldg4(py0 + cv);
+                        const float4 yl1 = ldg4(py1 + RP + cv), yl0 = ldg4(py0 + RP + cv);
                         dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
                                          (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
                         dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
