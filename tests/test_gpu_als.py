@@ -68,11 +68,13 @@ def test_hist_tensor_full_config2_sampled_rows():
     assert got.tobytes() == ref.tobytes()
 
 
-@pytest.mark.parametrize("R", [8, 32, 100])
+@pytest.mark.parametrize("N,A,R", [(64, 32, 8), (64, 32, 32), (64, 32, 100), (64, 32, 128), (32, 128, 16)])
 @pytest.mark.parametrize("mode", [0, 1, 2])
-def test_mttkrp_parity(R, mode):
+def test_mttkrp_parity(N, A, R, mode):
+    """Every operand width (Rp = 16..128, TMEM double buffers up to 256 columns), ragged last tiles
+    (P = 5461 / 1365 rows), A = 32 .. 128 (K = A^2 up to 16384 for mode Z)."""
     pndf = _pndf()
-    cfg, bins = _inputs(64, 32, R, 1)
+    cfg, bins = _inputs(N, A, R, 1)
     D, Dt = _gpu_hist(cfg, bins)
     Z, X, Y = _init(cfg.P, cfg.A, R, seed=R + mode)
     out_rows = cfg.P if mode == 0 else cfg.A
@@ -109,7 +111,7 @@ def _cmp_factors(got, ref, what):
     assert rel <= 1e-4, f"{what}: max |g - o| / column max = {rel:.3e}"
 
 
-@pytest.mark.parametrize("N,A,R,kind", [(64, 32, 8, 1), (64, 64, 16, 2)])
+@pytest.mark.parametrize("N,A,R,kind", [(64, 32, 8, 1), (64, 64, 16, 2), (32, 32, 96, 1)])
 def test_cp_als_sweeps_match_oracle(N, A, R, kind):
     """Three sweeps from a warm start (30 oracle sweeps from a seeded init) agree with the oracle's three.
     From a cold random init the first sweeps are chaotic: rounding M_Z to fp32 alone moves the oracle's own
