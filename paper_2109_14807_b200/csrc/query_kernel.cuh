@@ -140,6 +140,9 @@ constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced 
 #ifndef PNDF_F2
 #define PNDF_F2 1  // 1: packed fp32 FFMA2/FMUL2 for the interpolation and rank product (sm_100)
 #endif
+#ifndef PNDF_PF
+#define PNDF_PF 0  // 1: prefetch the next step's SAT rows into L1; 2: and its Zc rows (experiment)
+#endif
 #ifndef PNDF_TMA
 #define PNDF_TMA 0  // 1: stage SAT rows of the next query in smem with TMA bulk copies (measured slower on B200)
 #endif
@@ -261,6 +264,30 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 const float* px1 = PXl + (int64_t)so.y * PSTRIDE;
                 const float* py0 = PXl + (int64_t)so.z * PSTRIDE;
                 const float* py1 = PXl + (int64_t)so.w * PSTRIDE;
+#if PNDF_PF
+                // software prefetch (into L1) of the next step's SAT rows (and Zc rows with PNDF_PF=2), so
+                // their L2 latency overlaps this step's arithmetic; costs no registers or shared memory
+                if (!TMA && s + 1 < NSTEP) {
+                    const QDesc& dn = wd[(s + 1) * QPW + grp];
+                    const int4 sn = *reinterpret_cast<const int4*>(&dn.sat[0]);
+                    const int sr[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const float* pp = PXl + (int64_t)sr[e] * PSTRIDE;
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            prefetch_l1(pp + v * G * 4);
+                            if (!U32) prefetch_l1(pp + RP + v * G * 4);
+                        }
+                    }
+                    if (PNDF_PF >= 2 && !((G == 32) && ((reuse_mask >> (s + 1)) & 1u))) {
+#pragma unroll
+                        for (int k = 0; k < 8; ++k)
+#pragma unroll
+                            for (int v = 0; v < NV; ++v) prefetch_l1(Zc + (size_t)dn.row[k] * RP + (gl + v * G) * 4);
+                    }
+                }
+#endif
                 // warp-uniform for G == 32 (every lane reads the same descriptor)
                 const bool reuse = (G == 32) && s > 0 && ((reuse_mask >> s) & 1u);
                 if (!reuse) {

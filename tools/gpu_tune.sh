@@ -1,7 +1,10 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_sampler.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
 for rep in 1 2; do
-timeout 600 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/ab_new_$rep.log 2>&1
-echo "new $rep $(grep -o '"value": [0-9.e+]*' gpurun_out/ab_new_$rep.log | head -1) $(grep -o '"kernel_ms": [0-9.e+]*' gpurun_out/ab_new_$rep.log | head -1)" >> gpurun_out/ab.txt
+  for v in libpndf libpndf_f20; do
+    PNDF_LIB=paper_2109_14807_b200/$v.so timeout 600 python bench.py --config 4 --no-e2e --no-cpu-baseline > gpurun_out/ab4_${v}_$rep.log 2>&1
+    echo "c4 $v $rep $(grep -o '"value": [0-9.e+]*' gpurun_out/ab4_${v}_$rep.log | head -1) $(grep -o '"kernel_ms": [0-9.e+]*' gpurun_out/ab4_${v}_$rep.log | head -1)" >> gpurun_out/ab.txt
+    PNDF_LIB=paper_2109_14807_b200/$v.so timeout 600 python bench.py --config 3 --no-e2e --no-cpu-baseline > gpurun_out/ab3_${v}_$rep.log 2>&1
+    echo "c3 $v $rep $(grep -o '"value": [0-9.e+]*' gpurun_out/ab3_${v}_$rep.log | head -1) $(grep -o '"kernel_ms": [0-9.e+]*' gpurun_out/ab3_${v}_$rep.log | head -1)" >> gpurun_out/ab.txt
+  done
 done
