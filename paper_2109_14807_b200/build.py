@@ -16,7 +16,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 LIB = os.path.join(PKG, "libpndf.so")
 SOURCES = sorted(glob.glob(os.path.join(PKG, "csrc", "*.cu")))
-DEPS = SOURCES + sorted(glob.glob(os.path.join(PKG, "csrc", "*.h*"))) + [os.path.join(ROOT, "include", "pndf.h")]
+DEPS = (SOURCES + sorted(glob.glob(os.path.join(PKG, "csrc", "*.h"))) + sorted(glob.glob(os.path.join(PKG, "csrc", "*.cuh")))
+        + [os.path.join(ROOT, "include", "pndf.h")])
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC,-O2", "-Xptxas", "-v"]
 

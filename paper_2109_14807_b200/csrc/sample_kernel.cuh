@@ -44,6 +44,36 @@ __device__ __forceinline__ float group_sum(float v) {
     return v;
 }
 
+// Sum q0..q3 over the G lanes of each group with recursive halving (log2 G + 1 shuffles instead of
+// 4 log2 G), then gather the four totals into every lane of the group (3 more shuffles).
+template <int G>
+__device__ __forceinline__ void quad_reduce(float& q0, float& q1, float& q2, float& q3, int gl, int lane) {
+    if (G >= 4) {
+        constexpr int H = G / 2, Q = G / 4;
+        const bool up = (gl & H) != 0;  // upper half keeps (q2, q3)
+        float k0 = up ? q2 : q0, k1 = up ? q3 : q1;
+        const float s0 = up ? q0 : q2, s1 = up ? q1 : q3;
+        k0 += __shfl_xor_sync(0xffffffffu, s0, H);
+        k1 += __shfl_xor_sync(0xffffffffu, s1, H);
+        const bool up2 = (gl & Q) != 0;  // then keeps k1
+        float k = up2 ? k1 : k0;
+        k += __shfl_xor_sync(0xffffffffu, up2 ? k0 : k1, Q);
+#pragma unroll
+        for (int o = Q / 2; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o);
+        // lane gl now holds quad 2*[gl & H] + [gl & Q]
+        const int g0 = lane - gl;
+        q0 = __shfl_sync(0xffffffffu, k, g0);
+        q1 = __shfl_sync(0xffffffffu, k, g0 + Q);
+        q2 = __shfl_sync(0xffffffffu, k, g0 + H);
+        q3 = __shfl_sync(0xffffffffu, k, g0 + H + Q);
+    } else {
+        q0 = group_sum<G>(q0);
+        q1 = group_sum<G>(q1);
+        q2 = group_sum<G>(q2);
+        q3 = group_sum<G>(q3);
+    }
+}
+
 template <int G, int NV, bool WRAP, bool BINNED, bool U32>
 __global__ void __launch_bounds__(256) sample_kernel(const QParams p, const pndf_query* __restrict__ q,
                                                      const float* __restrict__ xi, const uint32_t* __restrict__ idx,
@@ -132,7 +162,6 @@ __global__ void __launch_bounds__(256) sample_kernel(const QParams p, const pndf
             const bool go = live && (xb - xa > 1 || yb - ya > 1);
             const int xm = go && xb - xa > 1 ? xa + (xb - xa + 1) / 2 : xb;
             const int ym = go && yb - ya > 1 ? ya + (yb - ya + 1) / 2 : yb;
-            float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
             SatV<U32> sxm[NV], sym[NV];
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
@@ -140,25 +169,31 @@ __global__ void __launch_bounds__(256) sample_kernel(const QParams p, const pndf
                 sxm[v].load(PX + (size_t)xm * PSTRIDE, c, RP);
                 sym[v].load(PY + (size_t)ym * PSTRIDE, c, RP);
             }
+            // quad sums: (x-lo|x-hi) x (y-lo|y-hi), two ranks per packed FFMA2; the y factor and Z-hat
+            // are multiplied first (u = ey z, w = fy z) so each quad costs one FMA per rank
+            float2 a0 = make_float2(0.f, 0.f), a1 = a0, a2 = a0, a3 = a0;
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const float4 dxl = SatV<U32>::diff(sxa[v], sxm[v]), dxr = SatV<U32>::diff(sxm[v], sxb[v]);
                 const float4 dyb = SatV<U32>::diff(sya[v], sym[v]), dyt = SatV<U32>::diff(sym[v], syb[v]);
-                const float ex[4] = {dxl.x, dxl.y, dxl.z, dxl.w}, fx[4] = {dxr.x, dxr.y, dxr.z, dxr.w};
-                const float ey[4] = {dyb.x, dyb.y, dyb.z, dyb.w}, fy[4] = {dyt.x, dyt.y, dyt.z, dyt.w};
-                const float z[4] = {zh[v].x, zh[v].y, zh[v].z, zh[v].w};
-#pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    q0 = fmaf(ex[k] * ey[k], z[k], q0);
-                    q1 = fmaf(fx[k] * ey[k], z[k], q1);
-                    q2 = fmaf(ex[k] * fy[k], z[k], q2);
-                    q3 = fmaf(fx[k] * fy[k], z[k], q3);
-                }
+                const float2 z01 = make_float2(zh[v].x, zh[v].y), z23 = make_float2(zh[v].z, zh[v].w);
+                const float2 u01 = __fmul2_rn(make_float2(dyb.x, dyb.y), z01);
+                const float2 u23 = __fmul2_rn(make_float2(dyb.z, dyb.w), z23);
+                const float2 w01 = __fmul2_rn(make_float2(dyt.x, dyt.y), z01);
+                const float2 w23 = __fmul2_rn(make_float2(dyt.z, dyt.w), z23);
+                const float2 e01 = make_float2(dxl.x, dxl.y), e23 = make_float2(dxl.z, dxl.w);
+                const float2 f01 = make_float2(dxr.x, dxr.y), f23 = make_float2(dxr.z, dxr.w);
+                a0 = __ffma2_rn(e01, u01, a0);
+                a0 = __ffma2_rn(e23, u23, a0);
+                a1 = __ffma2_rn(f01, u01, a1);
+                a1 = __ffma2_rn(f23, u23, a1);
+                a2 = __ffma2_rn(e01, w01, a2);
+                a2 = __ffma2_rn(e23, w23, a2);
+                a3 = __ffma2_rn(f01, w01, a3);
+                a3 = __ffma2_rn(f23, w23, a3);
             }
-            q0 = group_sum<G>(q0);
-            q1 = group_sum<G>(q1);
-            q2 = group_sum<G>(q2);
-            q3 = group_sum<G>(q3);
+            float q0 = a0.x + a0.y, q1 = a1.x + a1.y, q2 = a2.x + a2.y, q3 = a3.x + a3.y;
+            quad_reduce<G>(q0, q1, q2, q3, gl, lane);
             if (go) {
                 const float qs[4] = {q0, q1, q2, q3};
                 const float tot = ((q0 + q1) + q2) + q3;
