@@ -792,7 +792,11 @@ def run_als_op(args, cfg, rank, world, local_rank):
                          "bytes_per_sweep": 3 * dbytes, "peak_source": src,
                          "note": "achieved = the 3 tensor reads a sweep must make (modes Z, X on D, mode Y on Dt) "
                                  "over the whole sweep time (includes the HALS, Gram and host-sync steps)"},
-            "cpu_baseline": cpu, "gpu_launches": None, "clocks": clk,
+            "cpu_baseline": cpu,
+            # one pndf_cp_als call of K sweeps = 12 setup/teardown launches + 21 per sweep (3 tcgen05 GEMMs,
+            # 3 HALS + 3 Gram sums, 2 operand splits + 1 Khatri-Rao, 2 partial reductions, error, balance,
+            # 3 column scalings, 2 Gram scalings): profiles/r01_launches_als.txt
+            "gpu_launches": 12 + 21 * args.steps, "clocks": clk,
             "e2e": {"value": len(hist_e2e) / e2e_s, "unit": "sweeps/s", "h2d_bytes_per_step": int(bins.nbytes),
                     "d2h_bytes_per_step": int(sum(t.numel() * 4 for t in out)),
                     "builder_seconds": e2e_s, "sweeps": int(len(hist_e2e)), "fit_error": float(hist_e2e[-1]),

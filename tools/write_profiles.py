@@ -132,6 +132,14 @@ def main():
     if os.path.exists(sp):
         txt, _ = summarize(sp, 1e8, "pndf::sample_kernel, config 5, 1e8 samples (bench --op sample)")
         open(os.path.join(OUT, f"{rnd}_sample_kernel_ncu.txt"), "w").write(txt)
+    for rep_name, n_units, unit, title in (
+            ("prof_blocked", 1e6, "query", "pndf::blocked_query_kernel, config 2 blocked store (t=16, 8-texel regions)"),
+            ("prof_tiled", 1e7, "query", "pndf::tiled_query_kernel, 16 Wang tiles of 512^2, world 102400^2"),
+            ("prof_sg", 2e8, "light", "pndf::sg_rect_kernel, 2e8 SG lights (config 5)")):
+        rp = os.path.join(GP, rep_name + ".ncu-rep")
+        if os.path.exists(rp):
+            txt, _ = summarize(rp, n_units, title, 0, unit)
+            open(os.path.join(OUT, f"{rnd}_{rep_name[5:]}_kernel_ncu.txt"), "w").write(txt)
     la = os.path.join(GP, "launches_default.csv")
     if os.path.exists(la):
         open(os.path.join(OUT, f"{rnd}_launches_default.txt"), "w").write(launches(la))
