@@ -93,7 +93,10 @@ typedef struct {
  * (zero ranks, rows 16-byte aligned); prefix sums of X, Y accumulated in fp64 and
  * stored either as an fp32 (hi, lo) pair [2][(A+1)][2][Rp] (HILO, M_r = C_r) or as
  * uint32 fixed point [2][(A+1)][Rp] with per-rank scale 2^e_r folded into
- * M_r = C_r 2^-(ex_r + ey_r) (U32); see the PNDF_PREFIX_* flags.
+ * M_r = C_r 2^-(ex_r + ey_r) (U32); see the PNDF_PREFIX_* flags.  A range table
+ * DT[2][A][W][Rp] fp32 (W = min(16, A)) holds, for every range of at most W bins, the
+ * prefix difference exactly as the kernel computes it from the SATs, so a narrow range
+ * costs one look-up per axis instead of two with bit-identical results.
  * Every factor must be finite and >= 0 (nonnegative store), else PNDF_EINVAL.
  * Inputs are copied: the caller may free them on return.  device = CUDA
  * ordinal; cuda_stream = cudaStream_t used for the build (NULL = default). */
@@ -181,6 +184,9 @@ typedef struct {
     double bin_ms;            /* summed binning time of those batches           */
     int32_t last_binned;      /* 1 if the last batch was binned                 */
     int32_t prefix_format;    /* 0 = HILO, 1 = U32                              */
+    int64_t range_table_bytes;/* bytes of the narrow-range difference table DT  */
+    int32_t range_table_width;/* W: ranges of <= W bins read one DT row (0 = no table) */
+    int32_t pad;
 } pndf_store_stats;
 pndf_status pndf_store_stats_get(pndf_store s, pndf_store_stats* out);
 pndf_status pndf_store_stats_reset(pndf_store s);

@@ -11,6 +11,8 @@
 // Zc[z][r] = fl32(M_r * Z_r(z)) with M_r = C_r (HILO) or C_r 2^-(ex_r+ey_r) (U32,
 // a power-of-two rescale that is exact unless it underflows -- flagged).
 #include <cuda_runtime.h>
+
+#include <algorithm>
 #include <float.h>
 #include <stdint.h>
 
@@ -95,6 +97,40 @@ __global__ void prefix_u32_kernel(const float* __restrict__ X, const float* __re
         out[(size_t)k * Rp + r] = __double2uint_rn(ldexp(S, e));
         if (k < A && r < R) S += (double)F[(size_t)k * R + r];
     }
+}
+
+// DT[axis][x1][w-1][r] = the prefix difference of [x1, x1+w) computed exactly as query_kernel does
+// (U32: float of the integer difference; HILO: (hi1 - hi0) + (lo1 - lo0) in fp32), so a table look-up
+// returns the same bits as the two SAT look-ups it replaces.  Entries with x1 + w > A are 0.
+__global__ void range_table_kernel(const float* __restrict__ PXY, int A, int Rp, int u32, int W,
+                                   float* __restrict__ DT) {
+    const int64_t n = (int64_t)2 * A * W * Rp;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+        const int r = (int)(e % Rp);
+        const int64_t row = e / Rp;
+        const int w = (int)(row % W) + 1;
+        const int x1 = (int)((row / W) % A);
+        const int axis = (int)(row / ((int64_t)W * A));
+        float v = 0.f;
+        if (x1 + w <= A) {
+            if (u32) {
+                const uint32_t* Q = reinterpret_cast<const uint32_t*>(PXY) + (size_t)axis * (A + 1) * Rp;
+                v = __uint2float_rn(Q[(size_t)(x1 + w) * Rp + r] - Q[(size_t)x1 * Rp + r]);
+            } else {
+                const float* T = PXY + (size_t)axis * (A + 1) * 2 * Rp;
+                const float h1 = T[(size_t)(2 * (x1 + w)) * Rp + r], h0 = T[(size_t)(2 * x1) * Rp + r];
+                const float l1 = T[(size_t)(2 * (x1 + w) + 1) * Rp + r], l0 = T[(size_t)(2 * x1 + 1) * Rp + r];
+                v = __fadd_rn(__fsub_rn(h1, h0), __fsub_rn(l1, l0));
+            }
+        }
+        DT[e] = v;
+    }
+}
+
+cudaError_t launch_range_table(const float* PXY, int A, int Rp, int u32, int W, float* DT, cudaStream_t st) {
+    const int64_t n = (int64_t)2 * A * W * Rp;
+    range_table_kernel<<<(int)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(PXY, A, Rp, u32, W, DT);
+    return cudaGetLastError();
 }
 
 static int grid_for(int64_t total, int threads, int cap_blocks) {

@@ -34,6 +34,9 @@ struct QParams {
     int32_t prefix_u32;            // 1 = uint32 fixed-point SATs (PQ[2][A+1][Rp]), 0 = fp32 (hi, lo)
     float inv_s0;                  // 1/s0 (power of two, exact)
     uint32_t mean;                 // 1 = divide by the rectangle area
+    const float* DT;               // range table [2][A][W][Rp]: DT[axis][x1][w-1] = the SAT difference of
+                                   // [x1, x1+w) exactly as the query kernel computes it (NULL = none)
+    int32_t dt_w;                  // W: widest range served by DT (0 = none)
 };
 
 // Implicit Wang tiling (tiles.cu).

@@ -67,6 +67,7 @@ cudaError_t launch_fold_rows(const float* Zsrc, int64_t rows, int R, const float
                              uint32_t* flags, cudaStream_t st);
 cudaError_t launch_prefix_stats(const float* Xdev, const float* Ydev, int A, int R, int Rp, double* total,
                                 float* minnz, uint32_t* flags, cudaStream_t st);
+cudaError_t launch_range_table(const float* PXY, int A, int Rp, int u32, int W, float* DT, cudaStream_t st);
 cudaError_t launch_prefix(const float* Xdev, const float* Ydev, int A, int R, int Rp, int u32, const int* exps,
                           void* table, cudaStream_t st);
 

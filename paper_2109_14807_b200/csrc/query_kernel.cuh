@@ -20,12 +20,13 @@ struct __align__(16) QDesc {
     int32_t sat[4];  // SAT rows (entries of PXY) x1, x2+1, A+1+y1, A+1+y2+1 (the 4 look-ups)
     float div;       // rectangle area (MEAN), 1 (SUM), NaN (invalid record)
     int32_t out;     // output index within the (sub-)batch, -1 = no query
-    int32_t pad[2];
+    int32_t mode;    // bit 0: x range from the range table DT (sat[0] = its row), bit 1: y likewise (sat[2])
+    int32_t pad;
 };
 static_assert(sizeof(QDesc) == 96, "QDesc layout");
 
 // returns the reuse key (0xffffffff = never equal to a neighbour's)
-template <bool WRAP>
+template <bool WRAP, bool USE_DT>  // USE_DT: narrow ranges read the range table (not with TMA staging)
 __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& rec, int32_t out_index, QDesc& d) {
     int x1, x2, y1, y2;
     if (!record_valid(p, rec, x1, x2, y1, y2)) {
@@ -37,6 +38,7 @@ __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& r
         }
 #pragma unroll
         for (int k = 0; k < 4; ++k) d.sat[k] = 0;
+        d.mode = 0;
         d.div = __int_as_float(0x7fc00000);
         d.out = out_index;
         return 0xffffffffu;
@@ -76,6 +78,15 @@ __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& r
     d.sat[1] = x2 + 1;
     d.sat[2] = p.A + 1 + y1;
     d.sat[3] = p.A + 2 + y2;
+    d.mode = 0;
+    if (USE_DT && x2 - x1 < p.dt_w) {  // narrow range: one table row DT[0][x1][w-1] instead of two SAT rows
+        d.sat[0] = x1 * p.dt_w + (x2 - x1);
+        d.mode |= 1;
+    }
+    if (USE_DT && y2 - y1 < p.dt_w) {
+        d.sat[2] = (p.A + y1) * p.dt_w + (y2 - y1);
+        d.mode |= 2;
+    }
     d.div = p.mean ? (float)((x2 - x1 + 1) * (y2 - y1 + 1)) : 1.f;
     d.out = out_index;
     if (WRAP) return cell_key(p, rec, l0, 1) & 0x7fffffffu;
@@ -186,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
     // SAT rows: HILO = [hi row | lo row] per entry (stride 2*RP floats), U32 = one uint32 row
     constexpr int PSTRIDE = LY::PSTRIDE;
     const float* __restrict__ PXl = p.PXY + gl * 4;  // this lane's first rank chunk of SAT row 0
+    const float* __restrict__ DTl = p.DT + gl * 4;   // ... and of range-table row 0
     uint64_t* wbar = sbar + warp * kSlots;
     uint32_t* wslot = sslot + (size_t)warp * kSlots * 4 * PSTRIDE;
     uint32_t phase = 0;  // bit k: parity of slot k's next completion
@@ -221,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 // binned: idx is the radix-sorted permutation; gather the record through it
                 const int64_t src = BINNED ? (int64_t)__ldg(idx + qi) : qi;
                 const pndf_query rec = ldg_query(q + src);
-                key = decode<WRAP>(p, rec, (int32_t)src, wd[lane]);
+                key = decode<WRAP, !TMA>(p, rec, (int32_t)src, wd[lane]);
             } else {
                 wd[lane].out = -1;
 #pragma unroll
@@ -231,6 +243,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 }
 #pragma unroll
                 for (int k = 0; k < 4; ++k) wd[lane].sat[k] = 0;
+                wd[lane].mode = 0;
                 wd[lane].div = 1.f;
             }
             const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
@@ -259,10 +272,12 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
                 const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
                 const int4 so = *reinterpret_cast<const int4*>(&d.sat[0]);
+                const int dmode = d.mode;  // warp-uniform for G == 32
                 const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
-                const float* px0 = PXl + (int64_t)so.x * PSTRIDE;  // one IMAD.WIDE each
+                const bool tx = dmode & 1, ty = (dmode >> 1) & 1;
+                const float* px0 = tx ? DTl + (int64_t)so.x * RP : PXl + (int64_t)so.x * PSTRIDE;
                 const float* px1 = PXl + (int64_t)so.y * PSTRIDE;
-                const float* py0 = PXl + (int64_t)so.z * PSTRIDE;
+                const float* py0 = ty ? DTl + (int64_t)so.z * RP : PXl + (int64_t)so.z * PSTRIDE;
                 const float* py1 = PXl + (int64_t)so.w * PSTRIDE;
 #if PNDF_PF
                 // software prefetch (into L1) of the next step's SAT rows (and Zc rows with PNDF_PF=2), so
@@ -332,26 +347,42 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                                          (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
                     } else if (U32) {
                         // exact integer differences of the fixed-point SATs (scale folded into Zc)
-                        const uint4 qx1 = ldg_sat(px1 + v * G * 4);
-                        const uint4 qx0 = ldg_sat(px0 + v * G * 4);
-                        const uint4 qy1 = ldg_sat(py1 + v * G * 4);
-                        const uint4 qy0 = ldg_sat(py0 + v * G * 4);
-                        dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
-                                         __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
-                        dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
-                                         __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                        if (tx) {
+                            dx = ldg4(px0 + v * G * 4);
+                        } else {
+                            const uint4 qx1 = ldg_sat(px1 + v * G * 4);
+                            const uint4 qx0 = ldg_sat(px0 + v * G * 4);
+                            dx = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                             __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                        }
+                        if (ty) {
+                            dy = ldg4(py0 + v * G * 4);
+                        } else {
+                            const uint4 qy1 = ldg_sat(py1 + v * G * 4);
+                            const uint4 qy0 = ldg_sat(py0 + v * G * 4);
+                            dy = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                             __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                        }
                     } else {
                         // Xbar, Ybar numerators: (hi1 - hi0) + (lo1 - lo0); hi1 - hi0 is exact
                         // under cancellation (Sterbenz), lo carries the fp64 residual.
                         const int cv = v * G * 4;
-                        const float4 xh1 = ldg4(px1 + cv), xh0 = ldg4(px0 + cv);
-                        const float4 xl1 = ldg4(px1 + RP + cv), xl0 = ldg4(px0 + RP + cv);
-                        const float4 yh1 = ldg4(py1 + cv), yh0 = ldg4(py0 + cv);
-                        const float4 yl1 = ldg4(py1 + RP + cv), yl0 = ldg4(py0 + RP + cv);
-                        dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
-                                         (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
-                        dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
-                                         (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                        if (tx) {
+                            dx = ldg4(px0 + cv);
+                        } else {
+                            const float4 xh1 = ldg4(px1 + cv), xh0 = ldg4(px0 + cv);
+                            const float4 xl1 = ldg4(px1 + RP + cv), xl0 = ldg4(px0 + RP + cv);
+                            dx = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                             (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                        }
+                        if (ty) {
+                            dy = ldg4(py0 + cv);
+                        } else {
+                            const float4 yh1 = ldg4(py1 + cv), yh0 = ldg4(py0 + cv);
+                            const float4 yl1 = ldg4(py1 + RP + cv), yl0 = ldg4(py0 + RP + cv);
+                            dy = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                             (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                        }
                     }
 #if PNDF_F2
                     // packed fp32 (FFMA2/FMUL2, sm_100): two ranks per instruction, same per-element

@@ -13,6 +13,10 @@
 #include <new>
 
 #include "internal.cuh"
+
+#ifndef PNDF_DTAB
+#define PNDF_DTAB 1  // build the small-range difference table (query_kernel: one load per axis and rank chunk)
+#endif
 #include "launch.h"
 
 using namespace pndf;
@@ -101,6 +105,7 @@ struct pndf_store_s {
     QParams qp{};
     float* Zc = nullptr;
     float* PXY = nullptr;
+    float* DT = nullptr;
     uint32_t* err = nullptr;
     Scratch main;
     Slot slots[kSlots];
@@ -243,6 +248,7 @@ void destroy(pndf_store_s* s) {
     cudaDeviceSynchronize();
     cudaFree(s->Zc);
     cudaFree(s->PXY);
+    cudaFree(s->DT);
     cudaFree(s->err);
     cudaFree(s->d_slab_ptr);
     cudaFree(s->d_group_set);
@@ -671,6 +677,26 @@ static pndf_status load_impl(const pndf_desc* desc, int64_t P_override, const fl
     p.prefix_u32 = use_u32 ? 1 : 0;
     p.inv_s0 = 1.0f / (float)s0;
     p.mean = 1;
+    p.DT = nullptr;
+    p.dt_w = 0;
+#if PNDF_DTAB
+    {  // range table for rectangles of side <= W (2 A W Rp floats; 8.4 MB for config 5)
+        const int W = std::min(16, A);
+        if (cudaMalloc(&s->DT, sizeof(float) * (size_t)2 * A * W * Rp) == cudaSuccess &&
+            launch_range_table(s->PXY, A, Rp, use_u32 ? 1 : 0, W, s->DT, st) == cudaSuccess &&
+            cudaStreamSynchronize(st) == cudaSuccess) {
+            p.DT = s->DT;
+            p.dt_w = W;
+            s->stats.kernel_launches += 1;
+            s->stats.range_table_bytes = (int64_t)sizeof(float) * 2 * A * W * Rp;
+            s->stats.range_table_width = W;
+        } else {
+            cudaGetLastError();
+            cudaFree(s->DT);
+            s->DT = nullptr;
+        }
+    }
+#endif
     s->stats.rows = s->P;
     s->stats.rank_padded = Rp;
     s->stats.lanes_per_query = s->G;

@@ -351,3 +351,31 @@ def test_binning_sorts_by_half_cell_key(k):
         return out
     want = 4 * off + (spread(hu) | (spread(hv) << 1))
     assert np.array_equal(kk, want[p])
+
+
+@pytest.mark.parametrize("prefix", [2, 4])
+def test_range_table_widths(prefix):
+    """Narrow ranges (<= W = 16 bins) read the range table DT, wider ones the two SAT rows: every
+    width 1..A on each axis, both SAT formats, against the oracle."""
+    from paper_2109_14807_b200 import pndf
+    N, s0, L, A, R = 32, 1, 6, 40, 12
+    P = sum((N >> l) ** 2 for l in range(L))
+    f = synth.random_factors(A, R, P, seed=17, sparsity=0.3)
+    rng = np.random.default_rng(18)
+    wx = np.repeat(np.arange(1, A + 1), A)
+    wy = np.tile(np.arange(1, A + 1), A)
+    x1 = rng.integers(0, A - wx + 1)
+    y1 = rng.integers(0, A - wy + 1)
+    n = wx.shape[0]
+    recs = synth.make_records(rng.uniform(0, N, n), rng.uniform(0, N, n), np.exp2(rng.uniform(0, L, n)),
+                              x1, x1 + wx - 1, y1, y1 + wy - 1)
+    d = pndf.make_desc(N, s0, L, A, R, True, prefix=prefix)
+    st = pndf.load_factors(d, f.C, f.X, f.Y, f.Z)
+    s = st.stats()
+    assert s["range_table_width"] == 16 and s["range_table_bytes"] == 4 * 2 * A * 16 * s["rank_padded"]
+    out = torch.empty(n, dtype=torch.float32, device="cuda")
+    st.query_batch(torch_records(recs), out, 0)
+    st.sync()
+    st.free()
+    ref = oracle.query_batch(oracle.make_desc(N, s0, L, A, R, True), f.C, f.X, f.Y, f.Z, recs)
+    assert_parity(out.cpu().numpy(), ref, "range table widths")
