@@ -317,6 +317,16 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 }
                 float acc = 0.f;
                 float2 acc2 = make_float2(0.f, 0.f);
+                float4 dxv[NV], dyv[NV];
+                if (!TMA && dmode == 3) {
+                    // both ranges narrow (every BJ config): one range-table row per axis; a real
+                    // (warp-uniform) branch, so the SAT path below costs no issue slots here
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        dxv[v] = ldg4(px0 + v * G * 4);
+                        dyv[v] = ldg4(py0 + v * G * 4);
+                    }
+                } else {
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     const int c = (gl + v * G) * 4;
@@ -384,6 +394,13 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                                              (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
                         }
                     }
+                    dxv[v] = dx;
+                    dyv[v] = dy;
+                }
+                }
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float4 dx = dxv[v], dy = dyv[v];
 #if PNDF_F2
                     // packed fp32 (FFMA2/FMUL2, sm_100): two ranks per instruction, same per-element
                     // rounding as the scalar chain; the rank sum runs in two interleaved halves
