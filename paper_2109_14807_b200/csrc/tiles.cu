@@ -42,6 +42,11 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
     const float* __restrict__ PX = p.PXY;
     const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * PSTRIDE;
     const uint64_t seed_mixed = tile_mix(tp.seed);
+    // per group: tile ids of the level's candidate-tile box, hashed once by the group's lanes
+    constexpr int TBOX = G >= 8 ? 64 : 16;  // 6 x 6 candidate tiles at the top levels (8 KB of smem at G = 8)
+    __shared__ int s_tile[8][32 / G][TBOX];
+    int* my_tiles = s_tile[threadIdx.x >> 5][grp];
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
     const int M = tp.margin;
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -75,6 +80,17 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
                 const int64_t iu = (int64_t)flu, iv = (int64_t)flv;
                 const float wa = wl * (1.f - a), wb = wl * a;
                 const float wk4[4] = {wa * (1.f - b), wb * (1.f - b), wa * b, wb * b};
+                // candidate tiles of all 4 neighbours lie in one small box: hash each cell once
+                const int64_t MB = M < 2 ? M : 2;
+                const int64_t bx0 = (iu - (nl + MB) + 1) >> sh, bx1 = (iu + 1 + MB) >> sh;
+                const int64_t by0 = (iv - (nl + MB) + 1) >> sh, by1 = (iv + 1 + MB) >> sh;
+                const int bw = (int)(bx1 - bx0 + 1);
+                const int nc = bw * (int)(by1 - by0 + 1);
+                const bool boxed = nc <= TBOX;  // group-uniform
+                __syncwarp(gmask);              // the previous level's readers are done
+                if (boxed)
+                    for (int c = gl; c < nc; c += G) my_tiles[c] = tile_of(seed_mixed, bx0 + c % bw, by0 + c / bw);
+                __syncwarp(gmask);
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int64_t iw = iu + (k & 1), jw = iv + (k >> 1);
@@ -89,7 +105,8 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
                         for (int64_t tx = tx0; tx <= tx1; ++tx) {
                             const int64_t il = iw - (tx << sh), jl = jw - (ty << sh);
                             if (il < -MA || il >= nl + MA || jl < -MA || jl >= nl + MA) continue;
-                            const int tile = tile_of(seed_mixed, tx, ty);
+                            const int tile = boxed ? my_tiles[(int)(ty - by0) * bw + (int)(tx - bx0)]
+                                                   : tile_of(seed_mixed, tx, ty);
                             const int64_t row = (int64_t)tile * tp.p_ext + off + (jl + M) * ne + (il + M);
 #pragma unroll
                             for (int v = 0; v < NV; ++v) {
