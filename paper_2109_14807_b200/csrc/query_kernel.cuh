@@ -151,6 +151,9 @@ constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced 
 #ifndef PNDF_F2
 #define PNDF_F2 1  // 1: packed fp32 FFMA2/FMUL2 for the interpolation and rank product (sm_100)
 #endif
+#ifndef PNDF_NOREUSE
+#define PNDF_NOREUSE 0  // 1: no cross-step register reuse of Zc rows (fewer live registers; experiment)
+#endif
 #ifndef PNDF_PF
 #define PNDF_PF 0  // 1: prefetch the next step's SAT rows into L1; 2: and its Zc rows (experiment)
 #endif
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 #endif
                 // warp-uniform for G == 32 (every lane reads the same descriptor)
                 const bool reuse = (G == 32) && s > 0 && ((reuse_mask >> s) & 1u);
-                if (!reuse) {
+                if (!PNDF_NOREUSE && !reuse) {
                     const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
                     const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
                     const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
@@ -401,6 +404,16 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 #pragma unroll
                 for (int v = 0; v < NV; ++v) {
                     const float4 dx = dxv[v], dy = dyv[v];
+#if PNDF_NOREUSE
+                    {  // experiment: Zc rows loaded per rank chunk, no cross-step register copy
+                        const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
+                        const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
+                        const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
+                                            (int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) zc[v][k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
+                    }
+#endif
 #if PNDF_F2
                     // packed fp32 (FFMA2/FMUL2, sm_100): two ranks per instruction, same per-element
                     // rounding as the scalar chain; the rank sum runs in two interleaved halves
