@@ -151,6 +151,9 @@ constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced 
 #ifndef PNDF_F2
 #define PNDF_F2 1  // 1: packed fp32 FFMA2/FMUL2 for the interpolation and rank product (sm_100)
 #endif
+#ifndef PNDF_PREUSE
+#define PNDF_PREUSE 1  // 1: per-level Zc row reuse (rows 0-3 / 4-7 separately); 0: all 8 rows or none
+#endif
 #ifndef PNDF_NOREUSE
 #define PNDF_NOREUSE 0  // 1: no cross-step register reuse of Zc rows (fewer live registers; experiment)
 #endif
@@ -249,12 +252,28 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 wd[lane].mode = 0;
                 wd[lane].div = 1.f;
             }
+#if PNDF_PREUSE
+            // the 4 rows of each level are fixed by the level's first row: reuse per level when it
+            // repeats (same l0 cell -> rows 0-3, same l0+1 cell -> rows 4-7)
+            const bool kv = key != 0xffffffffu;
+            const int32_t klo = kv ? wd[lane].row[0] : -1, khi = kv ? wd[lane].row[4] : -1;
+            const int32_t plo = __shfl_up_sync(0xffffffffu, klo, 1), phi = __shfl_up_sync(0xffffffffu, khi, 1);
+            const uint32_t same_lo = __ballot_sync(0xffffffffu, lane > 0 && kv && klo == plo);
+            const uint32_t same_hi = __ballot_sync(0xffffffffu, lane > 0 && kv && khi == phi);
+            if (lane == 0) {
+                sreuse[2 * warp] = same_lo;
+                sreuse[2 * warp + 1] = same_hi;
+            }
+#else
             const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
             const uint32_t same = __ballot_sync(0xffffffffu, lane > 0 && key == prev && key != 0xffffffffu);
-            if (lane == 0) sreuse[warp] = same;
+            if (lane == 0) sreuse[2 * warp] = sreuse[2 * warp + 1] = same;
+#endif
         }
         __syncwarp();
-        const uint32_t reuse_mask = (G == 32) ? sreuse[warp] : 0u;
+        const uint32_t reuse_mask = (G == 32) ? (sreuse[2 * warp] & sreuse[2 * warp + 1]) : 0u;
+        const uint32_t reuse_lo = (G == 32) ? sreuse[2 * warp] : 0u;
+        const uint32_t reuse_hi = (G == 32) ? sreuse[2 * warp + 1] : 0u;
         if (TMA) issue_sat(0);
         // 2-3. gather + batched reduce
         float res = 0.f;
@@ -307,16 +326,26 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 }
 #endif
                 // warp-uniform for G == 32 (every lane reads the same descriptor)
-                const bool reuse = (G == 32) && s > 0 && ((reuse_mask >> s) & 1u);
-                if (!PNDF_NOREUSE && !reuse) {
+                // warp-uniform for G == 32: level l0's rows (0-3) and level l0+1's rows (4-7) are
+                // re-read only when they differ from the previous query's
+                const bool reuse0 = (G == 32) && s > 0 && ((reuse_lo >> s) & 1u);
+                const bool reuse1 = (G == 32) && s > 0 && ((reuse_hi >> s) & 1u);
+                if (!PNDF_NOREUSE && !reuse0) {
                     const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
-                    const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
-                    const int row[8] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w,
-                                        (int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
+                    const int row[4] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w};
 #pragma unroll
                     for (int v = 0; v < NV; ++v)
 #pragma unroll
-                        for (int k = 0; k < 8; ++k) zc[v][k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
+                        for (int k = 0; k < 4; ++k) zc[v][k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
+                }
+                if (!PNDF_NOREUSE && !reuse1) {
+                    const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
+                    const int row[4] = {(int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
+#pragma unroll
+                    for (int v = 0; v < NV; ++v)
+#pragma unroll
+                        for (int k = 0; k < 4; ++k)
+                            zc[v][4 + k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
                 }
                 float acc = 0.f;
                 float2 acc2 = make_float2(0.f, 0.f);
