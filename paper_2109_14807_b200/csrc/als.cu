@@ -140,6 +140,13 @@ __device__ __forceinline__ void tma_2d(void* dst, const CUtensorMap* tm, int c0,
         "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* tm, int c0, int c1, int c2, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
 // K-major operand tile in the 128-byte swizzle layout TMA writes (8-row atoms of 1024 B):
 // start >> 4, LBO = 1 (unused for swizzled K-major), SBO = 1024 B, version 1, layout SWIZZLE_128B
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -178,6 +185,7 @@ struct GemmArgs {
     int32_t stages;
     int32_t a_shift;   // log2(A): z = row >> a_shift (epilogue 1)
     int32_t bres;      // 1: the whole B operand (kblocks x hi/lo) is loaded once and stays in shared memory
+    int32_t kbs;       // K-blocks per pipeline stage (> 1 only with bres: one 3-D TMA box per tile row block)
     float* out;        // epilogue 0: [rows][RP]
     const float* Zf;   // epilogue 1: [P][RP] fp32 Z
     float* part;       // epilogue 1: [grid][BM][RP] per-thread partial sums
@@ -194,8 +202,12 @@ struct GemmLayout {
     // B-resident variant (short K: modes X / Y): B region [kblocks][hi | lo] then A-only stages
     __host__ __device__ static int bres_bytes(int kblocks) { return kblocks * 2 * B_BYTES; }
     static bool bres_fits(int kblocks) { return bres_bytes(kblocks) <= 64 * 1024; }
-    static int bres_stages(int kblocks) { return std::min(8, (200 * 1024 - bres_bytes(kblocks)) / A_BYTES); }
-    static size_t bres_smem(int kblocks, int st) { return 1024 + (size_t)bres_bytes(kblocks) + (size_t)st * A_BYTES + 256; }
+    static int bres_stages(int kblocks, int kbs) {
+        return std::min(8, (200 * 1024 - bres_bytes(kblocks)) / (kbs * A_BYTES));
+    }
+    static size_t bres_smem(int kblocks, int kbs, int st) {
+        return 1024 + (size_t)bres_bytes(kblocks) + (size_t)st * kbs * A_BYTES + 256;
+    }
 };
 
 // Warp-specialised persistent GEMM, one CTA per SM: warps 0-3 epilogue (TMEM lanes 32w..32w+31),
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(192, 1) mttkrp_gemm_kernel(const __grid_consta
     unsigned char* gsm = reinterpret_cast<unsigned char*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
     const int S = g.stages;
     const bool bres = g.bres != 0;
-    const int stage_bytes = bres ? LY::A_BYTES : LY::STAGE;
+    const int stage_bytes = bres ? g.kbs * LY::A_BYTES : LY::STAGE;
     unsigned char* bsm = gsm;                                                   // resident B (bres)
     unsigned char* asm_ = gsm + (bres ? LY::bres_bytes(g.kblocks) : 0);          // stages
     uint64_t* full = reinterpret_cast<uint64_t*>(asm_ + (size_t)S * stage_bytes);
@@ -257,11 +269,14 @@ __global__ void __launch_bounds__(192, 1) mttkrp_gemm_kernel(const __grid_consta
             int s = 0;
             uint32_t ph = 0;
             for (int64_t tile = blockIdx.x; tile < g.ntiles; tile += gridDim.x) {
-                for (int kb = 0; kb < g.kblocks; ++kb) {
+                for (int kb = 0; kb < g.kblocks; kb += g.kbs) {
                     mbar_wait(empty + s, ph ^ 1u);
                     unsigned char* st = asm_ + (size_t)s * stage_bytes;
                     mbar_arrive_expect_tx(full + s, stage_bytes);
-                    tma_2d(st, &tmA, kb * BK, (int)(tile * BM), full + s);
+                    if (g.kbs > 1)  // [kb][128 rows][32] in one box: whole 128-row x K slab, read contiguously
+                        tma_3d(st, &tmA, 0, (int)(tile * BM), kb, full + s);
+                    else
+                        tma_2d(st, &tmA, kb * BK, (int)(tile * BM), full + s);
                     if (!bres) {
                         tma_2d(st + LY::A_BYTES, &tmBh, kb * BK, 0, full + s);
                         tma_2d(st + LY::A_BYTES + LY::B_BYTES, &tmBl, kb * BK, 0, full + s);
@@ -286,19 +301,22 @@ __global__ void __launch_bounds__(192, 1) mttkrp_gemm_kernel(const __grid_consta
             mbar_wait(tempty + b, ((uint32_t)(i >> 1) & 1u) ^ 1u);
             tc_fence_after();
             const uint32_t d = tmem + (uint32_t)(b * RP);
-            for (int kb = 0; kb < g.kblocks; ++kb) {
+            for (int kb0 = 0; kb0 < g.kblocks; kb0 += g.kbs) {
                 mbar_wait(full + s, ph);
                 tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t sa = smem_u32(asm_ + (size_t)s * stage_bytes);
-                    const uint32_t sb = bres ? smem_u32(bsm + (size_t)(2 * kb) * LY::B_BYTES) : sa + LY::A_BYTES;
-                    const uint64_t da = sw128_desc(sa);
-                    const uint64_t dh = sw128_desc(sb);
-                    const uint64_t dl = sw128_desc(sb + LY::B_BYTES);
+                    for (int j = 0; j < g.kbs; ++j) {
+                        const int kb = kb0 + j;
+                        const uint32_t sa = smem_u32(asm_ + (size_t)s * stage_bytes) + (uint32_t)(j * LY::A_BYTES);
+                        const uint32_t sb = bres ? smem_u32(bsm + (size_t)(2 * kb) * LY::B_BYTES) : sa + LY::A_BYTES;
+                        const uint64_t da = sw128_desc(sa);
+                        const uint64_t dh = sw128_desc(sb);
+                        const uint64_t dl = sw128_desc(sb + LY::B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < BK / 8; ++k) {  // UMMA K = 8 tf32 = 32 bytes = +2 in the address field
-                        mma_tf32(d, da + 2 * k, dh + 2 * k, idesc, (kb | k) != 0);
-                        mma_tf32(d, da + 2 * k, dl + 2 * k, idesc, 1u);
+                        for (int k = 0; k < BK / 8; ++k) {  // UMMA K = 8 tf32 = 32 bytes = +2 in the address field
+                            mma_tf32(d, da + 2 * k, dh + 2 * k, idesc, (kb | k) != 0);
+                            mma_tf32(d, da + 2 * k, dl + 2 * k, idesc, 1u);
+                        }
                     }
                     mma_commit(empty + s);  // frees the stage when these MMAs complete
                 }
@@ -735,6 +753,32 @@ CUtensorMap make_map(const float* base, uint64_t rows, uint64_t cols, uint32_t b
     return m;
 }
 
+// 3-D view [kblock][rows][32] of a row-major [rows][K] fp32 operand (K = 32 * kblocks): box {32, box_rows,
+// kblocks} lands as kblocks stacked 128-byte-swizzled [box_rows][32] tiles, i.e. the UMMA K-major layout
+CUtensorMap make_map3(const float* base, uint64_t rows, uint64_t K, uint32_t box_rows) {
+    CUtensorMap m;
+    auto fn = encode_fn();
+    if (!fn) {
+        pndf::set_last_error("cuTensorMapEncodeTiled unavailable");
+        throw Fail{PNDF_ECUDA};
+    }
+    const uint32_t kb = (uint32_t)(K / BK);
+    cuuint64_t dims[3] = {(cuuint64_t)BK, rows, kb};
+    cuuint64_t strides[2] = {K * sizeof(float), BK * sizeof(float)};
+    cuuint32_t box[3] = {(cuuint32_t)BK, box_rows, kb};
+    cuuint32_t es[3] = {1, 1, 1};
+    CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        char msg[64];
+        snprintf(msg, sizeof(msg), "cuTensorMapEncodeTiled (3-D) failed (%d)", (int)r);
+        pndf::set_last_error(msg);
+        throw Fail{PNDF_ECUDA};
+    }
+    return m;
+}
+
 int ilog2i(int64_t x) {
     int l = 0;
     while ((int64_t(1) << (l + 1)) <= x) ++l;
@@ -784,7 +828,18 @@ int num_sms() {
 struct Buffers {
     cudaStream_t st;
     std::vector<void*> ptrs;
-    explicit Buffers(cudaStream_t s) : st(s) {}
+    explicit Buffers(cudaStream_t s) : st(s) { keep_pool(); }
+    // keep freed blocks cached in the device's default pool (the default release threshold of 0 hands
+    // them back to the driver at every synchronisation, so each call would re-map ~10^8 bytes)
+    static void keep_pool() {
+        int dev = 0;
+        cudaMemPool_t pool;
+        if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+        cudaGetLastError();
+    }
     template <class T>
     T* alloc(size_t n) {
         void* p = nullptr;
@@ -801,9 +856,10 @@ template <int RP, int EPI>
 void launch_gemm_rp(const CUtensorMap& a, const CUtensorMap& bh, const CUtensorMap& bl, GemmArgs g, int grid,
                     cudaStream_t st) {
     using LY = GemmLayout<RP>;
-    g.bres = 0;  // B-resident staging for short K measured no faster than streaming B from L2
-    g.stages = g.bres ? LY::bres_stages(g.kblocks) : LY::stages();
-    const size_t sm = g.bres ? LY::bres_smem(g.kblocks, g.stages) : LY::smem(g.stages);
+    // short K (modes X / Y, a3d map): B resident, all K-blocks of a tile in one stage (one 3-D TMA box)
+    g.bres = g.kbs > 1 ? 1 : 0;
+    g.stages = g.bres ? LY::bres_stages(g.kblocks, g.kbs) : LY::stages();
+    const size_t sm = g.bres ? LY::bres_smem(g.kblocks, g.kbs, g.stages) : LY::smem(g.stages);
     ACK(cudaFuncSetAttribute(mttkrp_gemm_kernel<RP, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
     mttkrp_gemm_kernel<RP, EPI><<<grid, 192, sm, st>>>(a, bh, bl, g);
     ACK(cudaGetLastError());
@@ -825,7 +881,7 @@ struct Builder {
     Geometry g;
     cudaStream_t st;
     int sms;
-    Buffers buf{nullptr};
+    Buffers buf{nullptr};  // stream set in the constructor
     double *Z, *X, *Y;          // masters [rows][R]
     float* Zf;                  // [P][RP]
     float *kr_hi, *kr_lo;       // [RP][A^2]
@@ -840,6 +896,7 @@ struct Builder {
     uint32_t* bad;
     int ggrid;                  // Gram partial blocks
     CUtensorMap mD_z, mD_x, mDt_y, mKr_h, mKr_l, mT_h, mT_l;
+    int kbs_xy = 1;  // K-blocks per stage of the mode X / Y GEMMs
 
     Builder(const Geometry& geo, cudaStream_t s, const float* D, const float* Dt) : g(geo), st(s) {
         buf.st = s;
@@ -867,8 +924,12 @@ struct Builder {
         terms = buf.alloc<double>(2);
         bad = buf.alloc<uint32_t>(1);
         mD_z = make_map(D, (uint64_t)P, (uint64_t)A * A, BM);
-        mD_x = make_map(D, (uint64_t)P * A, (uint64_t)A, BM);
-        if (Dt) mDt_y = make_map(Dt, (uint64_t)P * A, (uint64_t)A, BM);
+        const int64_t bres_b = (int64_t)(A / BK) * 2 * RP * BK * sizeof(float);  // resident B (hi + lo)
+        kbs_xy = (A / BK > 1 && bres_b <= 64 * 1024) ? A / BK : 1;
+        mD_x = kbs_xy > 1 ? make_map3(D, (uint64_t)P * A, (uint64_t)A, BM) : make_map(D, (uint64_t)P * A, (uint64_t)A, BM);
+        if (Dt)
+            mDt_y = kbs_xy > 1 ? make_map3(Dt, (uint64_t)P * A, (uint64_t)A, BM)
+                               : make_map(Dt, (uint64_t)P * A, (uint64_t)A, BM);
         mKr_h = make_map(kr_hi, RP, (uint64_t)A * A, RP);
         mKr_l = make_map(kr_lo, RP, (uint64_t)A * A, RP);
         mT_h = make_map(t_hi, RP, A, RP);
@@ -900,6 +961,7 @@ struct Builder {
         a.rows = g.P;
         a.ntiles = (g.P + BM - 1) / BM;
         a.kblocks = A * A / BK;
+        a.kbs = 1;
         a.out = Mz;
         launch_gemm<0>(g.RP, mD_z, mKr_h, mKr_l, a, (int)std::min<int64_t>(a.ntiles, sms), st);
     }
@@ -913,6 +975,7 @@ struct Builder {
         a.rows = g.P * A;
         a.ntiles = (a.rows + BM - 1) / BM;
         a.kblocks = A / BK;
+        a.kbs = kbs_xy;
         a.a_shift = g.a_shift;
         a.Zf = Zf;
         a.part = part;
