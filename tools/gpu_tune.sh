@@ -1,5 +1,7 @@
 #!/bin/bash
+# config 5 at the 8-GPU shard size (1.25e8 queries) and at 2 GPUs (5e8), single GPU
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_als.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_als.csv python bench.py --op als --config 2 --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu_als_l.log 2>&1
-timeout 600 python bench.py --op als --config 2 > gpurun_out/bench_als.log 2>&1
+for q in 125000000 250000000 500000000; do
+timeout 600 python bench.py --queries $q --no-e2e --no-cpu-baseline > gpurun_out/shard_$q.log 2>&1
+echo "$q $(grep -o '"value": [0-9.e+]*' gpurun_out/shard_$q.log | head -1) $(grep -o '"kernel_ms": [0-9.e+]*' gpurun_out/shard_$q.log | head -1) $(grep -o '"binning_ms": [0-9.e+]*' gpurun_out/shard_$q.log | head -1)" >> gpurun_out/shard.txt
+done
