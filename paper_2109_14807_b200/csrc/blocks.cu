@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(256) blocked_query_kernel(const QParams p, con
                 axis_cells<WRAP>(p, rec.u, l, i0, i1, a);
                 axis_cells<WRAP>(p, rec.v, l, j0, j1, b);
                 const int64_t nl = p.n0 >> l;
-                const int64_t s = (int64_t)(p.N / p.n0) << l;  // s0 * 2^l
+                const int lsh = __ffs(p.N / p.n0) - 1 + l;  // log2(s0 * 2^l)
                 const int64_t off = level_offset(p.n0, l);
                 const float wa = wl * (1.f - a), wb = wl * a;
                 const float wk4[4] = {wa * (1.f - b), wb * (1.f - b), wa * b, wb * b};
@@ -100,7 +100,11 @@ __global__ void __launch_bounds__(256) blocked_query_kernel(const QParams p, con
                     if (wk == 0.f) continue;  // group-uniform
                     const int64_t i = (k & 1) ? i1 : i0, j = (k >> 1) ? j1 : j0;
                     const int64_t z = off + j * nl + i;
-                    const int64_t reg = (((2 * j + 1) * s) / (2 * bp.region)) * bp.nr + ((2 * i + 1) * s) / (2 * bp.region);
+                    // region of the centre ((i+1/2)s, (j+1/2)s) = floor((2i+1) s / (2 region)); s and region
+                    // are powers of two, so a shift (a 64-bit division here costs ~70 instructions)
+                    const int rsh = lsh - 1 - bp.r_shift;
+                    const int64_t reg = (rsh >= 0 ? ((2 * j + 1) << rsh) : ((2 * j + 1) >> -rsh)) * bp.nr +
+                                        (rsh >= 0 ? ((2 * i + 1) << rsh) : ((2 * i + 1) >> -rsh));
                     for (int byb = y1 / t; byb <= y2 / t; ++byb)
                         for (int bxb = x1 / t; bxb <= x2 / t; ++bxb) {
                             const int blk = byb * nb + bxb;

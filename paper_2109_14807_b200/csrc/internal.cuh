@@ -55,6 +55,7 @@ struct BlockParams {
     int32_t nr;                 // regions per axis (N / region)
     const int32_t* slab_ptr;    // [P][nb^2] Zc row or -1
     const int32_t* group_set;   // [nr^2 * nb^2] factor set or -1
+    int32_t r_shift;            // log2 region (a power of two)
 };
 
 // Device scratch of one in-flight binned batch (radix sort double buffers).

@@ -478,6 +478,7 @@ pndf_status pndf_load_blocked(const pndf_block_desc* bd, const float* C, const f
     s->bp.nb = nb;
     s->bp.region = bd->region;
     s->bp.nr = (int32_t)nr;
+    s->bp.r_shift = ilog2(bd->region);
     s->bp.slab_ptr = s->d_slab_ptr;
     s->bp.group_set = s->d_group_set;
     s->stats.rows = S;

@@ -1,7 +1,6 @@
 #!/bin/bash
-# config 5 at the 8-GPU shard size (1.25e8 queries) and at 2 GPUs (5e8), single GPU
 mkdir -p gpurun_out
-for q in 125000000 250000000 500000000; do
-timeout 600 python bench.py --queries $q --no-e2e --no-cpu-baseline > gpurun_out/shard_$q.log 2>&1
-echo "$q $(grep -o '"value": [0-9.e+]*' gpurun_out/shard_$q.log | head -1) $(grep -o '"kernel_ms": [0-9.e+]*' gpurun_out/shard_$q.log | head -1) $(grep -o '"binning_ms": [0-9.e+]*' gpurun_out/shard_$q.log | head -1)" >> gpurun_out/shard.txt
-done
+timeout 900 python -m pytest tests/test_gpu_blocked.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --op blocked --config 2 > gpurun_out/bench_blocked.log 2>&1
+BCMD="python bench.py --op blocked --config 2 --steps 1 --warmup 1 --no-cpu-baseline"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:blocked_query -c 1 -o gpurun_out/prof_blocked -f $BCMD > gpurun_out/ncu_blocked.log 2>&1
