@@ -83,6 +83,7 @@ __global__ void __launch_bounds__(256) blocked_query_kernel(const QParams p, con
             int l0;
             float tl;
             level_select(p, rec.size, l0, tl);
+            const int bx0 = x1 / t, bx1 = x2 / t, by0 = y1 / t, by1 = y2 / t;  // the rectangle's blocks
             for (int dl = 0; dl < 2; ++dl) {
                 const int l = l0 + dl;
                 const float wl = dl ? tl : 1.f - tl;
@@ -105,8 +106,8 @@ __global__ void __launch_bounds__(256) blocked_query_kernel(const QParams p, con
                     const int rsh = lsh - 1 - bp.r_shift;
                     const int64_t reg = (rsh >= 0 ? ((2 * j + 1) << rsh) : ((2 * j + 1) >> -rsh)) * bp.nr +
                                         (rsh >= 0 ? ((2 * i + 1) << rsh) : ((2 * i + 1) >> -rsh));
-                    for (int byb = y1 / t; byb <= y2 / t; ++byb)
-                        for (int bxb = x1 / t; bxb <= x2 / t; ++bxb) {
+                    for (int byb = by0; byb <= by1; ++byb)
+                        for (int bxb = bx0; bxb <= bx1; ++bxb) {
                             const int blk = byb * nb + bxb;
                             const int32_t slab = __ldg(bp.slab_ptr + z * nb2 + blk);
                             if (slab < 0) continue;  // blank block
