@@ -276,7 +276,7 @@ pndf_status pndf_set_lanes(pndf_store s, int32_t lanes);
  * The tensor the paper compresses (footprint NDF images stacked along the third dimension) and its
  * CP decomposition by alternating least squares (Eq. 5: "maximum error 1e-4, maximum
  * iteration count 500"), for ONE global group (readings 14, 23).  Limits: A a power of two,
- * 4 <= A <= 128, 1 <= R <= 128, P * A < 2^32.  All pointers are DEVICE memory; calls enqueue on cuda_stream
+ * 32 <= A <= 128, 1 <= R <= 128, N <= 32768, P * A < 2^31.  All pointers are DEVICE memory; calls enqueue on cuda_stream
  * and pndf_cp_als synchronises once per sweep (to test the stopping rule).
  *
  * pndf_hist_tensor: D[z][x][y] = tf32(count / total) -- the footprint-weighted histogram of the map's

@@ -72,9 +72,9 @@ __global__ void __launch_bounds__(256) hist_kernel(const uint16_t* __restrict__ 
         const int bu = (int)((((int64_t)i * h.s + h.qmin) % N + N) % N);
         const int bv = (int)((((int64_t)j * h.s + h.qmin) % N + N) % N);
         const uint32_t* w = wtab + h.woff;
-        const int64_t nwin = (int64_t)h.wf * h.wf;
-        for (int64_t t = threadIdx.x; t < nwin; t += blockDim.x) {
-            const int q = (int)(t / h.wf), p = (int)(t % h.wf);
+        const int nwin = h.wf * h.wf;  // <= N^2 < 2^31; 32-bit division (the 64-bit one costs ~70 instructions)
+        for (int t = threadIdx.x; t < nwin; t += blockDim.x) {
+            const int q = t / h.wf, p = t - q * h.wf;
             int v = bv + q, u = bu + p;
             if (v >= N) v -= N;
             if (u >= N) u = 0 + (u - N);
@@ -83,14 +83,23 @@ __global__ void __launch_bounds__(256) hist_kernel(const uint16_t* __restrict__ 
             atomicAdd(&cnt[y * AP + x], (unsigned long long)w[q] * (unsigned long long)w[p]);
         }
         __syncthreads();
+        // counts -> tf32 values in place (once per bin; most bins of a footprint are empty), then both
+        // layouts are written with coalesced stores
+        for (int b = threadIdx.x; b < A * AP; b += blockDim.x) {
+            const unsigned long long k = cnt[b];
+            cnt[b] = k ? (unsigned long long)__float_as_uint(tf32_rne((double)k / h.tot)) : 0ull;
+        }
+        __syncthreads();
         const int64_t base = z * (int64_t)A * A;
         for (int o = threadIdx.x; o < A * A; o += blockDim.x) {
-            const int x = o / A, y = o % A;  // D[z][x][y]; most bins of a footprint are empty
-            const unsigned long long k = cnt[y * AP + x];
-            const float v = k ? tf32_rne((double)k / h.tot) : 0.f;
-            D[base + o] = v;
-            if (Dt) Dt[base + y * A + x] = v;
+            const int x = o / A, y = o % A;  // D[z][x][y]
+            D[base + o] = __uint_as_float((uint32_t)cnt[y * AP + x]);
         }
+        if (Dt)
+            for (int o = threadIdx.x; o < A * A; o += blockDim.x) {
+                const int y = o / A, x = o % A;  // Dt[z][y][x]
+                Dt[base + o] = __uint_as_float((uint32_t)cnt[y * AP + x]);
+            }
         __syncthreads();
     }
 }
@@ -796,7 +805,7 @@ pndf_status check_desc(const pndf_desc* d, Geometry& g) {
     const int N = d->map_size, s0 = d->base_stride, L = d->num_levels, A = d->ang_res, R = d->rank;
     auto pow2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
     if (!pow2(N) || !pow2(s0) || s0 > N || L < 2 || L > 24 || (N / s0) < (1 << (L - 1))) return PNDF_EINVAL;
-    if (!pow2(A) || A < 32 || A > 128 || R < 1 || R > 128) return PNDF_EINVAL;
+    if (!pow2(A) || A < 32 || A > 128 || R < 1 || R > 128 || N > 32768) return PNDF_EINVAL;
     g.N = N;
     g.s0 = s0;
     g.L = L;
