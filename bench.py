@@ -47,6 +47,11 @@ def parse():
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
                          "prefiltering (SG rectangle generation + range query)")
     ap.add_argument("--queries", type=int, default=0, help="override the config's total query count")
+    ap.add_argument("--as-shard", default="", help="K/W: one GPU runs rank K's shard of a W-GPU job "
+                                                    "(per-GPU cost of the multi-GPU run on a one-GPU box)")
+    ap.add_argument("--shard", default="spatial", choices=["spatial", "index"],
+                    help="N > 1: spatial = rank k answers the stream's queries centred in the k-th vertical "
+                         "strip of the map; index = the k-th contiguous index range (identical at N = 1)")
     ap.add_argument("--bin", default="auto", choices=["auto", "on", "off"])
     ap.add_argument("--lanes", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -225,6 +230,22 @@ def oracle_sample_rate(cfg, f, recs, threads=0, min_seconds=0.0):
     return recs.shape[0] * passes / dt, dt, out, passes
 
 
+def spatial_shard(cfg, bins, n_total: int, rank: int, world: int):
+    """The stream's queries [0, n_total) whose centre lies in this rank's strip (shard.spatial_owner),
+    generated chunk by chunk (untimed setup), in stream order, as a pinned [n, 4] int32 tensor."""
+    import torch
+    from paper_2109_14807_b200.shard import spatial_owner
+    keep = []
+    chunk = 1 << 26
+    for a in range(0, n_total, chunk):
+        recs = synth.gen_queries(cfg, bins, a, min(n_total, a + chunk))
+        keep.append(recs[spatial_owner(recs["u"], cfg.N, world) == rank])
+    mine = np.concatenate(keep) if keep else np.empty(0, synth.QREC)
+    h_q = torch.empty((mine.shape[0], 4), dtype=torch.int32, pin_memory=True)
+    h_q.numpy().view(synth.QREC).reshape(-1)[:] = mine
+    return h_q
+
+
 def cpu_baseline(cfg, f, bins, shard0: int, seconds: float):
     """Oracle on a bounded sample of the same workload (first m queries of the stream), all host cores."""
     import oracle
@@ -300,8 +321,18 @@ def run_ours(args, cfg, rank, world, local_rank):
         store.set_lanes(args.lanes)
 
     # ---- this rank's query shard: pinned host copy (for e2e) + resident device copy
-    h_q = torch.empty((n, 4), dtype=torch.int32, pin_memory=True)
-    synth.gen_queries(cfg, bins, i0, i1, out=h_q.numpy().view(synth.QREC).reshape(-1))
+    sim_rank, sim_world = (int(x) for x in args.as_shard.split("/")) if args.as_shard else (rank, world)
+    if sim_world > 1 and args.shard == "spatial":
+        h_q = spatial_shard(cfg, bins, n_total, sim_rank, sim_world)
+        n = h_q.shape[0]
+    elif sim_world > 1:
+        i0, i1 = shard_range(n_total, sim_rank, sim_world)
+        n = i1 - i0
+        h_q = torch.empty((n, 4), dtype=torch.int32, pin_memory=True)
+        synth.gen_queries(cfg, bins, i0, i1, out=h_q.numpy().view(synth.QREC).reshape(-1))
+    else:
+        h_q = torch.empty((n, 4), dtype=torch.int32, pin_memory=True)
+        synth.gen_queries(cfg, bins, i0, i1, out=h_q.numpy().view(synth.QREC).reshape(-1))
     d_q = h_q.to(dev, non_blocking=False)
     d_out = torch.empty(n, dtype=torch.float32, device=dev)
     opts = {"auto": pndf.BIN_AUTO, "on": pndf.BIN_ON, "off": pndf.BIN_OFF}[args.bin]
@@ -340,7 +371,7 @@ def run_ours(args, cfg, rank, world, local_rank):
 
     checksum = float(d_out.double().sum().item())
     (ms_step, q_ms_max, b_ms_max), checksum = reduce_times_and_checksum([ms_rank, q_ms, b_ms], checksum, dev)
-    value = n_total / (ms_step * 1e-3)
+    value = (n if args.as_shard else n_total) / (ms_step * 1e-3)  # --as-shard: this shard's own rate
 
     # ---- end to end through the public API with HOST buffers (H2D + kernels + D2H inside)
     e2e = None
@@ -388,7 +419,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_name(cfg), "queries_total": n_total, "queries_per_rank": n,
-                       "parallelism": f"query-sharded x{world}, factors replicated",
+                       "parallelism": f"query-sharded x{world} ({args.shard if world > 1 else 'whole stream'}), "
+                                      "factors replicated",
                        "binning": args.bin, "binned": bool(st["last_binned"]),
                        "lanes_per_query": st["lanes_per_query"], "rank_padded": st["rank_padded"],
                        "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]],

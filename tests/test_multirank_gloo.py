@@ -68,3 +68,22 @@ def test_two_gloo_ranks_match_one_process(tmp_path):
     tmax, total = np.load(tmp_path / "reduced.npy")
     assert tmax == 2.0                                         # MAX over ranks of the step time
     assert total == pytest.approx(parts[0].sum() + parts[1].sum(), rel=1e-15)
+
+
+def test_spatial_owner_partitions_the_stream():
+    """Spatial sharding: every query has exactly one owner (a function of its centre), strips are
+    balanced for the configs' uniformly placed centres, world 1 owns everything."""
+    import synth
+    from paper_2109_14807_b200.shard import spatial_owner
+    cfg = synth.CONFIGS[5]
+    recs = synth.gen_queries(cfg, None, 0, 400_000)
+    for w in (1, 2, 4, 8):
+        own = spatial_owner(recs["u"], cfg.N, w)
+        assert own.min() >= 0 and own.max() <= w - 1
+        counts = np.bincount(own, minlength=w)
+        assert counts.sum() == recs.shape[0]
+        assert np.abs(counts / recs.shape[0] - 1.0 / w).max() < 0.01
+    assert (spatial_owner(recs["u"], cfg.N, 1) == 0).all()
+    # strips: owner is monotone in u and wraps
+    u = np.array([0.0, 511.99, 512.0, 4095.99, 4096.0, -1.0])
+    assert spatial_owner(u, 4096, 8).tolist() == [0, 0, 1, 7, 0, 7]

@@ -1,6 +1,9 @@
 #!/bin/bash
+# per-GPU cost of the 2/4/8-GPU config-5 jobs on one GPU: shard 0 of W, spatial vs index sharding
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_sampler.py -x -q > gpurun_out/pytest_gpu.log 2>&1; echo rc=$? >> gpurun_out/pytest_gpu.log
-timeout 600 python bench.py --op sample > gpurun_out/bench_sample.log 2>&1
-SCMD="python bench.py --op sample --steps 1 --warmup 1 --no-cpu-baseline"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:sample_kernel -c 1 -o gpurun_out/prof_sample -f $SCMD > gpurun_out/ncu_sample.log 2>&1
+for w in 2 4 8; do
+  for sh in spatial index; do
+    timeout 900 python bench.py --as-shard 0/$w --shard $sh --no-e2e --no-cpu-baseline > gpurun_out/as_${sh}_$w.log 2>&1
+    echo "W=$w $sh $(grep -o '"value": [0-9.e+]*' gpurun_out/as_${sh}_$w.log | head -1) $(grep -o '"ms_per_step": [0-9.e+]*' gpurun_out/as_${sh}_$w.log | head -1) $(grep -o '"queries_per_rank": [0-9]*' gpurun_out/as_${sh}_$w.log | head -1) $(grep -o '"pass": [a-z]*' gpurun_out/as_${sh}_$w.log | head -1)" >> gpurun_out/as.txt
+  done
+done
