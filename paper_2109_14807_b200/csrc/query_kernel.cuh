@@ -151,6 +151,9 @@ constexpr int kSteps = PNDF_KSTEPS;  // gather steps whose partials are reduced 
 #ifndef PNDF_F2
 #define PNDF_F2 1  // 1: packed fp32 FFMA2/FMUL2 for the interpolation and rank product (sm_100)
 #endif
+#ifndef PNDF_WSEG
+#define PNDF_WSEG 0  // 1: contiguous per-warp segments with row reuse across 32-query batches (experiment)
+#endif
 #ifndef PNDF_PREUSE
 #define PNDF_PREUSE 1  // 1: per-level Zc row reuse (rows 0-3 / 4-7 separately); 0: all 8 rows or none
 #endif
@@ -228,9 +231,19 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
     };
 
     const int64_t c0 = (int64_t)blockIdx.x * chunk;
-    const int64_t c1 = min(n, c0 + chunk);
     float4 zc[NV][8];
+#if PNDF_WSEG
+    // each warp walks its own contiguous segment of the CTA's range, so the rows of one batch's last
+    // query can be reused by the next batch's first
+    const int64_t wlen = (((chunk + kWarpsPerBlock - 1) / kWarpsPerBlock) + 31) / 32 * 32;
+    const int64_t ws = c0 + (int64_t)warp * wlen;
+    const int64_t c1 = min(min(n, c0 + chunk), ws + wlen);
+    int32_t prev_lo = -1, prev_hi = -1;
+    for (int64_t base = ws; base < c1; base += 32) {
+#else
+    const int64_t c1 = min(n, c0 + chunk);
     for (int64_t base = c0 + (int64_t)warp * 32; base < c1; base += (int64_t)kWarpsPerBlock * 32) {
+#endif
         // 1. decode 32 records, one per lane
         {
             const int64_t qi = base + lane;
@@ -257,9 +270,20 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
             // repeats (same l0 cell -> rows 0-3, same l0+1 cell -> rows 4-7)
             const bool kv = key != 0xffffffffu;
             const int32_t klo = kv ? wd[lane].row[0] : -1, khi = kv ? wd[lane].row[4] : -1;
-            const int32_t plo = __shfl_up_sync(0xffffffffu, klo, 1), phi = __shfl_up_sync(0xffffffffu, khi, 1);
-            const uint32_t same_lo = __ballot_sync(0xffffffffu, lane > 0 && kv && klo == plo);
-            const uint32_t same_hi = __ballot_sync(0xffffffffu, lane > 0 && kv && khi == phi);
+            int32_t plo = __shfl_up_sync(0xffffffffu, klo, 1), phi = __shfl_up_sync(0xffffffffu, khi, 1);
+#if PNDF_WSEG
+            if (lane == 0) {  // the previous batch's last query (its rows are still in zc)
+                plo = prev_lo;
+                phi = prev_hi;
+            }
+            prev_lo = __shfl_sync(0xffffffffu, klo, 31);
+            prev_hi = __shfl_sync(0xffffffffu, khi, 31);
+            const bool first_ok = true;
+#else
+            const bool first_ok = lane > 0;
+#endif
+            const uint32_t same_lo = __ballot_sync(0xffffffffu, first_ok && kv && klo == plo);
+            const uint32_t same_hi = __ballot_sync(0xffffffffu, first_ok && kv && khi == phi);
             if (lane == 0) {
                 sreuse[2 * warp] = same_lo;
                 sreuse[2 * warp + 1] = same_hi;
@@ -328,8 +352,8 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 // warp-uniform for G == 32 (every lane reads the same descriptor)
                 // warp-uniform for G == 32: level l0's rows (0-3) and level l0+1's rows (4-7) are
                 // re-read only when they differ from the previous query's
-                const bool reuse0 = (G == 32) && s > 0 && ((reuse_lo >> s) & 1u);
-                const bool reuse1 = (G == 32) && s > 0 && ((reuse_hi >> s) & 1u);
+                const bool reuse0 = (G == 32) && (PNDF_WSEG || s > 0) && ((reuse_lo >> s) & 1u);
+                const bool reuse1 = (G == 32) && (PNDF_WSEG || s > 0) && ((reuse_hi >> s) & 1u);
                 if (!PNDF_NOREUSE && !reuse0) {
                     const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
                     const int row[4] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w};
