@@ -18,7 +18,10 @@
 namespace pndf {
 
 constexpr int kMaxLevels = 24;
-constexpr int kThreads = 256;  // query-kernel block size
+#ifndef PNDF_QTHREADS
+#define PNDF_QTHREADS 256
+#endif
+constexpr int kThreads = PNDF_QTHREADS;  // query-kernel block size
 
 struct QParams {
     const float* Zc;
