@@ -67,50 +67,53 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
                 const int l = l0 + dl;
                 const float wl = dl ? t : 1.f - t;
                 const int sh = __ffs(p.n0 >> l) - 1;  // log2 n_l
-                const int64_t nl = (int64_t)1 << sh, ne = nl + 2 * M;
-                int64_t off = 0;
+                // 32-bit index math: world cells |i| <= 2^22, tile rows < 2^31 (the 64-bit products
+                // were a third of the kernel's instructions)
+                const int nl = 1 << sh, ne = nl + 2 * M;
+                int off = 0;
                 for (int m = 0; m < l; ++m) {
-                    const int64_t e2 = (int64_t)(p.n0 >> m) + 2 * M;
+                    const int e2 = (p.n0 >> m) + 2 * M;
                     off += e2 * e2;
                 }
                 const float inv_s = __int_as_float(__float_as_int(p.inv_s0) - (l << 23));
                 const float fu = fmaf(rec.u, inv_s, -0.5f), fv = fmaf(rec.v, inv_s, -0.5f);
                 const float flu = floorf(fu), flv = floorf(fv);
                 const float a = fu - flu, b = fv - flv;
-                const int64_t iu = (int64_t)flu, iv = (int64_t)flv;
+                const int iu = (int)flu, iv = (int)flv;
                 const float wa = wl * (1.f - a), wb = wl * a;
                 const float wk4[4] = {wa * (1.f - b), wb * (1.f - b), wa * b, wb * b};
                 // candidate tiles of all 4 neighbours lie in one small box: hash each cell once
-                const int64_t MB = M < 2 ? M : 2;
-                const int64_t bx0 = (iu - (nl + MB) + 1) >> sh, bx1 = (iu + 1 + MB) >> sh;
-                const int64_t by0 = (iv - (nl + MB) + 1) >> sh, by1 = (iv + 1 + MB) >> sh;
-                const int bw = (int)(bx1 - bx0 + 1);
-                const int nc = bw * (int)(by1 - by0 + 1);
+                const int MA = M < 2 ? M : 2;
+                const int bx0 = (iu - (nl + MA) + 1) >> sh, bx1 = (iu + 1 + MA) >> sh;
+                const int by0 = (iv - (nl + MA) + 1) >> sh, by1 = (iv + 1 + MA) >> sh;
+                const int bw = bx1 - bx0 + 1;
+                const int nc = bw * (by1 - by0 + 1);
                 const bool boxed = nc <= TBOX;  // group-uniform
                 __syncwarp(gmask);              // the previous level's readers are done
                 if (boxed)
                     for (int c = gl; c < nc; c += G) my_tiles[c] = tile_of(seed_mixed, bx0 + c % bw, by0 + c / bw);
                 __syncwarp(gmask);
+                const int base_rows = off + M * ne + M;  // (jl + M) ne + (il + M) = jl ne + il + base
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    const int64_t iw = iu + (k & 1), jw = iv + (k >> 1);
+                    const int iw = iu + (k & 1), jw = iv + (k >> 1);
                     const float wk = wk4[k];
                     // tiles whose texels this centre's footprint reaches: local cell il in [-2, nl + 1]
                     // (support +-4 sigma = +-1.73 cells around the centre at (il + 1/2) cells); rows
                     // further out in the extended grid are zero and skipped (exact: they add +0)
-                    const int64_t MA = M < 2 ? M : 2;
-                    const int64_t tx0 = (iw - (nl + MA) + 1) >> sh, tx1 = (iw + MA) >> sh;
-                    const int64_t ty0 = (jw - (nl + MA) + 1) >> sh, ty1 = (jw + MA) >> sh;
-                    for (int64_t ty = ty0; ty <= ty1; ++ty)
-                        for (int64_t tx = tx0; tx <= tx1; ++tx) {
-                            const int64_t il = iw - (tx << sh), jl = jw - (ty << sh);
+                    const int tx0 = (iw - (nl + MA) + 1) >> sh, tx1 = (iw + MA) >> sh;
+                    const int ty0 = (jw - (nl + MA) + 1) >> sh, ty1 = (jw + MA) >> sh;
+                    for (int ty = ty0; ty <= ty1; ++ty)
+                        for (int tx = tx0; tx <= tx1; ++tx) {
+                            const int il = iw - (tx << sh), jl = jw - (ty << sh);
                             if (il < -MA || il >= nl + MA || jl < -MA || jl >= nl + MA) continue;
-                            const int tile = boxed ? my_tiles[(int)(ty - by0) * bw + (int)(tx - bx0)]
+                            const int tile = boxed ? my_tiles[(ty - by0) * bw + (tx - bx0)]
                                                    : tile_of(seed_mixed, tx, ty);
-                            const int64_t row = (int64_t)tile * tp.p_ext + off + (jl + M) * ne + (il + M);
+                            const int row = tile * (int)tp.p_ext + base_rows + jl * ne + il;
+                            const float* zr0 = p.Zc + (size_t)row * RP + gl * 4;
 #pragma unroll
                             for (int v = 0; v < NV; ++v) {
-                                const float4 zr = ldg4(p.Zc + (size_t)row * RP + (gl + v * G) * 4);
+                                const float4 zr = ldg4(zr0 + v * G * 4);
                                 zh[v].x = fmaf(wk, zr.x, zh[v].x);
                                 zh[v].y = fmaf(wk, zr.y, zh[v].y);
                                 zh[v].z = fmaf(wk, zr.z, zh[v].z);
