@@ -91,27 +91,29 @@ __global__ void __launch_bounds__(256) blocked_query_kernel(const QParams p, con
                 float a, b;
                 axis_cells<WRAP>(p, rec.u, l, i0, i1, a);
                 axis_cells<WRAP>(p, rec.v, l, j0, j1, b);
-                const int64_t nl = p.n0 >> l;
+                const int nl = p.n0 >> l;
                 const int lsh = __ffs(p.N / p.n0) - 1 + l;  // log2(s0 * 2^l)
-                const int64_t off = level_offset(p.n0, l);
+                const int off = (int)level_offset(p.n0, l);  // 32-bit row math: P < 2^31
                 const float wa = wl * (1.f - a), wb = wl * a;
                 const float wk4[4] = {wa * (1.f - b), wb * (1.f - b), wa * b, wb * b};
                 for (int k = 0; k < 4; ++k) {
                     const float wk = wk4[k];
                     if (wk == 0.f) continue;  // group-uniform
-                    const int64_t i = (k & 1) ? i1 : i0, j = (k >> 1) ? j1 : j0;
-                    const int64_t z = off + j * nl + i;
+                    const int i = (k & 1) ? i1 : i0, j = (k >> 1) ? j1 : j0;
+                    const int z = off + j * nl + i;
                     // region of the centre ((i+1/2)s, (j+1/2)s) = floor((2i+1) s / (2 region)); s and region
                     // are powers of two, so a shift (a 64-bit division here costs ~70 instructions)
                     const int rsh = lsh - 1 - bp.r_shift;
-                    const int64_t reg = (rsh >= 0 ? ((2 * j + 1) << rsh) : ((2 * j + 1) >> -rsh)) * bp.nr +
-                                        (rsh >= 0 ? ((2 * i + 1) << rsh) : ((2 * i + 1) >> -rsh));
+                    const int reg = (rsh >= 0 ? ((2 * j + 1) << rsh) : ((2 * j + 1) >> -rsh)) * bp.nr +
+                                    (rsh >= 0 ? ((2 * i + 1) << rsh) : ((2 * i + 1) >> -rsh));
+                    const int32_t* __restrict__ slab_row = bp.slab_ptr + (int64_t)z * nb2;
+                    const int32_t* __restrict__ set_row = bp.group_set + (int64_t)reg * nb2;
                     for (int byb = by0; byb <= by1; ++byb)
                         for (int bxb = bx0; bxb <= bx1; ++bxb) {
                             const int blk = byb * nb + bxb;
-                            const int32_t slab = __ldg(bp.slab_ptr + z * nb2 + blk);
+                            const int32_t slab = __ldg(slab_row + blk);
                             if (slab < 0) continue;  // blank block
-                            const int32_t set = __ldg(bp.group_set + reg * nb2 + blk);
+                            const int32_t set = __ldg(set_row + blk);
                             if (set < 0) continue;
                             const int lx1 = max(x1, bxb * t) - bxb * t, lx2 = min(x2, bxb * t + t - 1) - bxb * t;
                             const int ly1 = max(y1, byb * t) - byb * t, ly2 = min(y2, byb * t + t - 1) - byb * t;
