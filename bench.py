@@ -241,7 +241,7 @@ def spatial_shard(cfg, bins, n_total: int, rank: int, world: int):
         recs = synth.gen_queries(cfg, bins, a, min(n_total, a + chunk))
         keep.append(recs[spatial_owner(recs["u"], cfg.N, world) == rank])
     mine = np.concatenate(keep) if keep else np.empty(0, synth.QREC)
-    h_q = torch.empty((mine.shape[0], 4), dtype=torch.int32, pin_memory=True)
+    h_q = torch.empty((mine.shape[0], 4), dtype=torch.int32, pin_memory=torch.cuda.is_available())
     h_q.numpy().view(synth.QREC).reshape(-1)[:] = mine
     return h_q
 

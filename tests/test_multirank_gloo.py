@@ -87,3 +87,27 @@ def test_spatial_owner_partitions_the_stream():
     # strips: owner is monotone in u and wraps
     u = np.array([0.0, 511.99, 512.0, 4095.99, 4096.0, -1.0])
     assert spatial_owner(u, 4096, 8).tolist() == [0, 0, 1, 7, 0, 7]
+
+
+def test_bench_spatial_shards_cover_the_stream_exactly():
+    """bench.py's spatial shards of a W-rank job: disjoint, in stream order, and together exactly the
+    stream (every query answered once), for W = 2 and 3."""
+    import sys
+    import os
+    import synth
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import bench
+    cfg = synth.CONFIGS[2]
+    n = 50_000
+    bins = synth.bin_map(cfg, synth.make_map(cfg))
+    full = synth.gen_queries(cfg, bins, 0, n)
+    for w in (2, 3):
+        parts = [bench.spatial_shard(cfg, bins, n, r, w).numpy().view(synth.QREC).reshape(-1) for r in range(w)]
+        assert sum(p.shape[0] for p in parts) == n
+        merged = np.concatenate(parts)
+        key = lambda a: np.sort(a.view(np.dtype((np.void, 16))))  # noqa: E731
+        assert np.array_equal(key(merged), key(full))
+        for r, p in enumerate(parts):  # stream order kept inside a shard, and every record in its strip
+            pos = np.flatnonzero(np.isin(full.view(np.dtype((np.void, 16))), p.view(np.dtype((np.void, 16)))))
+            assert np.all(np.diff(pos) > 0)
+            assert (np.minimum((p["u"] * w / cfg.N).astype(int), w - 1) == r).all()
