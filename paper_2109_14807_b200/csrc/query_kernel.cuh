@@ -354,7 +354,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 // re-read only when they differ from the previous query's
                 const bool reuse0 = (G == 32) && (PNDF_WSEG || s > 0) && ((reuse_lo >> s) & 1u);
                 const bool reuse1 = (G == 32) && (PNDF_WSEG || s > 0) && ((reuse_hi >> s) & 1u);
-                if (!PNDF_NOREUSE && !reuse0) {
+                // outer warp-uniform branch: a fully reused step (the common binned case) skips the
+                // whole load block instead of issuing it predicated off
+                if (__builtin_expect(!PNDF_NOREUSE && !(reuse0 && reuse1), 0)) {
+                if (!reuse0) {
                     const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
                     const int row[4] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w};
 #pragma unroll
@@ -362,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 #pragma unroll
                         for (int k = 0; k < 4; ++k) zc[v][k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
                 }
-                if (!PNDF_NOREUSE && !reuse1) {
+                if (!reuse1) {
                     const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
                     const int row[4] = {(int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
 #pragma unroll
@@ -370,6 +373,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
 #pragma unroll
                         for (int k = 0; k < 4; ++k)
                             zc[v][4 + k] = ldg4_stream(Zc + (size_t)row[k] * RP + (gl + v * G) * 4);
+                }
                 }
                 float acc = 0.f;
                 float2 acc2 = make_float2(0.f, 0.f);
