@@ -94,7 +94,7 @@ typedef struct {
  * stored either as an fp32 (hi, lo) pair [2][(A+1)][2][Rp] (HILO, M_r = C_r) or as
  * uint32 fixed point [2][(A+1)][Rp] with per-rank scale 2^e_r folded into
  * M_r = C_r 2^-(ex_r + ey_r) (U32); see the PNDF_PREFIX_* flags.  A range table
- * DT[2][A][W][Rp] fp32 (W = min(16, A)) holds, for every range of at most W bins, the
+ * DT[2][A][W][Rp] fp32 (W = min(48, A)) holds, for every range of at most W bins, the
  * prefix difference exactly as the kernel computes it from the SATs, so a narrow range
  * costs one look-up per axis instead of two with bit-identical results.
  * Every factor must be finite and >= 0 (nonnegative store), else PNDF_EINVAL.

@@ -14,6 +14,9 @@
 
 #include "internal.cuh"
 
+#ifndef PNDF_DTW
+#define PNDF_DTW 48  // widest range (bins) served by the range table (SG rectangles reach ~40)
+#endif
 #ifndef PNDF_DTAB
 #define PNDF_DTAB 1  // build the small-range difference table (query_kernel: one load per axis and rank chunk)
 #endif
@@ -682,7 +685,7 @@ static pndf_status load_impl(const pndf_desc* desc, int64_t P_override, const fl
     p.dt_w = 0;
 #if PNDF_DTAB
     {  // range table for rectangles of side <= W (2 A W Rp floats; 8.4 MB for config 5)
-        const int W = std::min(16, A);
+        const int W = std::min(PNDF_DTW, A);
         if (cudaMalloc(&s->DT, sizeof(float) * (size_t)2 * A * W * Rp) == cudaSuccess &&
             launch_range_table(s->PXY, A, Rp, use_u32 ? 1 : 0, W, s->DT, st) == cudaSuccess &&
             cudaStreamSynchronize(st) == cudaSuccess) {

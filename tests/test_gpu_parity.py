@@ -355,10 +355,10 @@ def test_binning_sorts_by_half_cell_key(k):
 
 @pytest.mark.parametrize("prefix", [2, 4])
 def test_range_table_widths(prefix):
-    """Narrow ranges (<= W = 16 bins) read the range table DT, wider ones the two SAT rows: every
+    """Narrow ranges (<= W = 48 bins) read the range table DT, wider ones the two SAT rows: every
     width 1..A on each axis, both SAT formats, against the oracle."""
     from paper_2109_14807_b200 import pndf
-    N, s0, L, A, R = 32, 1, 6, 40, 12
+    N, s0, L, A, R = 32, 1, 6, 64, 12
     P = sum((N >> l) ** 2 for l in range(L))
     f = synth.random_factors(A, R, P, seed=17, sparsity=0.3)
     rng = np.random.default_rng(18)
@@ -372,7 +372,7 @@ def test_range_table_widths(prefix):
     d = pndf.make_desc(N, s0, L, A, R, True, prefix=prefix)
     st = pndf.load_factors(d, f.C, f.X, f.Y, f.Z)
     s = st.stats()
-    assert s["range_table_width"] == 16 and s["range_table_bytes"] == 4 * 2 * A * 16 * s["rank_padded"]
+    assert s["range_table_width"] == 48 and s["range_table_bytes"] == 4 * 2 * A * 48 * s["rank_padded"]
     out = torch.empty(n, dtype=torch.float32, device="cuda")
     st.query_batch(torch_records(recs), out, 0)
     st.sync()

@@ -1,9 +1,10 @@
 #!/bin/bash
-# per-GPU cost of the 2/4/8-GPU config-5 jobs on one GPU: shard 0 of W, spatial vs index sharding
 mkdir -p gpurun_out
-for w in 2 4 8; do
-  for sh in spatial index; do
-    timeout 900 python bench.py --as-shard 0/$w --shard $sh --no-e2e --no-cpu-baseline > gpurun_out/as_${sh}_$w.log 2>&1
-    echo "W=$w $sh $(grep -o '"value": [0-9.e+]*' gpurun_out/as_${sh}_$w.log | head -1) $(grep -o '"ms_per_step": [0-9.e+]*' gpurun_out/as_${sh}_$w.log | head -1) $(grep -o '"queries_per_rank": [0-9]*' gpurun_out/as_${sh}_$w.log | head -1) $(grep -o '"pass": [a-z]*' gpurun_out/as_${sh}_$w.log | head -1)" >> gpurun_out/as.txt
+for rep in 1 2; do
+  for v in libpndf libpndf_w48; do
+    PNDF_LIB=paper_2109_14807_b200/$v.so timeout 600 python bench.py --no-e2e --no-cpu-baseline > gpurun_out/ab_${v}_5_$rep.log 2>&1
+    echo "c5 $v $rep $(grep -o '"value": [0-9.e+]*' gpurun_out/ab_${v}_5_$rep.log | head -1)" >> gpurun_out/ab.txt
+    PNDF_LIB=paper_2109_14807_b200/$v.so timeout 600 python bench.py --op sg --no-cpu-baseline > gpurun_out/ab_${v}_sg_$rep.log 2>&1
+    echo "sg $v $rep $(grep -o '"value": [0-9.e+]*' gpurun_out/ab_${v}_sg_$rep.log | head -1) $(grep -o '"pass": [a-z]*' gpurun_out/ab_${v}_sg_$rep.log | head -1)" >> gpurun_out/ab.txt
   done
 done
