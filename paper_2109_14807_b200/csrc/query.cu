@@ -176,13 +176,18 @@ __global__ void __launch_bounds__(kRsThreads) rs_hist_kernel(const uint32_t* __r
     for (int d = threadIdx.x; d < RADIX; d += kRsThreads) counts[(int64_t)d * ntiles + blockIdx.x] = h[d];
 }
 
-// Stable scatter of one tile.  Item order inside the tile is round-major
-// (item i*256 + t belongs to thread t in round i); an item's rank among equal
-// digits = earlier rounds + earlier warps of its round + lower lanes of its warp.
-// The tile is staged in shared memory in digit order, then written out so that
-// consecutive items of a digit run go to consecutive global addresses.
+// Stable scatter of one tile.  Warp w owns the contiguous segment
+// [w*IPW, (w+1)*IPW) of the tile (IPW = 512 items, read 32 at a time, so the
+// global loads stay coalesced).  Each warp ranks its segment against its own
+// digit counters in shared memory (match_any + popc, rounds in order), so the
+// ranking needs no block barrier; one scan over (digit, warp) afterwards turns
+// the per-warp counts into offsets.  An item's tile-local position is
+//   start[d] + (items of digit d in earlier warps) + (its rank inside its warp),
+// which keeps the sort stable.  The tile is staged in shared memory in digit
+// order, then written out so that consecutive items of a digit run go to
+// consecutive global addresses.
 template <int BITS>
-__global__ void __launch_bounds__(kRsThreads) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(kRsThreads, 3) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in, int64_t n,
                                                                 int shift, const uint32_t* __restrict__ offsets,
                                                                 int64_t ntiles, uint32_t* keys_out,
@@ -190,22 +195,24 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter_kernel(const uint32_t* 
     constexpr int RADIX = 1 << BITS;
     constexpr int DPT = RADIX / kRsThreads;  // digits owned per thread
     constexpr int DPL = RADIX / 32;          // digits per lane in the tile scan
+    constexpr int IPW = kRsTile / kRsWarps;  // items per warp segment
     extern __shared__ uint32_t rs_smem[];  // rs_smem_bytes<BITS>() of dynamic shared memory
     uint32_t* s_keys = rs_smem;                                      // [kRsTile]
     uint32_t* s_vals = s_keys + kRsTile;                             // [kRsTile]
     uint32_t(*s_cnt)[RADIX] = reinterpret_cast<uint32_t(*)[RADIX]>(s_vals + kRsTile);  // [kRsWarps][RADIX]
-    uint32_t* s_run = s_vals + kRsTile + kRsWarps * RADIX;  // tile histogram, then items placed so far
+    uint32_t* s_run = s_vals + kRsTile + kRsWarps * RADIX;  // tile histogram
     uint32_t* s_start = s_run + RADIX;                      // tile-local start of each digit run
-    uint32_t* s_goff = s_start + RADIX;                     // global start of this tile's digit run
+    uint32_t* s_goff = s_start + RADIX;                     // global start minus tile-local start
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
     const int nt = (int)((n - t0) < (int64_t)kRsTile ? (n - t0) : (int64_t)kRsTile);
+    const int seg = warp * IPW + lane;  // tile-local index of item 0 of this lane
 
     uint32_t k[kRsItems], v[kRsItems];
 #pragma unroll
     for (int i = 0; i < kRsItems; ++i) {
-        const int64_t g = t0 + (int64_t)i * kRsThreads + t;
-        const bool ok = g < n;
+        const int64_t g = t0 + seg + i * 32;
+        const bool ok = seg + i * 32 < nt;
         k[i] = ok ? __ldg(keys_in + g) : 0xffffffffu;
         v[i] = ok ? (vals_in ? __ldg(vals_in + g) : (uint32_t)g) : 0u;
     }
@@ -214,13 +221,37 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter_kernel(const uint32_t* 
         const int d = t + j * kRsThreads;
 #pragma unroll
         for (int w = 0; w < kRsWarps; ++w) s_cnt[w][d] = 0;
-        s_run[d] = 0;
-        s_goff[d] = offsets[(int64_t)d * ntiles + blockIdx.x];
+    }
+    __syncthreads();
+    // warp-private stable ranking: r[i] = items of the same digit earlier in this warp's segment
+    uint32_t r[kRsItems / 2];  // two 16-bit ranks per register (a rank is < IPW)
+    const uint32_t lt_mask = (1u << lane) - 1u;
+#pragma unroll
+    for (int i = 0; i < kRsItems; ++i) {
+        const bool ok = seg + i * 32 < nt;
+        const uint32_t d = (k[i] >> shift) & (RADIX - 1);
+        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : 0xffffffffu);
+        const uint32_t lt = peers & lt_mask;
+        const uint32_t base = ok ? s_cnt[warp][d] : 0u;
+        const uint32_t ri = base + __popc(lt);
+        r[i >> 1] = (i & 1) ? (r[i >> 1] | (ri << 16)) : ri;
+        __syncwarp();
+        if (ok && lt == 0) s_cnt[warp][d] = base + __popc(peers);
+        __syncwarp();
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i)
-        if (i * kRsThreads + t < nt) atomicAdd(&s_run[(k[i] >> shift) & (RADIX - 1)], 1u);
+    for (int j = 0; j < DPT; ++j) {  // thread t owns digits t + j*256: exclusive offsets over the warps
+        const int dd = t + j * kRsThreads;
+        uint32_t acc = 0;
+#pragma unroll
+        for (int w = 0; w < kRsWarps; ++w) {
+            const uint32_t c = s_cnt[w][dd];
+            s_cnt[w][dd] = acc;
+            acc += c;
+        }
+        s_run[dd] = acc;
+    }
     __syncthreads();
     if (warp == 0) {  // exclusive scan of the tile histogram, DPL digits per lane
         uint32_t c[DPL], sum = 0;
@@ -238,53 +269,27 @@ __global__ void __launch_bounds__(kRsThreads) rs_scatter_kernel(const uint32_t* 
         uint32_t acc = incl - sum;
 #pragma unroll
         for (int j = 0; j < DPL; ++j) {
-            s_start[lane * DPL + j] = acc;
+            const int d = lane * DPL + j;
+            s_start[d] = acc;
+            s_goff[d] = offsets[(int64_t)d * ntiles + blockIdx.x] - acc;
             acc += c[j];
         }
     }
     __syncthreads();
 #pragma unroll
-    for (int j = 0; j < DPT; ++j) s_run[t + j * kRsThreads] = 0;
-    __syncthreads();
-    // stable ranking, one round (256 items) at a time (unrolled: k[], v[] stay in registers)
-#pragma unroll
     for (int i = 0; i < kRsItems; ++i) {
-        const bool ok = i * kRsThreads + t < nt;
-        const uint32_t d = (k[i] >> shift) & (RADIX - 1);
-        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : 0xffffffffu);
-        const uint32_t lt = peers & ((1u << lane) - 1u);
-        const uint32_t rank = __popc(lt);
-        if (ok && lt == 0) s_cnt[warp][d] = __popc(peers);
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < DPT; ++j) {  // thread t owns digits t + j*256: offsets over this round's warps
-            const int dd = t + j * kRsThreads;
-            uint32_t acc = s_run[dd];
-#pragma unroll
-            for (int w = 0; w < kRsWarps; ++w) {
-                const uint32_t c = s_cnt[w][dd];
-                s_cnt[w][dd] = acc;
-                acc += c;
-            }
-            s_run[dd] = acc;
-        }
-        __syncthreads();
-        if (ok) {
-            const uint32_t pos = s_start[d] + s_cnt[warp][d] + rank;
+        if (seg + i * 32 < nt) {
+            const uint32_t d = (k[i] >> shift) & (RADIX - 1);
+            const uint32_t pos = s_start[d] + s_cnt[warp][d] + ((r[i >> 1] >> ((i & 1) * 16)) & 0xffffu);
             s_keys[pos] = k[i];
             s_vals[pos] = v[i];
         }
-        __syncthreads();
-#pragma unroll
-        for (int j = 0; j < DPT; ++j)
-#pragma unroll
-            for (int w = 0; w < kRsWarps; ++w) s_cnt[w][t + j * kRsThreads] = 0;
-        __syncthreads();
     }
+    __syncthreads();
     for (int j = t; j < nt; j += kRsThreads) {
         const uint32_t key = s_keys[j];
         const uint32_t d = (key >> shift) & (RADIX - 1);
-        const uint32_t pos = s_goff[d] + (uint32_t)j - s_start[d];
+        const uint32_t pos = s_goff[d] + (uint32_t)j;
         keys_out[pos] = key;
         vals_out[pos] = s_vals[j];
     }
