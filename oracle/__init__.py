@@ -66,6 +66,8 @@ def lib():
         L.oracle_tile_id.restype = ctypes.c_int
         L.oracle_tile_id.argtypes = [ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64]
         L.oracle_tiled_query_batch.argtypes = [ctypes.POINTER(TilesDesc), P, P, P, P, P, ctypes.c_int64, ctypes.c_int, P]
+        L.oracle_tiled_sample_batch.argtypes = [ctypes.POINTER(TilesDesc), P, P, P, P, P, P, ctypes.c_int64, P, P, P,
+                                                P, P, P, P, P, P]
         L.oracle_blocked_query_batch.argtypes = [ctypes.POINTER(BlockedDesc), P, P, P, P, P, P, P, ctypes.c_int64,
                                                  ctypes.c_int, P]
         L.oracle_max_threads.restype = ctypes.c_int
@@ -165,6 +167,37 @@ def tiled_query_batch(td: TilesDesc, C, X, Y, Z, records: np.ndarray, mean: bool
     lib().oracle_tiled_query_batch(ctypes.byref(td), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(recs),
                                    recs.shape[0], 1 if mean else 0, _ptr(out))
     return out
+
+
+def tiled_sample_batch(td: TilesDesc, C, X, Y, Z, records: np.ndarray, xi: np.ndarray):
+    """Importance sampling over implicit Wang tiles (Sec. 5.5), fp64: one covered tile instance
+    chosen with equal probability (xi[:, 10]), the hierarchical descent of sample_batch on its partial
+    NDF (xi[:, 0:8], jitter xi[:, 8:10]), pdf from the full NDF.  Returns dict of pixel int32 [n, 2]
+    (-1 = none), prob (full pixel mass / full domain mass), prob_tile (the chosen tile's pmf), h,
+    margin, tile int64 [n, 2] (tx, ty), count int32 [n] (covered instances), mass_tile / mass_all (domain
+    mass of the chosen tile's partial NDF / of the full NDF)."""
+    C = np.ascontiguousarray(C, np.float32)
+    X = np.ascontiguousarray(X, np.float32)
+    Y = np.ascontiguousarray(Y, np.float32)
+    Z = np.ascontiguousarray(Z, np.float32)
+    recs = np.ascontiguousarray(records)
+    xi = np.ascontiguousarray(xi, np.float32)
+    n = recs.shape[0]
+    assert xi.shape == (n, 11)
+    pix = np.empty((n, 2), np.int32)
+    prob = np.empty(n, np.float64)
+    prob_t = np.empty(n, np.float64)
+    h = np.empty((n, 2), np.float64)
+    mg = np.empty(n, np.float64)
+    tile = np.empty((n, 2), np.int64)
+    cnt = np.empty(n, np.int32)
+    mt = np.empty(n, np.float64)
+    ma = np.empty(n, np.float64)
+    lib().oracle_tiled_sample_batch(ctypes.byref(td), _ptr(C), _ptr(X), _ptr(Y), _ptr(Z), _ptr(recs), _ptr(xi), n,
+                                    _ptr(pix), _ptr(prob), _ptr(prob_t), _ptr(h), _ptr(mg), _ptr(tile), _ptr(cnt),
+                                    _ptr(mt), _ptr(ma))
+    return dict(pixel=pix, prob=prob, prob_tile=prob_t, h=h, margin=mg, tile=tile, count=cnt, mass_tile=mt,
+                mass_all=ma)
 
 
 def blocked_query_batch(cfg, bs, records: np.ndarray, mean: bool = True) -> np.ndarray:

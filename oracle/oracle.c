@@ -466,6 +466,191 @@ typedef struct {
     int32_t N, s0, L, A, t, region, R, wrap;
 } oracle_blocked;
 
+/* ------------------------------------------------------------------------
+ * Importance sampling over implicit Wang tiles (Sec. 5.5): "we first
+ * choose one Wang tile from all the Wang tiles covered by the pixel footprint
+ * with equal probability.  Then, we sample a direction from the chosen Wang
+ * tile, similar to Sec. 5.2.  After getting the sampled direction, we computed
+ * the NDF value, which is the same as BRDF evaluation.  The PDF is set the
+ * same as NDF value."
+ * Readings (reading 25):
+ *   - a tile instance (world cell (tx, ty)) is covered by the footprint when
+ *     it holds texels of the footprint: its partial NDF has positive mass over
+ *     the whole angular domain, sum_k w_k sum_r C_r (sum_x X_r)(sum_y Y_r) Z_r(z_k)
+ *     > 0 over the rows z_k of the instance that the query reads;
+ *   - the covered instances are ordered by (ty, tx); the chosen one is the
+ *     c-th, c = floor(xi[10] * count) taken in fp32 (a float decision made in
+ *     the same precision as the GPU), clamped to count - 1;
+ *   - "sample a direction from the chosen Wang tile": the hierarchical descent
+ *     of oracle_sample_batch on that instance's partial NDF (its rows only);
+ *   - "the PDF is set the same as NDF value": the full (all-tile) NDF mass of
+ *     the sampled pixel over the full mass of the record's rectangle, i.e. the
+ *     plain sampler's pmf definition evaluated on the combined NDF.
+ * Outputs per sample: pixel (-1 = none), prob (full pixel mass / full domain
+ * mass), prob_tile (the chosen tile's pixel mass / its domain mass), h,
+ * margin (as oracle_sample_batch), tile (tx, ty), count, and the domain masses
+ * of the chosen tile's partial NDF and of the full NDF (for tests).
+ */
+#define TILE_MAX_ROWS 4096
+
+typedef struct { int64_t tx, ty, z; double w; } oracle_tile_row;
+
+/* every (tile instance, row, weight) the query reads with positive weight */
+static int oracle_tile_rows_of(const oracle_tiles* d, const oracle_rec* q, int64_t Pext, oracle_tile_row* rows) {
+    const oracle_desc pd = {d->T, d->s0, d->L, d->A, d->R, 0};
+    int l0, nrow = 0;
+    double t;
+    oracle_level(&pd, (double)q->size, &l0, &t);
+    for (int dl = 0; dl < 2; ++dl) {
+        const int l = l0 + dl;
+        const double wl = dl ? t : 1.0 - t;
+        const int64_t s = (int64_t)d->s0 << l, nn = d->T / s, ne = nn + 2 * d->margin;
+        int64_t off = 0;
+        for (int m = 0; m < l; ++m) {
+            const int64_t e2 = d->T / ((int64_t)d->s0 << m) + 2 * d->margin;
+            off += e2 * e2;
+        }
+        const double fu = (double)q->u / (double)s - 0.5, fv = (double)q->v / (double)s - 0.5;
+        const int64_t iu = (int64_t)floor(fu), iv = (int64_t)floor(fv);
+        const double a = fu - floor(fu), b = fv - floor(fv);
+        for (int k = 0; k < 4; ++k) {
+            const int64_t iw = iu + (k & 1), jw = iv + (k >> 1);
+            const double wk = wl * ((k & 1) ? a : 1.0 - a) * ((k >> 1) ? b : 1.0 - b);
+            if (!(wk > 0.0)) continue;
+            /* brute force over nearby tile instances: every extended grid that holds this centre */
+            const int64_t cx = (int64_t)floor((double)iw / (double)nn), cy = (int64_t)floor((double)jw / (double)nn);
+            const int64_t B = d->margin + 1;
+            for (int64_t ty = cy - B; ty <= cy + B; ++ty)
+                for (int64_t tx = cx - B; tx <= cx + B; ++tx) {
+                    const int64_t il = iw - tx * nn, jl = jw - ty * nn;
+                    if (il < -d->margin || il >= nn + d->margin || jl < -d->margin || jl >= nn + d->margin)
+                        continue;
+                    if (nrow >= TILE_MAX_ROWS) return -1;
+                    const int tile = oracle_tile_id(d->seed, tx, ty);
+                    rows[nrow].tx = tx;
+                    rows[nrow].ty = ty;
+                    rows[nrow].z = (int64_t)tile * Pext + off + (jl + d->margin) * ne + (il + d->margin);
+                    rows[nrow].w = wk;
+                    ++nrow;
+                }
+        }
+    }
+    return nrow;
+}
+
+/* Eq. 6 SUM over [xa, xb) x [ya, yb) of the rows of instance (tx, ty) (all instances if all != 0) */
+static double oracle_tile_rect_sum(const oracle_tiles* d, const float* C, const float* X, const float* Y,
+                                   const float* Z, const oracle_tile_row* rows, int nrow, int all, int64_t tx,
+                                   int64_t ty, int xa, int xb, int ya, int yb, oracle_scratch* sc) {
+    if (xb <= xa || yb <= ya) return 0.0;
+    const int R = d->R;
+    const oracle_desc pd = {d->T, d->s0, d->L, d->A, d->R, 0};
+    for (int r = 0; r < R; ++r) { sc->xs[r] = 0.0; sc->ys[r] = 0.0; }
+    for (int x = xa; x < xb; ++x)
+        for (int r = 0; r < R; ++r) sc->xs[r] += (double)X[(int64_t)x * R + r];
+    for (int y = ya; y < yb; ++y)
+        for (int r = 0; r < R; ++r) sc->ys[r] += (double)Y[(int64_t)y * R + r];
+    double sum = 0.0;
+    for (int k = 0; k < nrow; ++k)
+        if (all || (rows[k].tx == tx && rows[k].ty == ty))
+            sum += rows[k].w * oracle_range_sum(&pd, C, sc->xs, sc->ys, Z + rows[k].z * R);
+    return sum;
+}
+
+EXPORT void oracle_tiled_sample_batch(const oracle_tiles* d, const float* C, const float* X, const float* Y,
+                                      const float* Z, const oracle_rec* q, const float* xi /* [n][11] */, int64_t n,
+                                      int32_t* pixel /* [n][2] */, double* prob, double* prob_tile,
+                                      double* hxy /* [n][2] */, double* margin, int64_t* tile /* [n][2] */,
+                                      int32_t* count, double* mass_tile, double* mass_all) {
+    const int64_t Pext = oracle_tile_rows(d);
+    const oracle_desc pd = {d->T, d->s0, d->L, d->A, d->R, 0};
+#pragma omp parallel
+    {
+        oracle_scratch* sc = (oracle_scratch*)malloc(sizeof(oracle_scratch));
+        oracle_tile_row* rows = (oracle_tile_row*)malloc(sizeof(oracle_tile_row) * TILE_MAX_ROWS);
+#pragma omp for schedule(dynamic, 16)
+        for (int64_t i = 0; i < n; ++i) {
+            int x1, x2, y1, y2;
+            pixel[2 * i] = pixel[2 * i + 1] = -1;
+            prob[i] = prob_tile[i] = NAN;
+            hxy[2 * i] = hxy[2 * i + 1] = NAN;
+            margin[i] = INFINITY;
+            tile[2 * i] = tile[2 * i + 1] = 0;
+            count[i] = 0;
+            mass_tile[i] = mass_all[i] = NAN;
+            if (!oracle_valid(&pd, &q[i], &x1, &x2, &y1, &y2)) continue;
+            const int nrow = oracle_tile_rows_of(d, &q[i], Pext, rows);
+            if (nrow <= 0) continue;
+            /* distinct covered instances (positive full-domain mass), ordered by (ty, tx) */
+            int64_t inst[TILE_MAX_ROWS][2];
+            int ni = 0;
+            for (int k = 0; k < nrow; ++k) {
+                int seen = 0;
+                for (int j = 0; j < ni; ++j) seen |= (inst[j][0] == rows[k].tx && inst[j][1] == rows[k].ty);
+                if (seen) continue;
+                const double m = oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 0, rows[k].tx, rows[k].ty, 0, d->A,
+                                                      0, d->A, sc);
+                if (m > 0.0) { inst[ni][0] = rows[k].tx; inst[ni][1] = rows[k].ty; ++ni; }
+            }
+            if (ni == 0) { prob[i] = prob_tile[i] = 0.0; continue; }
+            for (int a = 1; a < ni; ++a)  /* insertion sort by (ty, tx) */
+                for (int b = a; b > 0 && (inst[b][1] < inst[b - 1][1] ||
+                                          (inst[b][1] == inst[b - 1][1] && inst[b][0] < inst[b - 1][0])); --b) {
+                    int64_t t0 = inst[b][0], t1 = inst[b][1];
+                    inst[b][0] = inst[b - 1][0]; inst[b][1] = inst[b - 1][1];
+                    inst[b - 1][0] = t0; inst[b - 1][1] = t1;
+                }
+            const float cf = xi[11 * i + 10] * (float)ni;  /* fp32 decision (reading 25) */
+            int c = (int)floorf(cf);
+            if (c > ni - 1) c = ni - 1;
+            const int64_t tx = inst[c][0], ty = inst[c][1];
+            tile[2 * i] = tx;
+            tile[2 * i + 1] = ty;
+            count[i] = ni;
+            int xa = x1, xb = x2 + 1, ya = y1, yb = y2 + 1;
+            const double root_all = oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 1, 0, 0, xa, xb, ya, yb, sc);
+            const double root = oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 0, tx, ty, xa, xb, ya, yb, sc);
+            mass_tile[i] = root;
+            mass_all[i] = root_all;
+            if (!(root > 0.0)) { prob[i] = prob_tile[i] = 0.0; continue; }
+            double last = root, mg = INFINITY;
+            for (int l = 0; xb - xa > 1 || yb - ya > 1; ++l) {
+                const int xm = xa + (xb - xa + 1) / 2, ym = ya + (yb - ya + 1) / 2;
+                const double Q[4] = {
+                    oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 0, tx, ty, xa, xm, ya, ym, sc),
+                    oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 0, tx, ty, xm, xb, ya, ym, sc),
+                    oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 0, tx, ty, xa, xm, ym, yb, sc),
+                    oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 0, tx, ty, xm, xb, ym, yb, sc)};
+                const double tot = ((Q[0] + Q[1]) + Q[2]) + Q[3];
+                const double tt = (double)xi[11 * i + l] * tot;
+                double cum = 0.0;
+                int k = -1;
+                for (int j = 0; j < 4; ++j) {
+                    if (Q[j] > 0.0) {
+                        const double dist = fabs(tt - cum) / tot;
+                        if (cum > 0.0 && dist < mg) mg = dist;
+                    }
+                    cum += Q[j];
+                    if (k < 0 && tt < cum) k = j;
+                }
+                if (k < 0) for (int j = 3; j >= 0; --j) if (Q[j] > 0.0) { k = j; break; }
+                if (k & 1) xa = xm; else xb = xm;
+                if (k & 2) ya = ym; else yb = ym;
+                last = Q[k];
+            }
+            pixel[2 * i] = xa;
+            pixel[2 * i + 1] = ya;
+            prob_tile[i] = last / root;
+            prob[i] = oracle_tile_rect_sum(d, C, X, Y, Z, rows, nrow, 1, 0, 0, xa, xb, ya, yb, sc) / root_all;
+            hxy[2 * i] = ((double)xa + (double)xi[11 * i + 8]) * 2.0 / d->A - 1.0;
+            hxy[2 * i + 1] = ((double)ya + (double)xi[11 * i + 9]) * 2.0 / d->A - 1.0;
+            margin[i] = mg;
+        }
+        free(rows);
+        free(sc);
+    }
+}
+
 EXPORT void oracle_blocked_query_batch(const oracle_blocked* d, const float* C, const float* X, const float* Y,
                                        const int32_t* group_set, const int64_t* slab_ptr, const float* Z,
                                        const oracle_rec* q, int64_t n, int mean, double* out) {
