@@ -42,7 +42,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang", "blocked", "als"],
+    ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang", "wang_sample", "blocked", "als"],
                     help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
                          "prefiltering (SG rectangle generation + range query)")
@@ -631,6 +631,7 @@ def run_sg_op(args, cfg, rank, world, local_rank):
 
 
 WANG_METRIC = "Wang-tiled NDF range queries/sec (Sec. 5.5: implicit 16-tile map, 100K^2 texels)"
+WANG_SAMPLE_METRIC = "Wang-tiled NDF importance samples/sec (Sec. 5.5, P:454: equal-probability covered tile + hierarchical descent)"
 
 
 def run_wang_op(args, cfg, rank, world, local_rank):
@@ -660,11 +661,23 @@ def run_wang_op(args, cfg, rank, world, local_rank):
     recs = synth.make_records(rng.uniform(0, tc.world, n), rng.uniform(0, tc.world, n),
                               np.exp2(rng.uniform(0, np.log2(tc.T), n)), x1, x1 + side[:, 0] - 1, y1,
                               y1 + side[:, 1] - 1)
+    sample = args.op == "wang_sample"
+    if sample:  # plain NDF sampling over the whole image (Sec. 5.5)
+        recs["rect"] = synth.pack_rect(0, A - 1, 0, A - 1)
+        xi_h = np.random.default_rng(600 + rank).random((n, 11), dtype=np.float32)
+        d_xi = torch.from_numpy(xi_h).to(dev)
     d_q = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).to(dev)
-    d_out = torch.empty(n, dtype=torch.float32, device=dev)
-    for _ in range(args.warmup):
-        store.query_batch(d_q, d_out, 0)
+    d_out = torch.empty((n, 4) if sample else n, dtype=torch.float32, device=dev)
+
+    def step(opts):
+        if sample:
+            store.sample_tiles(d_q, d_xi, d_out, None, opts)
+        else:
+            store.query_batch(d_q, d_out, opts)
         store.sync()
+
+    for _ in range(args.warmup):
+        step(0)
     store.reset_stats()
     clocks = ClockSampler(bus_id_of(dev))
     clocks.start()
@@ -674,8 +687,7 @@ def run_wang_op(args, cfg, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        store.query_batch(d_q, d_out, pndf.TIMING)
-        store.sync()
+        step(pndf.TIMING)
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -687,30 +699,46 @@ def run_wang_op(args, cfg, rank, world, local_rank):
     if rank != 0:
         store.free()
         return 0
-    idx = np.unique(np.random.default_rng(5).integers(0, n, min(n, 20000)))
     td_o = oracle.TilesDesc(T=tc.T, s0=tc.s0, L=tc.L, margin=tc.margin, A=tc.A, R=tc.R, seed=tc.seed)
-    t0 = time.perf_counter()
-    ref = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, recs[idx])
-    cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
-    got = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
-    err = np.abs(got - ref)
-    line = {"metric": WANG_METRIC, "value": n_total / (ms_step * 1e-3), "unit": "queries/s", "n_gpus": world,
+    if sample:
+        idx = np.unique(np.random.default_rng(5).integers(0, n, min(n, 4000)))
+        t0 = time.perf_counter()
+        ref = oracle.tiled_sample_batch(td_o, f.C, f.X, f.Y, f.Z, recs[idx], xi_h[idx])
+        cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
+        o = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy()
+        pix = o[:, 3].view(np.uint32)
+        firm = (ref["pixel"][:, 0] >= 0) & (ref["margin"] > 1e-4)
+        passed = bool(np.array_equal((pix[firm] & 0xffff).astype(np.int64), ref["pixel"][firm, 0]) and
+                      np.array_equal((pix[firm] >> 16).astype(np.int64), ref["pixel"][firm, 1]) and
+                      np.array_equal(pix == 0xffffffff, ref["pixel"][:, 0] < 0))
+        unit, kern = "samples/s", "pndf::tiled_sample_kernel"
+    else:
+        idx = np.unique(np.random.default_rng(5).integers(0, n, min(n, 20000)))
+        t0 = time.perf_counter()
+        ref = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, recs[idx])
+        cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
+        got = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
+        err = np.abs(got - ref)
+        passed = bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())
+        unit, kern = "queries/s", "pndf::tiled_query_kernel"
+    line = {"metric": WANG_SAMPLE_METRIC if sample else WANG_METRIC, "value": n_total / (ms_step * 1e-3),
+            "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"16 Wang tiles of {tc.T}^2 flakes (spacing {tc.spacing}, alpha {tc.alpha}), "
-                                   f"A={tc.A}, R={tc.R}, margin {tc.margin}, world {tc.world}^2, S log-U[1,{tc.T}]",
+                                   f"A={tc.A}, R={tc.R}, margin {tc.margin}, world {tc.world}^2, S log-U[1,{tc.T}]"
+                                   + (", whole-image sampling domain" if sample else ""),
                        "queries_total": n_total, "rows": int(st["rows"]),
                        "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]]},
             "roofline": {"bound": "hbm", "achieved": None, "peak": measured_peaks()[0]["hbm_gbs"], "unit": "GB/s",
-                         "frac": None, "traffic": None, "kernel": "pndf::tiled_query_kernel",
+                         "frac": None, "traffic": None, "kernel": kern,
                          "kernel_ms": st["query_ms"] / max(1, st["timed_batches"]),
                          "note": "16 tiles' Zc %.0f MB; Zc rows per query grow with the footprint (tiles overlapped)"
                                  % (st["zc_bytes"] / 1e6)},
-            "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
-                             "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
+            "cpu_baseline": {"value": cpu_rate, "unit": unit, "cores": oracle.max_threads(),
+                             "kind": "oracle", "sample": f"{idx.shape[0]} records of the timed batch"},
             "gpu_launches": args.steps, "clocks": clk,
-            "parity_sample": {"checked": int(idx.shape[0]),
-                              "pass": bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())},
+            "parity_sample": {"checked": int(idx.shape[0]), "pass": passed},
             "e2e": None}
     print(json.dumps(line), flush=True)
     store.free()
@@ -928,7 +956,7 @@ def main():
             return run_sample_op(args, cfg, rank, world, local_rank)
         if args.op == "sg":
             return run_sg_op(args, cfg, rank, world, local_rank)
-        if args.op == "wang":
+        if args.op in ("wang", "wang_sample"):
             return run_wang_op(args, cfg, rank, world, local_rank)
         if args.op == "blocked":
             return run_blocked_op(args, cfg, rank, world, local_rank)

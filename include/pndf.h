@@ -224,9 +224,32 @@ typedef struct {
 
 /* Build a tiled store (Z = [16 * P_ext][R], other arguments as pndf_load_factors).
  * pndf_query_batch / pndf_query_batch_host answer world-space queries on it
- * (never binned); pndf_sample_batch returns PNDF_EINVAL for tiled stores. */
+ * (never binned); pndf_sample_batch returns PNDF_EINVAL for tiled stores (use
+ * pndf_sample_tiles). */
 pndf_status pndf_load_tiles(const pndf_tile_desc* desc, const float* C, const float* X, const float* Y,
                             const float* Z, int device, void* cuda_stream, pndf_store* out);
+
+/* Importance sampling over implicit Wang tiles (Sec. 5.5: "we first
+ * choose one Wang tile from all the Wang tiles covered by the pixel footprint
+ * with equal probability.  Then, we sample a direction from the chosen Wang
+ * tile ... The PDF is set the same as NDF value"; reading 25).
+ * s must be a tiled store (else PNDF_EINVAL).  Record i as in pndf_sample_batch
+ * (world footprint; rect = the sampling domain).  The covered tile instances
+ * are the world cells (tx, ty) holding a row the tiled query reads with
+ * positive weight (a neighbour within 2 cells of the tile), ordered by
+ * (ty, tx); the c-th is chosen with c = floor(xi[i][10] * count) (fp32),
+ * then the hierarchical descent of pndf_sample_batch runs on that tile's
+ * partial NDF with xi[i][0..7] and jitters with xi[i][8], xi[i][9].  pdf is
+ * the FULL (all-tile) NDF's mass in the sampled pixel over its mass in the
+ * domain, per unit projected-h area (pmf / (2/A)^2).  No sample (chosen tile
+ * blank on the domain): pixel = 0xffffffff, pdf = 0.
+ *   d_xi   DEVICE [n][11] fp32 in [0,1), caller-supplied
+ *   d_out  DEVICE [n] pndf_sample
+ *   d_tile DEVICE [n][2] int32 (tx, ty) of the chosen instance, or NULL
+ * opts: 0 or PNDF_TIMING (never binned).  Enqueued on cuda_stream; complete
+ * with pndf_sync; invalid records give NaN + the sticky PNDF_EQUERY. */
+pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
+                              pndf_sample* d_out, int32_t* d_tile, uint32_t opts, void* cuda_stream);
 
 /* Blocked / clustered store (Sec. 4.2).  Each
  * A x A NDF image is cut into t x t angular blocks; the blocks of footprints

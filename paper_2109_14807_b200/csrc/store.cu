@@ -769,6 +769,38 @@ pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const f
     return PNDF_OK;
 }
 
+pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
+                              pndf_sample* d_out, int32_t* d_tile, uint32_t opts, void* cuda_stream) {
+    if (!s || n < 0 || (n > 0 && (!d_queries || !d_xi || !d_out))) return PNDF_EINVAL;
+    if (opts & ~PNDF_TIMING) return PNDF_EINVAL;  // tiled batches are never binned
+    if (!s->tiled) return PNDF_EINVAL;
+    if (n == 0) return PNDF_OK;
+    if ((uintptr_t)d_queries % 16 != 0 || (uintptr_t)d_out % 16 != 0 || (uintptr_t)d_xi % 4 != 0 ||
+        (uintptr_t)d_tile % 4 != 0)
+        return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const bool timing = (opts & PNDF_TIMING) != 0;
+    if (timing) {
+        CK(cudaEventRecord(s->ev[0], st));
+        CK(cudaEventRecord(s->ev[1], st));
+    }
+    const int64_t step = int64_t(1) << 30;
+    int launches = 0;
+    for (int64_t a = 0; a < n; a += step) {
+        const int64_t m = std::min(step, n - a);
+        CK(launch_tiled_sample(s->qp, s->tp, s->G, s->NV, d_queries + a, d_xi + (size_t)a * 11, m, d_out + a,
+                               d_tile ? d_tile + 2 * a : nullptr, s->num_sms, st));
+        launches += 1;
+    }
+    if (timing) CK(cudaEventRecord(s->ev[2], st));
+    s->stats.kernel_launches += (uint64_t)launches;
+    s->stats.last_binned = 0;
+    s->timing_pending = timing;
+    return PNDF_OK;
+}
+
 pndf_status pndf_sg_queries(const pndf_sg_light* d_in, int64_t n, float eps, int32_t ang_res, pndf_query* d_out,
                             void* cuda_stream) {
     if (n < 0 || (n > 0 && (!d_in || !d_out))) return PNDF_EINVAL;

@@ -10,6 +10,7 @@
 
 #include "device.cuh"
 #include "launch.h"
+#include "sample_kernel.cuh"
 
 namespace pndf {
 
@@ -169,6 +170,350 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
             }
         }
     }
+}
+
+// Importance sampling over the implicit Wang tiles (Sec. 5.5; DESIGN.md
+// reading 25): "choose one Wang tile from all the Wang tiles covered by the
+// pixel footprint with equal probability", descend on that tile's partial NDF
+// as in sample_kernel (Sec. 5.2), and set the pdf to the full (all-tile) NDF
+// value of the sampled pixel.  A tile instance is covered when its partial
+// NDF has positive mass over the whole angular domain (it holds texels of the
+// footprint).  Pass 1 walks the query's rows once: it accumulates Z-hat of all
+// tiles (pdf) and, per row, the row's full-domain mass sum_r PX[A] PY[A] Zc,
+// setting the instance's bit in a 64-bit mask over the (ty, tx) box of
+// candidate instances (row-major, so bit order = the (ty, tx) order).  The
+// c-th set bit, c = floor(xi[10] * popc(mask)) in fp32, is the chosen tile;
+// pass 2 re-reads only its rows (L1/L2-hot) into Z-hat of the tile.
+template <int G>
+__device__ __forceinline__ float group_sum_m(float v, unsigned gmask) {
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) v += __shfl_xor_sync(gmask, v, o);
+    return v;
+}
+
+template <int G, int NV, bool U32>
+__global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, const TileParams tp,
+                                                           const pndf_query* __restrict__ q,
+                                                           const float* __restrict__ xi, int64_t n,
+                                                           pndf_sample* __restrict__ out,
+                                                           int32_t* __restrict__ tile_out) {
+    constexpr int QPW = 32 / G;
+    constexpr int RP = 4 * G * NV;
+    constexpr int PSTRIDE = U32 ? RP : 2 * RP;
+    constexpr int REACH = 2;  // stored rows reach 2 cells past the tile (+-4 sigma support)
+    const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
+    const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
+    const float* __restrict__ PX = p.PXY;
+    const float* __restrict__ PY = p.PXY + (size_t)(p.A + 1) * PSTRIDE;
+    const uint64_t seed_mixed = tile_mix(tp.seed);
+    const int M = tp.margin;
+    const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t base = gw * QPW; base < n; base += nw * QPW) {  // warp-uniform trip count
+        const int64_t si = base + grp;
+        const bool active = si < n;
+        const pndf_query rec = ldg_query(q + (active ? si : 0));
+        int x1, x2, y1, y2;
+        bool valid = active && record_valid(p, rec, x1, x2, y1, y2);
+        if (!valid) x1 = x2 = y1 = y2 = 0;
+        const float* sxi = xi + (size_t)(active ? si : 0) * 11;
+        int l0;
+        float t;
+        level_select(p, valid ? rec.size : 1.f, l0, t);
+        // per-level geometry; candidate instances: the union box of both levels' reach
+        int iu[2], iv[2], sh[2], offl[2];
+        float fa[2], fb[2], wlv[2];
+        bool use[2];
+        int bx0 = 0x7fffffff, bx1 = -0x7fffffff, by0 = 0x7fffffff, by1 = -0x7fffffff;
+#pragma unroll
+        for (int dl = 0; dl < 2; ++dl) {
+            const int l = l0 + dl;
+            wlv[dl] = dl ? t : 1.f - t;
+            sh[dl] = __ffs(p.n0 >> l) - 1;
+            const float inv_s = __int_as_float(__float_as_int(p.inv_s0) - (l << 23));
+            const float fu = fmaf(valid ? rec.u : 0.f, inv_s, -0.5f), fv = fmaf(valid ? rec.v : 0.f, inv_s, -0.5f);
+            const float flu = floorf(fu), flv = floorf(fv);
+            fa[dl] = fu - flu;
+            fb[dl] = fv - flv;
+            iu[dl] = (int)flu;
+            iv[dl] = (int)flv;
+            use[dl] = valid && wlv[dl] > 0.f;
+            int off = 0;
+            for (int m = 0; m < l; ++m) {
+                const int e2 = (p.n0 >> m) + 2 * M;
+                off += e2 * e2;
+            }
+            offl[dl] = off;
+            if (use[dl]) {
+                bx0 = min(bx0, (iu[dl] - REACH) >> sh[dl]);
+                bx1 = max(bx1, (iu[dl] + REACH + 1) >> sh[dl]);
+                by0 = min(by0, (iv[dl] - REACH) >> sh[dl]);
+                by1 = max(by1, (iv[dl] + REACH + 1) >> sh[dl]);
+            }
+        }
+        const int bw = bx1 - bx0 + 1;
+        if (valid && bw * (by1 - by0 + 1) > 64) valid = false;  // cannot happen for s0 2^l strides; guard
+        // full-domain angular factor sum_x X_r sum_y Y_r (C folded into Zc)
+        float4 full[NV];
+        {
+            SatV<U32> a0, a1, b0, b1;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const int c = (gl + v * G) * 4;
+                a0.load(PX, c, RP);
+                a1.load(PX + (size_t)p.A * PSTRIDE, c, RP);
+                b0.load(PY, c, RP);
+                b1.load(PY + (size_t)p.A * PSTRIDE, c, RP);
+                const float4 dx = SatV<U32>::diff(a0, a1), dy = SatV<U32>::diff(b0, b1);
+                full[v] = make_float4(dx.x * dy.x, dx.y * dy.y, dx.z * dy.z, dx.w * dy.w);
+            }
+        }
+        // pass 1: Z-hat of all tiles + covered-instance mask
+        float4 zt[NV], za[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) zt[v] = za[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+        uint64_t mask = 0;
+#pragma unroll
+        for (int dl = 0; dl < 2; ++dl) {
+            if (!use[dl]) continue;
+            const int s_ = sh[dl], nl = 1 << s_, ne = nl + 2 * M;
+            const int base_rows = offl[dl] + M * ne + M;
+            const float wa = wlv[dl] * (1.f - fa[dl]), wb = wlv[dl] * fa[dl];
+            const float wk4[4] = {wa * (1.f - fb[dl]), wb * (1.f - fb[dl]), wa * fb[dl], wb * fb[dl]};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const float wk = wk4[k];
+                if (!(wk > 0.f)) continue;
+                const int iw = iu[dl] + (k & 1), jw = iv[dl] + (k >> 1);
+                const int tx0 = (iw - REACH) >> s_, tx1 = (iw + REACH) >> s_;
+                const int ty0 = (jw - REACH) >> s_, ty1 = (jw + REACH) >> s_;
+                for (int ty = ty0; ty <= ty1; ++ty)
+                    for (int tx = tx0; tx <= tx1; ++tx) {
+                        const int il = iw - (tx << s_), jl = jw - (ty << s_);
+                        const int tile = tile_of(seed_mixed, tx, ty);
+                        const int row = tile * (int)tp.p_ext + base_rows + jl * ne + il;
+                        const float* zr0 = p.Zc + (size_t)row * RP + gl * 4;
+                        float m = 0.f;
+#pragma unroll
+                        for (int v = 0; v < NV; ++v) {
+                            const float4 zr = ldg4(zr0 + v * G * 4);
+                            za[v].x = fmaf(wk, zr.x, za[v].x);
+                            za[v].y = fmaf(wk, zr.y, za[v].y);
+                            za[v].z = fmaf(wk, zr.z, za[v].z);
+                            za[v].w = fmaf(wk, zr.w, za[v].w);
+                            m = fmaf(full[v].x, zr.x, m);
+                            m = fmaf(full[v].y, zr.y, m);
+                            m = fmaf(full[v].z, zr.z, m);
+                            m = fmaf(full[v].w, zr.w, m);
+                        }
+                        m = group_sum_m<G>(m, gmask);
+                        if (m > 0.f) mask |= 1ull << ((ty - by0) * bw + (tx - bx0));
+                    }
+            }
+        }
+        const int count = __popcll(mask);
+        int ptx = 0, pty = 0;
+        if (count > 0) {
+            int c = (int)floorf(__fmul_rn(__ldg(sxi + 10), (float)count));
+            if (c > count - 1) c = count - 1;
+            uint64_t mm = mask;
+            for (int j = 0; j < c; ++j) mm &= mm - 1;  // drop the c lowest set bits
+            const int bit = __ffsll((long long)mm) - 1;
+            ptx = bx0 + bit % bw;
+            pty = by0 + bit / bw;
+            // pass 2: Z-hat of the chosen tile (its rows only)
+#pragma unroll
+            for (int dl = 0; dl < 2; ++dl) {
+                if (!use[dl]) continue;
+                const int s_ = sh[dl], nl = 1 << s_, ne = nl + 2 * M;
+                const int base_rows = offl[dl] + M * ne + M;
+                const int tile = tile_of(seed_mixed, ptx, pty);
+                const float wa = wlv[dl] * (1.f - fa[dl]), wb = wlv[dl] * fa[dl];
+                const float wk4[4] = {wa * (1.f - fb[dl]), wb * (1.f - fb[dl]), wa * fb[dl], wb * fb[dl]};
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const float wk = wk4[k];
+                    const int il = iu[dl] + (k & 1) - (ptx << s_), jl = iv[dl] + (k >> 1) - (pty << s_);
+                    if (!(wk > 0.f) || il < -REACH || il >= nl + REACH || jl < -REACH || jl >= nl + REACH) continue;
+                    const float* zr0 = p.Zc + (size_t)(tile * (int)tp.p_ext + base_rows + jl * ne + il) * RP + gl * 4;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const float4 zr = ldg4(zr0 + v * G * 4);
+                        zt[v].x = fmaf(wk, zr.x, zt[v].x);
+                        zt[v].y = fmaf(wk, zr.y, zt[v].y);
+                        zt[v].z = fmaf(wk, zr.z, zt[v].z);
+                        zt[v].w = fmaf(wk, zr.w, zt[v].w);
+                    }
+                }
+            }
+        }
+        // SAT values at the current range's corners [xa, xb) x [ya, yb)
+        int xa = x1, xb = x2 + 1, ya = y1, yb = y2 + 1;
+        SatV<U32> sxa[NV], sxb[NV], sya[NV], syb[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int c = (gl + v * G) * 4;
+            sxa[v].load(PX + (size_t)xa * PSTRIDE, c, RP);
+            sxb[v].load(PX + (size_t)xb * PSTRIDE, c, RP);
+            sya[v].load(PY + (size_t)ya * PSTRIDE, c, RP);
+            syb[v].load(PY + (size_t)yb * PSTRIDE, c, RP);
+        }
+        float root = 0.f, root_all = 0.f;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 dx = SatV<U32>::diff(sxa[v], sxb[v]), dy = SatV<U32>::diff(sya[v], syb[v]);
+            const float4 e = make_float4(dx.x * dy.x, dx.y * dy.y, dx.z * dy.z, dx.w * dy.w);
+            root = fmaf(e.x, zt[v].x, root);
+            root = fmaf(e.y, zt[v].y, root);
+            root = fmaf(e.z, zt[v].z, root);
+            root = fmaf(e.w, zt[v].w, root);
+            root_all = fmaf(e.x, za[v].x, root_all);
+            root_all = fmaf(e.y, za[v].y, root_all);
+            root_all = fmaf(e.z, za[v].z, root_all);
+            root_all = fmaf(e.w, za[v].w, root_all);
+        }
+        root = group_sum<G>(root);
+        root_all = group_sum<G>(root_all);
+        const bool live = valid && count > 0 && root > 0.f;
+        int lvl = 0;
+        while (__any_sync(0xffffffffu, live && (xb - xa > 1 || yb - ya > 1))) {
+            const bool go = live && (xb - xa > 1 || yb - ya > 1);
+            const int xm = go && xb - xa > 1 ? xa + (xb - xa + 1) / 2 : xb;
+            const int ym = go && yb - ya > 1 ? ya + (yb - ya + 1) / 2 : yb;
+            SatV<U32> sxm[NV], sym[NV];
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const int c = (gl + v * G) * 4;
+                sxm[v].load(PX + (size_t)xm * PSTRIDE, c, RP);
+                sym[v].load(PY + (size_t)ym * PSTRIDE, c, RP);
+            }
+            float q0 = 0.f, q1 = 0.f, q2 = 0.f, q3 = 0.f;
+#pragma unroll
+            for (int v = 0; v < NV; ++v) {
+                const float4 dxl = SatV<U32>::diff(sxa[v], sxm[v]), dxr = SatV<U32>::diff(sxm[v], sxb[v]);
+                const float4 dyb = SatV<U32>::diff(sya[v], sym[v]), dyt = SatV<U32>::diff(sym[v], syb[v]);
+                const float4 u = make_float4(dyb.x * zt[v].x, dyb.y * zt[v].y, dyb.z * zt[v].z, dyb.w * zt[v].w);
+                const float4 w = make_float4(dyt.x * zt[v].x, dyt.y * zt[v].y, dyt.z * zt[v].z, dyt.w * zt[v].w);
+                q0 = fmaf(dxl.x, u.x, fmaf(dxl.y, u.y, fmaf(dxl.z, u.z, fmaf(dxl.w, u.w, q0))));
+                q1 = fmaf(dxr.x, u.x, fmaf(dxr.y, u.y, fmaf(dxr.z, u.z, fmaf(dxr.w, u.w, q1))));
+                q2 = fmaf(dxl.x, w.x, fmaf(dxl.y, w.y, fmaf(dxl.z, w.z, fmaf(dxl.w, w.w, q2))));
+                q3 = fmaf(dxr.x, w.x, fmaf(dxr.y, w.y, fmaf(dxr.z, w.z, fmaf(dxr.w, w.w, q3))));
+            }
+            quad_reduce<G>(q0, q1, q2, q3, gl, lane);
+            if (go) {
+                const float qs[4] = {q0, q1, q2, q3};
+                const float tot = ((q0 + q1) + q2) + q3;
+                const float tt = __ldg(sxi + lvl) * tot;
+                float c = 0.f;
+                int k = -1;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    c += qs[j];
+                    if (k < 0 && tt < c) k = j;
+                }
+                if (k < 0) k = qs[3] > 0.f ? 3 : (qs[2] > 0.f ? 2 : (qs[1] > 0.f ? 1 : 0));
+                if (k & 1) {
+                    xa = xm;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) sxa[v] = sxm[v];
+                } else {
+                    xb = xm;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) sxb[v] = sxm[v];
+                }
+                if (k & 2) {
+                    ya = ym;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) sya[v] = sym[v];
+                } else {
+                    yb = ym;
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) syb[v] = sym[v];
+                }
+                ++lvl;
+            }
+        }
+        // pdf: the full NDF's mass in the sampled pixel over its mass in the domain
+        float pix = 0.f;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const float4 dx = SatV<U32>::diff(sxa[v], sxb[v]), dy = SatV<U32>::diff(sya[v], syb[v]);
+            pix = fmaf(dx.x * dy.x, za[v].x, pix);
+            pix = fmaf(dx.y * dy.y, za[v].y, pix);
+            pix = fmaf(dx.z * dy.z, za[v].z, pix);
+            pix = fmaf(dx.w * dy.w, za[v].w, pix);
+        }
+        pix = group_sum<G>(pix);
+        if (active && gl == 0) {
+            pndf_sample o;
+            if (!valid) {
+                atomicOr(p.err, 1u);
+                o.hx = o.hy = o.pdf = __int_as_float(0x7fc00000);
+                o.pixel = 0xffffffffu;
+            } else if (!live) {
+                o.hx = o.hy = __int_as_float(0x7fc00000);
+                o.pdf = 0.f;
+                o.pixel = 0xffffffffu;
+            } else {
+                const float inv = 2.f / (float)p.A;
+                o.hx = ((float)xa + __ldg(sxi + 8)) * inv - 1.f;
+                o.hy = ((float)ya + __ldg(sxi + 9)) * inv - 1.f;
+                o.pdf = (pix / root_all) / (inv * inv);
+                o.pixel = (uint32_t)xa | ((uint32_t)ya << 16);
+            }
+            out[si] = o;
+            if (tile_out) {
+                tile_out[2 * si] = valid ? ptx : 0;
+                tile_out[2 * si + 1] = valid ? pty : 0;
+            }
+        }
+    }
+}
+
+template <int G, int NV, bool U>
+static cudaError_t launch_ts(const QParams& p, const TileParams& tp, const pndf_query* q, const float* xi, int64_t n,
+                             pndf_sample* out, int32_t* tile_out, int num_sms, cudaStream_t st) {
+    const int64_t spb = 8 * (32 / G);
+    int64_t grid = (n + spb - 1) / spb;
+    if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
+    if (grid < 1) grid = 1;
+    tiled_sample_kernel<G, NV, U><<<(unsigned)grid, 256, 0, st>>>(p, tp, q, xi, n, out, tile_out);
+    return cudaGetLastError();
+}
+
+template <int G, bool U>
+static cudaError_t ts_nv(int NV, const QParams& p, const TileParams& tp, const pndf_query* q, const float* xi,
+                         int64_t n, pndf_sample* out, int32_t* to, int sms, cudaStream_t st) {
+    switch (NV) {
+        case 1: return launch_ts<G, 1, U>(p, tp, q, xi, n, out, to, sms, st);
+        case 2: return launch_ts<G, 2, U>(p, tp, q, xi, n, out, to, sms, st);
+        case 3: return launch_ts<G, 3, U>(p, tp, q, xi, n, out, to, sms, st);
+        case 4: return launch_ts<G, 4, U>(p, tp, q, xi, n, out, to, sms, st);
+        case 8: return launch_ts<G, 8, U>(p, tp, q, xi, n, out, to, sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+template <bool U>
+static cudaError_t ts_g(int G, int NV, const QParams& p, const TileParams& tp, const pndf_query* q, const float* xi,
+                        int64_t n, pndf_sample* out, int32_t* to, int sms, cudaStream_t st) {
+    switch (G) {
+        case 1: return ts_nv<1, U>(NV, p, tp, q, xi, n, out, to, sms, st);
+        case 2: return ts_nv<2, U>(NV, p, tp, q, xi, n, out, to, sms, st);
+        case 4: return ts_nv<4, U>(NV, p, tp, q, xi, n, out, to, sms, st);
+        case 8: return ts_nv<8, U>(NV, p, tp, q, xi, n, out, to, sms, st);
+        case 16: return ts_nv<16, U>(NV, p, tp, q, xi, n, out, to, sms, st);
+        case 32: return ts_nv<32, U>(NV, p, tp, q, xi, n, out, to, sms, st);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t launch_tiled_sample(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
+                                const float* xi, int64_t n, pndf_sample* out, int32_t* tile_out, int num_sms,
+                                cudaStream_t st) {
+    if (4 * G * NV != p.Rp) return cudaErrorInvalidValue;
+    if (p.prefix_u32) return ts_g<true>(G, NV, p, tp, q, xi, n, out, tile_out, num_sms, st);
+    return ts_g<false>(G, NV, p, tp, q, xi, n, out, tile_out, num_sms, st);
 }
 
 template <int G, int NV, bool U>

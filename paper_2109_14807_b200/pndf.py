@@ -68,7 +68,7 @@ class StoreStats(ctypes.Structure):
 
 SAMPLE_DTYPE = np.dtype([("hx", "<f4"), ("hy", "<f4"), ("pdf", "<f4"), ("pixel", "<u4")])
 
-EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_sync", "pndf_query_batch_host",
+EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_sample_tiles", "pndf_sync", "pndf_query_batch_host",
            "pndf_free",
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
@@ -103,6 +103,8 @@ def lib():
         L.pndf_query_batch.argtypes = [P, P, i64, P, u32, P]
         L.pndf_sample_batch.restype = i32
         L.pndf_sample_batch.argtypes = [P, P, P, i64, P, u32, P]
+        L.pndf_sample_tiles.restype = i32
+        L.pndf_sample_tiles.argtypes = [P, P, P, i64, P, P, u32, P]
         L.pndf_sync.restype = i32
         L.pndf_sync.argtypes = [P, P]
         L.pndf_query_batch_host.restype = i32
@@ -222,6 +224,14 @@ class Store:
         n = xi.shape[0] if n is None else n
         _check(lib().pndf_sample_batch(self.handle, _ptr(queries), _ptr(xi), n, _ptr(out), opts, _stream(stream)),
                "pndf_sample_batch")
+
+    def sample_tiles(self, queries, xi, out, tile=None, opts: int = 0, stream=None, n: int | None = None):
+        """Enqueue pndf_sample_tiles on a tiled store (Sec. 5.5): xi = device float32 [n, 11]
+        (8 descent levels, 2 jitter, 1 tile choice), out = n 16-byte pndf_sample records, tile =
+        optional device int32 [n, 2] receiving the chosen tile instance (tx, ty)."""
+        n = xi.shape[0] if n is None else n
+        _check(lib().pndf_sample_tiles(self.handle, _ptr(queries), _ptr(xi), n, _ptr(out), _ptr(tile), opts,
+                                       _stream(stream)), "pndf_sample_tiles")
 
     def sync(self, stream=None, raise_on_query_error: bool = True) -> int:
         st = lib().pndf_sync(self.handle, _stream(stream))

@@ -54,3 +54,59 @@ def test_tiled_query_parity(prefix):
     with pytest.raises(pndf.PndfError):
         st.sample_batch(torch_records(recs[:4]), xi, torch.empty((4, 4), dtype=torch.float32, device="cuda"))
     st.free()
+
+
+@pytest.mark.parametrize("prefix", [0, 2])
+def test_tiled_sample_parity(prefix):
+    """pndf_sample_tiles vs oracle.tiled_sample_batch (Sec. 5.5; reading 25).  The tile
+    choice is an integer decision from exact inputs (covered = positive mass; c = floor(xi * count) in fp32
+    on both sides): compared exactly.  Quad decisions are fp32 vs fp64 comparisons: pixels compared exactly
+    where the oracle's margin exceeds 1e-4, otherwise checked for validity; the pdf is the full NDF value of
+    the GPU's own pixel (oracle tiled query)."""
+    pndf = _pndf()
+    tc = synth.TileConfig(T=128)
+    f = synth.wang_factors(tc, synth.wang_tiles(tc))
+    n = 20_000
+    recs = _tile_queries(tc, n, 3)
+    recs["rect"][::2] = synth.pack_rect(0, tc.A - 1, 0, tc.A - 1)  # half: the whole image
+    recs[:64]["u"] = np.arange(64, dtype=np.float32) * tc.T          # exactly on tile borders
+    xi = np.random.default_rng(4).random((n, 11), dtype=np.float32)
+    td_o = oracle.TilesDesc(T=tc.T, s0=tc.s0, L=tc.L, margin=tc.margin, A=tc.A, R=tc.R, seed=tc.seed)
+    ref = oracle.tiled_sample_batch(td_o, f.C, f.X, f.Y, f.Z, recs, xi)
+    st = pndf.load_tiles(pndf.make_tile_desc(tc.T, tc.s0, tc.L, tc.margin, tc.A, tc.R, tc.seed, prefix=prefix),
+                         f.C, f.X, f.Y, f.Z)
+    out = torch.full((n, 4), float("nan"), dtype=torch.float32, device="cuda")
+    tile = torch.full((n, 2), -99, dtype=torch.int32, device="cuda")
+    st.sample_tiles(torch_records(recs), torch.from_numpy(xi).cuda(), out, tile)
+    st.sync()
+    o = out.cpu().numpy()
+    gt = tile.cpu().numpy()
+    pixel = o[:, 3].view(np.uint32)
+    np.testing.assert_array_equal(gt, ref["tile"])
+    assert (ref["count"] > 1).sum() > n // 4  # many footprints straddle tiles
+    none_g = pixel == 0xffffffff
+    none_o = ref["pixel"][:, 0] < 0
+    assert np.array_equal(none_g, none_o)
+    assert not none_o[::2].any()  # a covered tile has mass on the whole image
+    ok = ~none_o
+    gx = (pixel & 0xffff).astype(np.int64)
+    gy = (pixel >> 16).astype(np.int64)
+    firm = ok & (ref["margin"] > 1e-4)
+    assert firm.sum() > 0.9 * ok.sum()
+    assert np.array_equal(gx[firm], ref["pixel"][firm, 0]) and np.array_equal(gy[firm], ref["pixel"][firm, 1])
+    A = tc.A
+    np.testing.assert_allclose(o[ok, 0], (gx[ok] + xi[ok, 8].astype(np.float64)) * 2.0 / A - 1.0, atol=2e-6)
+    np.testing.assert_allclose(o[ok, 1], (gy[ok] + xi[ok, 9].astype(np.float64)) * 2.0 / A - 1.0, atol=2e-6)
+    pix = recs[ok].copy()
+    pix["rect"] = synth.pack_rect(gx[ok], gx[ok], gy[ok], gy[ok])
+    num = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, pix, mean=False)
+    den = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, recs[ok], mean=False)
+    assert (num > 0).all()
+    assert_parity(o[ok, 2].astype(np.float64), num / den * (A * A / 4.0), "tiled sampler pdf")
+    # invalid record -> NaN pdf + sticky PNDF_EQUERY; plain stores reject pndf_sample_tiles
+    bad = recs[:2].copy()
+    bad["size"][0] = -1.0
+    st.sample_tiles(torch_records(bad), torch.from_numpy(xi[:2]).cuda(), out[:2])
+    assert st.sync(raise_on_query_error=False) == pndf.EQUERY
+    assert np.isnan(out[0, 2].item())
+    st.free()
