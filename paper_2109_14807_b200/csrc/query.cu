@@ -44,22 +44,6 @@ cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, c
 //   scan_*_kernel      exclusive scan of the histograms -> each tile's digit offsets
 //   rs_scatter_kernel  stable tile-local ranking (match_any + per-warp counts),
 //                      staged in shared memory, written out digit run by run.
-__global__ void bin_keys_kernel(const QParams p, const pndf_query* __restrict__ q, int64_t n, uint32_t* keys,
-                                uint32_t invalid_key, int half) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-        const pndf_query rec = ldg_query(q + i);
-        int x1, x2, y1, y2;
-        uint32_t key = invalid_key;
-        if (record_valid(p, rec, x1, x2, y1, y2)) {
-            int l0;
-            float t;
-            level_select(p, rec.size, l0, t);
-            key = cell_key(p, rec, l0, half);
-        }
-        keys[i] = key;
-    }
-}
-
 constexpr int kScanThreads = 1024;
 constexpr int kScanItems = 4;
 constexpr int kScanTile = kScanThreads * kScanItems;
@@ -158,19 +142,74 @@ constexpr int kRsItems = 16;
 constexpr int kRsTile = kRsThreads * kRsItems;  // 4096 keys per tile
 constexpr int kRsWarps = kRsThreads / 32;
 
-// counts[d * ntiles + tile] = #keys of the tile whose digit is d (digits of BITS bits)
+// counts[d * ntiles + tile] = #keys of the tile whose digit is d (digits of BITS bits).
+// Keys are read as uint4 (4 per load, all 4 loads of a thread in flight) and
+// counted into two sub-histograms (even / odd warps) to halve atomic contention.
 template <int BITS>
 __global__ void __launch_bounds__(kRsThreads) rs_hist_kernel(const uint32_t* __restrict__ keys, int64_t n, int shift,
                                                              uint32_t* counts, int64_t ntiles) {
+    constexpr int RADIX = 1 << BITS;
+    __shared__ uint32_t h[2][RADIX];
+    for (int d = threadIdx.x; d < 2 * RADIX; d += kRsThreads) h[d / RADIX][d % RADIX] = 0;
+    __syncthreads();
+    uint32_t* hw = h[(threadIdx.x >> 5) & 1];
+    const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+    if (t0 + kRsTile <= n) {
+        const uint4* k4 = reinterpret_cast<const uint4*>(keys + t0);
+        uint4 v[kRsItems / 4];
+#pragma unroll
+        for (int i = 0; i < kRsItems / 4; ++i) v[i] = __ldg(k4 + i * kRsThreads + threadIdx.x);
+#pragma unroll
+        for (int i = 0; i < kRsItems / 4; ++i) {
+            atomicAdd(&hw[(v[i].x >> shift) & (RADIX - 1)], 1u);
+            atomicAdd(&hw[(v[i].y >> shift) & (RADIX - 1)], 1u);
+            atomicAdd(&hw[(v[i].z >> shift) & (RADIX - 1)], 1u);
+            atomicAdd(&hw[(v[i].w >> shift) & (RADIX - 1)], 1u);
+        }
+    } else {
+        for (int i = 0; i < kRsItems; ++i) {
+            const int64_t k = t0 + (int64_t)i * kRsThreads + threadIdx.x;
+            if (k < n) atomicAdd(&hw[(__ldg(keys + k) >> shift) & (RADIX - 1)], 1u);
+        }
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < RADIX; d += kRsThreads) counts[(int64_t)d * ntiles + blockIdx.x] = h[0][d] + h[1][d];
+}
+
+// a1 keys fused with the first radix pass's tile histogram: block b computes
+// the keys of radix tile b (kRsTile records) and counts their lowest digit.
+template <int BITS>
+__global__ void __launch_bounds__(kRsThreads) bin_keys_kernel(const QParams p, const pndf_query* __restrict__ q,
+                                                              int64_t n, uint32_t* keys, uint32_t invalid_key,
+                                                              int half, uint32_t* counts, int64_t ntiles) {
     constexpr int RADIX = 1 << BITS;
     __shared__ uint32_t h[RADIX];
     for (int d = threadIdx.x; d < RADIX; d += kRsThreads) h[d] = 0;
     __syncthreads();
     const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
-#pragma unroll 4
-    for (int i = 0; i < kRsItems; ++i) {
-        const int64_t k = t0 + (int64_t)i * kRsThreads + threadIdx.x;
-        if (k < n) atomicAdd(&h[(__ldg(keys + k) >> shift) & (RADIX - 1)], 1u);
+    constexpr int B = 4;  // records in flight per thread
+    for (int i0 = 0; i0 < kRsItems; i0 += B) {
+        pndf_query rec[B];
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int64_t k = t0 + (int64_t)(i0 + b) * kRsThreads + threadIdx.x;
+            if (k < n) rec[b] = ldg_query(q + k);
+        }
+#pragma unroll
+        for (int b = 0; b < B; ++b) {
+            const int64_t k = t0 + (int64_t)(i0 + b) * kRsThreads + threadIdx.x;
+            if (k >= n) continue;
+            int x1, x2, y1, y2;
+            uint32_t key = invalid_key;
+            if (record_valid(p, rec[b], x1, x2, y1, y2)) {
+                int l0;
+                float t;
+                level_select(p, rec[b].size, l0, t);
+                key = cell_key(p, rec[b], l0, half);
+            }
+            keys[k] = key;
+            atomicAdd(&h[key & (RADIX - 1)], 1u);
+        }
     }
     __syncthreads();
     for (int d = threadIdx.x; d < RADIX; d += kRsThreads) counts[(int64_t)d * ntiles + blockIdx.x] = h[d];
@@ -290,7 +329,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_scatter_kernel(const uint32_
         const uint32_t key = s_keys[j];
         const uint32_t d = (key >> shift) & (RADIX - 1);
         const uint32_t pos = s_goff[d] + (uint32_t)j;
-        keys_out[pos] = key;
+        if (keys_out) keys_out[pos] = key;
         vals_out[pos] = s_vals[j];
     }
 }
@@ -313,8 +352,8 @@ constexpr size_t rs_smem_bytes() {
 
 template <int BITS>
 static void radix_pass(const uint32_t* kin, const uint32_t* vin, int64_t n, int shift, BinScratch& sc, int64_t ntiles,
-                       uint32_t* kout, uint32_t* vout, cudaStream_t st) {
-    rs_hist_kernel<BITS><<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, n, shift, sc.counts, ntiles);
+                       uint32_t* kout, uint32_t* vout, bool have_hist, cudaStream_t st) {
+    if (!have_hist) rs_hist_kernel<BITS><<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, n, shift, sc.counts, ntiles);
     scan_exclusive(sc.counts, ntiles << BITS, sc.bsum, st);
     cudaFuncSetAttribute(rs_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)rs_smem_bytes<BITS>());
@@ -339,21 +378,25 @@ cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int
     const int bits = (kbits > 24 && kbits <= 27) ? 9 : 8;
     const int passes = (kbits + bits - 1) / bits;
     const int64_t ntiles = radix_tiles(n);
-    int64_t g = (n + 255) / 256;
-    if (g > (int64_t)num_sms * 8) g = (int64_t)num_sms * 8;
-    if (g < 1) g = 1;
-    bin_keys_kernel<<<(unsigned)g, 256, 0, st>>>(p, q, n, sc.keys[0], (uint32_t)(nkeys - 1), half);
+    if (bits == 9)
+        bin_keys_kernel<9><<<(unsigned)ntiles, kRsThreads, 0, st>>>(p, q, n, sc.keys[0], (uint32_t)(nkeys - 1), half,
+                                                                   sc.counts, ntiles);
+    else
+        bin_keys_kernel<8><<<(unsigned)ntiles, kRsThreads, 0, st>>>(p, q, n, sc.keys[0], (uint32_t)(nkeys - 1), half,
+                                                                   sc.counts, ntiles);
     *launches += 1;
     int cur = 0;
     const uint32_t* vals = nullptr;  // pass 0: identity permutation
     for (int ps = 0; ps < passes; ++ps) {
+        // the last pass writes sorted keys only when the caller asks for them
+        uint32_t* kout = (ps + 1 < passes || sorted_keys) ? sc.keys[cur ^ 1] : nullptr;
         if (bits == 9)
-            radix_pass<9>(sc.keys[cur], vals, n, 9 * ps, sc, ntiles, sc.keys[cur ^ 1], sc.vals[cur ^ 1], st);
+            radix_pass<9>(sc.keys[cur], vals, n, 9 * ps, sc, ntiles, kout, sc.vals[cur ^ 1], ps == 0, st);
         else
-            radix_pass<8>(sc.keys[cur], vals, n, 8 * ps, sc, ntiles, sc.keys[cur ^ 1], sc.vals[cur ^ 1], st);
+            radix_pass<8>(sc.keys[cur], vals, n, 8 * ps, sc, ntiles, kout, sc.vals[cur ^ 1], ps == 0, st);
         vals = sc.vals[cur ^ 1];
         cur ^= 1;
-        *launches += 5;
+        *launches += ps == 0 ? 4 : 5;
     }
     *perm = vals;
     if (sorted_keys) *sorted_keys = sc.keys[cur];
