@@ -12,6 +12,7 @@
 // system, so there are no tensor cores here.
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "internal.cuh"
 #include "device.cuh"
@@ -225,21 +226,22 @@ __global__ void __launch_bounds__(kRsThreads) bin_keys_kernel(const QParams p, c
 // which keeps the sort stable.  The tile is staged in shared memory in digit
 // order, then written out so that consecutive items of a digit run go to
 // consecutive global addresses.
-template <int BITS>
-__global__ void __launch_bounds__(kRsThreads, 3) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
+template <int BITS, int THREADS>
+__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : 3) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in, int64_t n,
                                                                 int shift, const uint32_t* __restrict__ offsets,
                                                                 int64_t ntiles, uint32_t* keys_out,
                                                                 uint32_t* vals_out) {
     constexpr int RADIX = 1 << BITS;
-    constexpr int DPT = RADIX / kRsThreads;  // digits owned per thread
-    constexpr int DPL = RADIX / 32;          // digits per lane in the tile scan
-    constexpr int IPW = kRsTile / kRsWarps;  // items per warp segment
+    constexpr int ITEMS = kRsTile / THREADS;  // items per thread
+    constexpr int WARPS = THREADS / 32;
+    constexpr int DPL = RADIX / 32;           // digits per lane in the tile scan
+    constexpr int IPW = kRsTile / WARPS;      // items per warp segment
     extern __shared__ uint32_t rs_smem[];  // rs_smem_bytes<BITS>() of dynamic shared memory
     uint32_t* s_keys = rs_smem;                                      // [kRsTile]
     uint32_t* s_vals = s_keys + kRsTile;                             // [kRsTile]
-    uint32_t(*s_cnt)[RADIX] = reinterpret_cast<uint32_t(*)[RADIX]>(s_vals + kRsTile);  // [kRsWarps][RADIX]
-    uint32_t* s_run = s_vals + kRsTile + kRsWarps * RADIX;  // tile histogram
+    uint32_t(*s_cnt)[RADIX] = reinterpret_cast<uint32_t(*)[RADIX]>(s_vals + kRsTile);  // [WARPS][RADIX]
+    uint32_t* s_run = s_vals + kRsTile + WARPS * RADIX;  // tile histogram
     uint32_t* s_start = s_run + RADIX;                      // tile-local start of each digit run
     uint32_t* s_goff = s_start + RADIX;                     // global start minus tile-local start
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
@@ -247,26 +249,24 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_scatter_kernel(const uint32_
     const int nt = (int)((n - t0) < (int64_t)kRsTile ? (n - t0) : (int64_t)kRsTile);
     const int seg = warp * IPW + lane;  // tile-local index of item 0 of this lane
 
-    uint32_t k[kRsItems], v[kRsItems];
+    uint32_t k[ITEMS], v[ITEMS];
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         const int64_t g = t0 + seg + i * 32;
         const bool ok = seg + i * 32 < nt;
         k[i] = ok ? __ldg(keys_in + g) : 0xffffffffu;
         v[i] = ok ? (vals_in ? __ldg(vals_in + g) : (uint32_t)g) : 0u;
     }
+    for (int d = t; d < RADIX; d += THREADS) {
 #pragma unroll
-    for (int j = 0; j < DPT; ++j) {
-        const int d = t + j * kRsThreads;
-#pragma unroll
-        for (int w = 0; w < kRsWarps; ++w) s_cnt[w][d] = 0;
+        for (int w = 0; w < WARPS; ++w) s_cnt[w][d] = 0;
     }
     __syncthreads();
     // warp-private stable ranking: r[i] = items of the same digit earlier in this warp's segment
-    uint32_t r[kRsItems / 2];  // two 16-bit ranks per register (a rank is < IPW)
+    uint32_t r[ITEMS / 2];  // two 16-bit ranks per register (a rank is < IPW)
     const uint32_t lt_mask = (1u << lane) - 1u;
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         const bool ok = seg + i * 32 < nt;
         const uint32_t d = (k[i] >> shift) & (RADIX - 1);
         const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : 0xffffffffu);
@@ -279,12 +279,10 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_scatter_kernel(const uint32_
         __syncwarp();
     }
     __syncthreads();
-#pragma unroll
-    for (int j = 0; j < DPT; ++j) {  // thread t owns digits t + j*256: exclusive offsets over the warps
-        const int dd = t + j * kRsThreads;
+    for (int dd = t; dd < RADIX; dd += THREADS) {  // exclusive offsets of each digit over the warps
         uint32_t acc = 0;
 #pragma unroll
-        for (int w = 0; w < kRsWarps; ++w) {
+        for (int w = 0; w < WARPS; ++w) {
             const uint32_t c = s_cnt[w][dd];
             s_cnt[w][dd] = acc;
             acc += c;
@@ -316,7 +314,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_scatter_kernel(const uint32_
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < kRsItems; ++i) {
+    for (int i = 0; i < ITEMS; ++i) {
         if (seg + i * 32 < nt) {
             const uint32_t d = (k[i] >> shift) & (RADIX - 1);
             const uint32_t pos = s_start[d] + s_cnt[warp][d] + ((r[i >> 1] >> ((i & 1) * 16)) & 0xffffu);
@@ -325,7 +323,7 @@ __global__ void __launch_bounds__(kRsThreads, 3) rs_scatter_kernel(const uint32_
         }
     }
     __syncthreads();
-    for (int j = t; j < nt; j += kRsThreads) {
+    for (int j = t; j < nt; j += THREADS) {
         const uint32_t key = s_keys[j];
         const uint32_t d = (key >> shift) & (RADIX - 1);
         const uint32_t pos = s_goff[d] + (uint32_t)j;
@@ -345,9 +343,27 @@ static cudaError_t scan_exclusive(uint32_t* a, int64_t nb, uint32_t* bsum, cudaS
     return cudaGetLastError();
 }
 
-template <int BITS>
+template <int BITS, int THREADS>
 constexpr size_t rs_smem_bytes() {
-    return sizeof(uint32_t) * (2 * kRsTile + (kRsWarps + 3) * (1 << BITS));
+    return sizeof(uint32_t) * (2 * kRsTile + (THREADS / 32 + 3) * (1 << BITS));
+}
+
+template <int BITS, int THREADS>
+static void launch_scatter(const uint32_t* kin, const uint32_t* vin, int64_t n, int shift, const uint32_t* offsets,
+                           int64_t ntiles, uint32_t* kout, uint32_t* vout, cudaStream_t st) {
+    constexpr size_t smem = rs_smem_bytes<BITS, THREADS>();
+    cudaFuncSetAttribute(rs_scatter_kernel<BITS, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    rs_scatter_kernel<BITS, THREADS><<<(unsigned)ntiles, THREADS, smem, st>>>(kin, vin, n, shift, offsets, ntiles,
+                                                                              kout, vout);
+}
+
+// scatter CTA size: 256 (default) or 512 threads per 4096-key tile (PNDF_SCATTER_THREADS, for A/B runs)
+static int scatter_threads() {
+    static int v = [] {
+        const char* e = getenv("PNDF_SCATTER_THREADS");
+        return (e && atoi(e) == 512) ? 512 : 256;
+    }();
+    return v;
 }
 
 template <int BITS>
@@ -355,10 +371,10 @@ static void radix_pass(const uint32_t* kin, const uint32_t* vin, int64_t n, int 
                        uint32_t* kout, uint32_t* vout, bool have_hist, cudaStream_t st) {
     if (!have_hist) rs_hist_kernel<BITS><<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, n, shift, sc.counts, ntiles);
     scan_exclusive(sc.counts, ntiles << BITS, sc.bsum, st);
-    cudaFuncSetAttribute(rs_scatter_kernel<BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)rs_smem_bytes<BITS>());
-    rs_scatter_kernel<BITS><<<(unsigned)ntiles, kRsThreads, rs_smem_bytes<BITS>(), st>>>(kin, vin, n, shift,
-                                                                                         sc.counts, ntiles, kout, vout);
+    if (scatter_threads() == 512)
+        launch_scatter<BITS, 512>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
+    else
+        launch_scatter<BITS, 256>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
 }
 
 int64_t bin_key_space(int64_t P, int* half) {
