@@ -7,6 +7,7 @@ for c in 1 2 3 4; do timeout 600 python bench.py --config $c > gpurun_out/bench_
 timeout 600 python bench.py --op sample > gpurun_out/bench_sample.log 2>&1
 timeout 600 python bench.py --op sg > gpurun_out/bench_sg.log 2>&1
 timeout 600 python bench.py --op wang > gpurun_out/bench_wang.log 2>&1
+timeout 600 python bench.py --op wang_sample > gpurun_out/bench_wang_sample.log 2>&1
 timeout 600 python bench.py --op blocked --config 2 > gpurun_out/bench_blocked.log 2>&1
 timeout 600 python bench.py --op als --config 2 > gpurun_out/bench_als.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1 && \
