@@ -47,6 +47,12 @@ def test_calls_that_need_no_gpu(libpath):
     assert pndf.error_string(pndf.EQUERY).startswith("invalid query")
     assert pndf.error_string(pndf.OK) == "ok"
     assert pndf.lib().pndf_free(None) == 0
+    # argument errors are returned synchronously, before any device work
+    L = pndf.lib()
+    assert L.pndf_query_batch(None, None, 0, None, 0, None) == pndf.EINVAL
+    assert L.pndf_sample_batch(None, None, None, 0, None, 0, None) == pndf.EINVAL
+    assert L.pndf_sample_tiles(None, None, None, 0, None, None, 0, None) == pndf.EINVAL
+    assert L.pndf_sync(None, None) == pndf.EINVAL
 
 
 def test_binding_matches_header_constants():
