@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(kRsThreads) bin_keys_kernel(const QParams p, c
 // which keeps the sort stable.  The tile is staged in shared memory in digit
 // order, then written out so that consecutive items of a digit run go to
 // consecutive global addresses.
-template <int BITS, int THREADS>
-__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : 3) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
+template <int BITS, int THREADS, bool LATE_V>
+__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in, int64_t n,
                                                                 int shift, const uint32_t* __restrict__ offsets,
                                                                 int64_t ntiles, uint32_t* keys_out,
@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : 3) rs_scatter_ke
         const int64_t g = t0 + seg + i * 32;
         const bool ok = seg + i * 32 < nt;
         k[i] = ok ? __ldg(keys_in + g) : 0xffffffffu;
-        v[i] = ok ? (vals_in ? __ldg(vals_in + g) : (uint32_t)g) : 0u;
+        if (!LATE_V) v[i] = ok ? (vals_in ? __ldg(vals_in + g) : (uint32_t)g) : 0u;
     }
     for (int d = t; d < RADIX; d += THREADS) {
 #pragma unroll
@@ -277,6 +277,14 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : 3) rs_scatter_ke
         __syncwarp();
         if (ok && lt == 0) s_cnt[warp][d] = base + __popc(peers);
         __syncwarp();
+    }
+    if (LATE_V) {  // values are needed only for placement: their loads overlap the scans below
+#pragma unroll
+        for (int i = 0; i < ITEMS; ++i) {
+            const int64_t g = t0 + seg + i * 32;
+            const bool ok = seg + i * 32 < nt;
+            v[i] = ok ? (vals_in ? __ldg(vals_in + g) : (uint32_t)g) : 0u;
+        }
     }
     __syncthreads();
     for (int dd = t; dd < RADIX; dd += THREADS) {  // exclusive offsets of each digit over the warps
@@ -348,13 +356,23 @@ constexpr size_t rs_smem_bytes() {
     return sizeof(uint32_t) * (2 * kRsTile + (THREADS / 32 + 3) * (1 << BITS));
 }
 
-template <int BITS, int THREADS>
+template <int BITS, int THREADS, bool LATE_V>
 static void launch_scatter(const uint32_t* kin, const uint32_t* vin, int64_t n, int shift, const uint32_t* offsets,
                            int64_t ntiles, uint32_t* kout, uint32_t* vout, cudaStream_t st) {
     constexpr size_t smem = rs_smem_bytes<BITS, THREADS>();
-    cudaFuncSetAttribute(rs_scatter_kernel<BITS, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    rs_scatter_kernel<BITS, THREADS><<<(unsigned)ntiles, THREADS, smem, st>>>(kin, vin, n, shift, offsets, ntiles,
-                                                                              kout, vout);
+    cudaFuncSetAttribute(rs_scatter_kernel<BITS, THREADS, LATE_V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    rs_scatter_kernel<BITS, THREADS, LATE_V><<<(unsigned)ntiles, THREADS, smem, st>>>(kin, vin, n, shift, offsets,
+                                                                                      ntiles, kout, vout);
+}
+
+// value loads after the ranking (4 CTAs/SM) vs with the keys (3 CTAs/SM): PNDF_SCATTER_LATEV=0/1
+static bool scatter_late_v() {
+    static bool v = [] {
+        const char* e = getenv("PNDF_SCATTER_LATEV");
+        return e && atoi(e) == 1;
+    }();
+    return v;
 }
 
 // scatter CTA size: 256 (default) or 512 threads per 4096-key tile (PNDF_SCATTER_THREADS, for A/B runs)
@@ -372,9 +390,11 @@ static void radix_pass(const uint32_t* kin, const uint32_t* vin, int64_t n, int 
     if (!have_hist) rs_hist_kernel<BITS><<<(unsigned)ntiles, kRsThreads, 0, st>>>(kin, n, shift, sc.counts, ntiles);
     scan_exclusive(sc.counts, ntiles << BITS, sc.bsum, st);
     if (scatter_threads() == 512)
-        launch_scatter<BITS, 512>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
+        launch_scatter<BITS, 512, false>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
+    else if (scatter_late_v())
+        launch_scatter<BITS, 256, true>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
     else
-        launch_scatter<BITS, 256>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
+        launch_scatter<BITS, 256, false>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
 }
 
 int64_t bin_key_space(int64_t P, int* half) {
