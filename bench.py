@@ -42,7 +42,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang", "wang_sample", "blocked", "als"],
+    ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang", "wang_sample", "blocked", "als",
+                                                      "sweep"],
                     help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
                          "prefiltering (SG rectangle generation + range query)")
@@ -430,6 +431,83 @@ def run_ours(args, cfg, rank, world, local_rank):
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "parity_sample": parity,
             "clocks": clk, "checksum": checksum}
+    print(json.dumps(line), flush=True)
+    store.free()
+    return 0
+
+
+SWEEP_METRIC = "NDF range queries/sec across footprint size x rectangle side (constant cost, P:118)"
+SWEEP_S = (1, 16, 256, 2048)
+SWEEP_SIDE = (1, 16, 128)
+
+
+def run_sweep_op(args, cfg, rank, world, local_rank):
+    """--op sweep (SURVEY §8(d) secondary sweep): config 3's store, each cell a batch of queries with the
+    footprint size S fixed in {1, 16, 256, 2048} and square rectangles of side fixed in {1, 16, 128},
+    centres uniform over the map, rectangles uniform over the grid.  The method's claim is constant cost
+    per query ("constant cost ... regardless of the footprint size and the angular range"): q/s
+    may vary with cache residency (S picks the level: S = 2048 touches 43 KB of Zc, S = 1 the whole 1.1
+    GB level 0) and with the a5 path (sides <= 48 read one range-table row per axis, side 128 two SAT
+    rows), never with rectangle area.  `value` = the slowest cell; each cell is parity-sampled."""
+    import torch
+    from paper_2109_14807_b200 import pndf
+    if world > 1 and rank != 0:
+        return 0  # replicas only: one GPU measures the sweep
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n = args.queries or cfg.n_queries
+    bins, f = host_inputs(cfg)
+    Z = synth.build_z_exact_cuda(cfg, f.info["atom_map"], local_rank) if f.Z is None else f.Z
+    store = pndf.load_factors(pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap), f.C, f.X, f.Y, Z,
+                              device=local_rank)
+    del Z
+    torch.cuda.empty_cache()
+    rng = np.random.default_rng(700)
+    h_q = torch.empty((n, 4), dtype=torch.int32, pin_memory=True)
+    d_q = torch.empty((n, 4), dtype=torch.int32, device=dev)
+    d_out = torch.empty(n, dtype=torch.float32, device=dev)
+    cells, worst, all_pass = [], None, True
+    clocks = ClockSampler(bus_id_of(dev))
+    clocks.start()
+    for S in SWEEP_S:
+        for side in SWEEP_SIDE:
+            x1 = rng.integers(0, cfg.A - side + 1, n)
+            y1 = rng.integers(0, cfg.A - side + 1, n)
+            recs = synth.make_records(rng.uniform(0, cfg.N, n), rng.uniform(0, cfg.N, n), np.full(n, float(S)),
+                                      x1, x1 + side - 1, y1, y1 + side - 1)
+            h_q.numpy().view(synth.QREC).reshape(-1)[:] = recs
+            d_q.copy_(h_q)
+            for _ in range(args.warmup):
+                store.query_batch(d_q, d_out, pndf.BIN_AUTO)
+                store.sync()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                store.query_batch(d_q, d_out, pndf.BIN_AUTO)
+                store.sync()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / args.steps
+            par = parity_sample(cfg, f, h_q, d_out, k=1024) if not args.no_parity else None
+            all_pass = all_pass and (par is None or par["pass"])
+            qps = n / (ms * 1e-3)
+            cells.append({"S": S, "side": side, "queries_per_s": qps, "ms": ms,
+                          "binned": bool(store.stats()["last_binned"]), "parity_pass": None if par is None
+                          else par["pass"]})
+            worst = qps if worst is None else min(worst, qps)
+    clk = clocks.stop()
+    by_s = {S: [c["queries_per_s"] for c in cells if c["S"] == S] for S in SWEEP_S}
+    line = {"metric": SWEEP_METRIC, "value": worst, "unit": "queries/s", "n_gpus": 1, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": max(c["ms"] for c in cells), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": workload_name(cfg) + f", {n} queries per cell, S fixed x square side fixed",
+                       "S": list(SWEEP_S), "side": list(SWEEP_SIDE)},
+            "sweep": cells,
+            "side_spread_at_fixed_S": {str(S): max(v) / min(v) for S, v in by_s.items()},
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": None, "parity_sample": {"pass": all_pass, "checked_per_cell": 1024},
+            "clocks": clk}
     print(json.dumps(line), flush=True)
     store.free()
     return 0
@@ -960,6 +1038,8 @@ def main():
             return run_wang_op(args, cfg, rank, world, local_rank)
         if args.op == "blocked":
             return run_blocked_op(args, cfg, rank, world, local_rank)
+        if args.op == "sweep":
+            return run_sweep_op(args, synth.CONFIGS[3], rank, world, local_rank)
         if args.op == "als":
             return run_als_op(args, cfg if cfg.idx in (1, 2) else synth.CONFIGS[2], rank, world, local_rank)
         return run_ours(args, cfg, rank, world, local_rank)
