@@ -445,7 +445,7 @@ def run_sweep_op(args, cfg, rank, world, local_rank):
     """--op sweep (SURVEY §8(d) secondary sweep): config 3's store, each cell a batch of queries with the
     footprint size S fixed in {1, 16, 256, 2048} and square rectangles of side fixed in {1, 16, 128},
     centres uniform over the map, rectangles uniform over the grid.  The method's claim is constant cost
-    per query ("constant cost ... regardless of the footprint size and the angular range"): q/s
+    per query ("achieving both constant performance and constant storage, a.k.a. constant cost"): q/s
     may vary with cache residency (S picks the level: S = 2048 touches 43 KB of Zc, S = 1 the whole 1.1
     GB level 0) and with the a5 path (sides <= 48 read one range-table row per axis, side 128 two SAT
     rows), never with rectangle area.  `value` = the slowest cell; each cell is parity-sampled."""
