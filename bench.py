@@ -538,6 +538,8 @@ def run_sample_op(args, cfg, rank, world, local_rank):
     Z = synth.build_z_exact_cuda(cfg, f.info["atom_map"], local_rank) if f.Z is None else f.Z
     store = pndf.load_factors(pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, cfg.wrap), f.C, f.X, f.Y, Z,
                               device=local_rank)
+    if args.lanes:
+        store.set_lanes(args.lanes)
     del Z
     torch.cuda.empty_cache()
     h_q = torch.empty((n, 4), dtype=torch.int32)

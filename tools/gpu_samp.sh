@@ -1,0 +1,5 @@
+#!/bin/bash
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_sampler.py -x -q > gpurun_out/pytest_sampler.log 2>&1; echo rc=$? >> gpurun_out/pytest_sampler.log
+timeout 600 python bench.py --op sample > gpurun_out/bench_sample.log 2>&1; echo rc=$? >> gpurun_out/bench_sample.log
+timeout 600 python bench.py --op sample --config 2 > gpurun_out/bench_sample_c2.log 2>&1; echo rc=$? >> gpurun_out/bench_sample_c2.log
