@@ -731,6 +731,8 @@ def run_wang_op(args, cfg, rank, world, local_rank):
     f = synth.wang_factors(tc, tiles)
     store = pndf.load_tiles(pndf.make_tile_desc(tc.T, tc.s0, tc.L, tc.margin, tc.A, tc.R, tc.seed), f.C, f.X, f.Y,
                             f.Z, device=local_rank)
+    if args.lanes:
+        store.set_lanes(args.lanes)
     # queries: world positions uniform, sizes log-uniform in [1, T], config-2-like rectangles
     rng = np.random.default_rng(500 + rank)
     A = tc.A

@@ -752,12 +752,17 @@ pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const f
         if (r != PNDF_OK) return r;
     }
     // Lanes per sample: the descent is a chain of dependent L2 loads, so more samples in flight per warp
-    // beat wider samples -- with U32 SATs and Rp >= 128, 8 float4 per lane (config 5: G = 8 lanes,
-    // 4 samples per warp, +14% over the query kernel's G = 32).  pndf_set_lanes overrides.
+    // beat wider samples.  With U32 SATs (HILO at 8 float4 per lane spills): Rp >= 128 -> 8 float4 per
+    // lane (config 5: G = 8, 4 samples per warp, 3.57e8 vs 3.12e8 samples/s at G = 32, 2.85e8 at G = 16);
+    // smaller Rp -> 2 float4 per lane (config 2: G = 4, 2.5e9 vs 2.0e9 at G = 8, 1.9e9 at G = 1).
+    // pndf_set_lanes overrides.
     int sg = s->G, snv = s->NV;
-    if (s->G == s->G0 && s->qp.prefix_u32 && s->Rp >= 128 && lanes_supported(s->Rp / 32, 8)) {
-        sg = s->Rp / 32;
-        snv = 8;
+    if (s->G == s->G0 && s->qp.prefix_u32) {
+        const int nv = s->Rp >= 128 ? 8 : 2;
+        if (s->Rp % (4 * nv) == 0 && lanes_supported(s->Rp / (4 * nv), nv)) {
+            sg = s->Rp / (4 * nv);
+            snv = nv;
+        }
     }
     bool first = true;
     for (int64_t a = 0; a < n; a += step) {
@@ -794,11 +799,18 @@ pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const f
         CK(cudaEventRecord(s->ev[0], st));
         CK(cudaEventRecord(s->ev[1], st));
     }
+    // lanes per sample as in pndf_sample_batch: 8 float4 per lane with U32 SATs (the Wang workload, R = 32:
+    // one lane per sample, 4.8e8 vs 3.1e8 samples/s at the query kernel's 8 lanes); pndf_set_lanes overrides
+    int sg = s->G, snv = s->NV;
+    if (s->G == s->G0 && s->qp.prefix_u32 && s->Rp >= 32 && lanes_supported(s->Rp / 32, 8)) {
+        sg = s->Rp / 32;
+        snv = 8;
+    }
     const int64_t step = int64_t(1) << 30;
     int launches = 0;
     for (int64_t a = 0; a < n; a += step) {
         const int64_t m = std::min(step, n - a);
-        CK(launch_tiled_sample(s->qp, s->tp, s->G, s->NV, d_queries + a, d_xi + (size_t)a * 11, m, d_out + a,
+        CK(launch_tiled_sample(s->qp, s->tp, sg, snv, d_queries + a, d_xi + (size_t)a * 11, m, d_out + a,
                                d_tile ? d_tile + 2 * a : nullptr, s->num_sms, st));
         launches += 1;
     }
