@@ -964,6 +964,8 @@ def run_blocked_op(args, cfg, rank, world, local_rank):
     bins = synth.bin_map(cfg, nxy)
     bs, _ = synth.build_blocked(cfg, nxy, bins, t=16, region=8)
     store = pndf.load_blocked(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.wrap, bs, device=local_rank)
+    if args.lanes:
+        store.set_lanes(args.lanes)
     recs = synth.gen_queries(cfg, bins, i0, i1)
     d_q = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).to(dev)
     d_out = torch.empty(n, dtype=torch.float32, device=dev)
