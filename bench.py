@@ -48,6 +48,8 @@ def parse():
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
                          "prefiltering (SG rectangle generation + range query)")
     ap.add_argument("--queries", type=int, default=0, help="override the config's total query count")
+    ap.add_argument("--s0", type=int, default=0, help="override the base stride (SURVEY §8(d): config 3 at s0=4 "
+                                                       "is the ~L2-resident variant, Zc 89.5 MB)")
     ap.add_argument("--as-shard", default="", help="K/W: one GPU runs rank K's shard of a W-GPU job "
                                                     "(per-GPU cost of the multi-GPU run on a one-GPU box)")
     ap.add_argument("--shard", default="spatial", choices=["spatial", "index"],
@@ -64,8 +66,9 @@ def parse():
 
 
 def workload_name(cfg) -> str:
+    s0 = f", base stride s0={cfg.s0}" if cfg.s0 != 1 else ""
     return (f"config{cfg.idx}-{cfg.name}: {cfg.N}^2 {cfg.map_kind} map, A={cfg.A}, R={cfg.R}, "
-            f"L={cfg.L} levels (P={cfg.P} rows), {cfg.n_queries:.0e} queries")
+            f"L={cfg.L} levels (P={cfg.P} rows){s0}, {cfg.n_queries:.0e} queries")
 
 
 def bytes_per_query(R: int) -> int:
@@ -1068,6 +1071,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = synth.CONFIGS[args.config]
+    if args.s0:
+        cfg = cfg.scaled(s0=args.s0)
     if args.impl == "reference":
         return run_reference(args, cfg, rank, world)
     if world > 1:
