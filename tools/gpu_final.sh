@@ -10,6 +10,8 @@ timeout 600 python bench.py --op wang > gpurun_out/bench_wang.log 2>&1
 timeout 600 python bench.py --op wang_sample > gpurun_out/bench_wang_sample.log 2>&1
 timeout 600 python bench.py --op blocked --config 2 > gpurun_out/bench_blocked.log 2>&1
 timeout 600 python bench.py --op als --config 2 > gpurun_out/bench_als.log 2>&1
+timeout 900 python bench.py --op sweep > gpurun_out/bench_sweep.log 2>&1
+timeout 600 python bench.py --config 3 --s0 4 > gpurun_out/bench_c3_s04.log 2>&1
 timeout 900 python bench.py > gpurun_out/bench_default.log 2>&1 && \
 timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_default.csv python bench.py > gpurun_out/ncu_launches.log 2>&1
 echo launches_rc=$? >> gpurun_out/ncu_launches.log

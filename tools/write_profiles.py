@@ -144,7 +144,7 @@ def main():
     if os.path.exists(la):
         open(os.path.join(OUT, f"{rnd}_launches_default.txt"), "w").write(launches(la))
     for name in ("bench_default", "bench_c1", "bench_c2", "bench_c3", "bench_c4", "bench_sample", "bench_sg",
-                 "bench_wang", "bench_wang_sample", "bench_blocked", "bench_als"):
+                 "bench_wang", "bench_wang_sample", "bench_blocked", "bench_als", "bench_sweep", "bench_c3_s04"):
         b = os.path.join(GP, name + ".log")
         if os.path.exists(b):
             lines = [l for l in open(b).read().splitlines() if l.startswith("{")]
