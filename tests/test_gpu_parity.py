@@ -136,6 +136,26 @@ def test_binning_bitwise_identical_config3():
     assert a.tobytes() == b.tobytes()
 
 
+def test_shards_bitwise_identical_to_whole_batch():
+    """per-query results are bitwise identical for any number of GPUs.  Each rank of a
+    W-GPU job answers its shard as its own batch (binned by its own AUTO decision), so every spatial and
+    index shard of W = 2, 4, 8 must reproduce the whole batch's bits at its queries."""
+    from paper_2109_14807_b200.shard import shard_range, spatial_owner
+    cfg, bins, f = config_inputs(3)
+    n = 2_000_000
+    recs = synth.gen_queries(cfg, bins, 0, n)
+    whole, _ = run_gpu(desc_args(cfg), f, recs, 2)  # BIN_ON, like the full config-3 batch
+    for W in (2, 4, 8):
+        owner = spatial_owner(recs["u"], cfg.N, W)
+        for k in (0, W - 1):
+            idx = np.nonzero(owner == k)[0]
+            got, _ = run_gpu(desc_args(cfg), f, recs[idx], 0)  # AUTO, as the rank would run it
+            assert got.tobytes() == whole[idx].tobytes(), (W, k, "spatial")
+        i0, i1 = shard_range(n, W - 1, W)
+        got, _ = run_gpu(desc_args(cfg), f, recs[i0:i1], 4)  # BIN_OFF
+        assert got.tobytes() == whole[i0:i1].tobytes(), (W, "index")
+
+
 def test_host_pipeline_matches_device_path():
     pndf = _pndf()
     cfg, bins, f = config_inputs(3)
