@@ -10,6 +10,7 @@
 #include <cmath>
 #include <vector>
 #include <mutex>
+#include <cstdlib>
 #include <new>
 
 #include "internal.cuh"
@@ -859,14 +860,25 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
     if (n == 0) return PNDF_OK;
     std::lock_guard<std::mutex> lk(s->mu);
     DeviceGuard g(s->device);
-    // chunk so that >= 8 chunks overlap when the batch allows, 1M..64M records each
-    // Chunking: >= 8 chunks overlap H2D / kernels / D2H on the three slot streams.  When the
-    // whole batch qualifies for binning, chunks are made large enough (>= 4 queries per
-    // positional row) to be binned on their own; otherwise 1M..64M records each.
+    // Chunking: chunks overlap H2D / kernels / D2H on the three slot streams.  When the whole
+    // batch qualifies for binning, chunks of n/32 records, but at least 2 queries per positional
+    // row so each is still binned on its own (config 5: 44.7M-record chunks, 3.07 G queries/s
+    // end to end vs 2.77 with 8 chunks at >= 4 queries/row; measured grid in DESIGN.md);
+    // otherwise 1M..64M records each (n/8).
     const bool bin_all = want_bins(s, n, opts);
+    static const int64_t kChunks = [] {  // binned chunk count (PNDF_E2E_CHUNKS, for A/B runs)
+        const char* e = getenv("PNDF_E2E_CHUNKS");
+        const int v = e ? atoi(e) : 32;
+        return (int64_t)(v >= 2 && v <= 64 ? v : 32);
+    }();
+    static const int64_t kMinQ = [] {  // binned chunks hold >= kMinQ queries per row (PNDF_E2E_MINQ)
+        const char* e = getenv("PNDF_E2E_MINQ");
+        const int v = e ? atoi(e) : 2;
+        return (int64_t)(v >= 1 && v <= 64 ? v : 2);
+    }();
     int64_t chunk;
     if (bin_all && !(opts & PNDF_BIN_ON))
-        chunk = std::max<int64_t>(4 * s->P, (n + 7) / 8);
+        chunk = std::max<int64_t>(kMinQ * s->P, (n + kChunks - 1) / kChunks);
     else
         chunk = std::max<int64_t>(int64_t(1) << 20, std::min<int64_t>(int64_t(1) << 26, (n + 7) / 8));
     chunk = std::min(chunk, n);
@@ -881,7 +893,7 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
             if (chunk > fit) chunk = std::max<int64_t>(int64_t(1) << 20, fit);
         }
     }
-    const bool binned = (opts & PNDF_BIN_ON) ? true : (bin_all && chunk >= 4 * s->P);
+    const bool binned = (opts & PNDF_BIN_ON) ? true : (bin_all && chunk >= kMinQ * s->P);
     const uint32_t chunk_opts = (opts & PNDF_SUM) | (binned ? PNDF_BIN_ON : PNDF_BIN_OFF);
     for (auto& sl : s->slots) {
         if (!sl.st) CK(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
