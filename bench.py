@@ -757,6 +757,31 @@ WANG_METRIC = "Wang-tiled NDF range queries/sec (Sec. 5.5: implicit 16-tile map,
 WANG_SAMPLE_METRIC = "Wang-tiled NDF importance samples/sec (Sec. 5.5, P:454: equal-probability covered tile + hierarchical descent)"
 
 
+def wang_rows_touched(tc, recs) -> np.ndarray:
+    """Zc rows the tiled kernels read per record (reading 21/25): for each level of positive weight and each
+    neighbour of positive weight, the tiles whose stored rows (within 2 cells of the tile) hold it."""
+    S = recs["size"].astype(np.float64)
+    ls = np.clip(np.log2(S / tc.s0), 0.0, tc.L - 1)
+    l0 = np.minimum(np.floor(ls), tc.L - 2).astype(np.int64)
+    t = ls - l0
+    rows = np.zeros(recs.shape[0], np.int64)
+    for dl in (0, 1):
+        l = l0 + dl
+        wl = t if dl else 1.0 - t
+        s = (tc.s0 << l).astype(np.float64)
+        nl = (tc.T // (tc.s0 << l)).astype(np.int64)
+        cnt = []
+        for c in ("u", "v"):
+            f = recs[c].astype(np.float64) / s - 0.5
+            i0 = np.floor(f).astype(np.int64)
+            a = f - i0
+            per = [(i0 + k + 2) // nl - (i0 + k - 2) // nl + 1 for k in (0, 1)]
+            cnt.append((per[0], per[1] * (a > 0)))
+        tot = (cnt[0][0] + cnt[0][1]) * (cnt[1][0] + cnt[1][1])
+        rows += np.where(wl > 0, tot, 0)
+    return rows
+
+
 def run_wang_op(args, cfg, rank, world, local_rank):
     """--op wang: range queries on an implicitly Wang-tiled 102400^2 map (16 tiles of 512^2, A=64, R=32)."""
     import torch
@@ -846,6 +871,20 @@ def run_wang_op(args, cfg, rank, world, local_rank):
         err = np.abs(got - ref)
         passed = bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())
         unit, kern = "queries/s", "pndf::tiled_query_kernel"
+    # algorithmic bytes: record + result, the Zc rows of every overlapped tile, and the angular rows
+    # (one range-table row per axis for the narrow query rectangles; for whole-image sampling the 4
+    # domain-corner SAT rows plus 2 midpoint rows per descent level)
+    rows_mean = float(wang_rows_touched(tc, recs[idx]).mean())
+    Rp, levels = st["rank_padded"], int(round(math.log2(tc.A)))
+    Bq = (32 + 4 * Rp * (rows_mean + 4 + 2 * levels)) if sample else (20 + 4 * Rp * (rows_mean + 2))
+    k_ms = st["query_ms"] / max(1, st["timed_batches"])
+    hbm = measured_peaks()[0]["hbm_gbs"]
+    achieved = Bq * n / (k_ms * 1e-3) / 1e9
+    wang_roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
+                 "traffic": None, "kernel": kern, "kernel_ms": k_ms, "bytes_per_query": Bq,
+                 "zc_rows_per_query_mean": rows_mean,
+                 "note": "16 tiles' Zc %.0f MB (> L2); bytes per record from the positive-weight Zc rows (all "
+                         "overlapped tiles' rows), measured on the parity sample" % (st["zc_bytes"] / 1e6)}
     line = {"metric": WANG_SAMPLE_METRIC if sample else WANG_METRIC, "value": n_total / (ms_step * 1e-3),
             "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -855,11 +894,7 @@ def run_wang_op(args, cfg, rank, world, local_rank):
                                    + (", whole-image sampling domain" if sample else ""),
                        "queries_total": n_total, "rows": int(st["rows"]),
                        "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]]},
-            "roofline": {"bound": "hbm", "achieved": None, "peak": measured_peaks()[0]["hbm_gbs"], "unit": "GB/s",
-                         "frac": None, "traffic": None, "kernel": kern,
-                         "kernel_ms": st["query_ms"] / max(1, st["timed_batches"]),
-                         "note": "16 tiles' Zc %.0f MB; Zc rows per query grow with the footprint (tiles overlapped)"
-                                 % (st["zc_bytes"] / 1e6)},
+            "roofline": wang_roof,
             "cpu_baseline": {"value": cpu_rate, "unit": unit, "cores": oracle.max_threads(),
                              "kind": "oracle", "sample": f"{idx.shape[0]} records of the timed batch"},
             "gpu_launches": args.steps, "clocks": clk,
