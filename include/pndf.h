@@ -246,8 +246,12 @@ pndf_status pndf_load_tiles(const pndf_tile_desc* desc, const float* C, const fl
  *   d_xi   DEVICE [n][11] fp32 in [0,1), caller-supplied
  *   d_out  DEVICE [n] pndf_sample
  *   d_tile DEVICE [n][2] int32 (tx, ty) of the chosen instance, or NULL
- * opts: 0 or PNDF_TIMING (never binned).  Enqueued on cuda_stream; complete
- * with pndf_sync; invalid records give NaN + the sticky PNDF_EQUERY. */
+ * opts: PNDF_TIMING; PNDF_BIN_OFF keeps the caller's order (by default batches
+ * of >= 65536 records are first sorted by footprint level -- a stable 8-bit
+ * radix pass -- so the lanes of a warp sample footprints of one size; results
+ * land at out[i] for record i either way, bitwise identical).  Enqueued on
+ * cuda_stream; complete with pndf_sync; invalid records give NaN + the sticky
+ * PNDF_EQUERY. */
 pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
                               pndf_sample* d_out, int32_t* d_tile, uint32_t opts, void* cuda_stream);
 

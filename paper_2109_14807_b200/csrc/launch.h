@@ -41,8 +41,11 @@ cudaError_t launch_sample_hilo_clamp(int G, int NV, const QParams& p, const pndf
 cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q, int64_t n,
                                float* out, int num_sms, cudaStream_t st);
 cudaError_t launch_tiled_sample(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
-                                const float* xi, int64_t n, pndf_sample* out, int32_t* tile_out, int num_sms,
-                                cudaStream_t st);
+                                const float* xi, const uint32_t* idx, int64_t n, pndf_sample* out,
+                                int32_t* tile_out, int num_sms, cudaStream_t st);
+// Stable sort of a batch by footprint level (query.cu): perm = records in level order.
+cudaError_t launch_level_sort(const QParams& p, const pndf_query* q, int64_t n, BinScratch& sc, cudaStream_t st,
+                              int* launches, const uint32_t** perm);
 
 // Blocked / clustered store (blocks.cu).
 cudaError_t launch_blocked_query(const QParams& p, const BlockParams& bp, int G, int NV, const pndf_query* q,

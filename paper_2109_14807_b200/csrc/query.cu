@@ -397,6 +397,45 @@ static void radix_pass(const uint32_t* kin, const uint32_t* vin, int64_t n, int 
         launch_scatter<BITS, 256, false>(kin, vin, n, shift, sc.counts, ntiles, kout, vout, st);
 }
 
+// Level sort for the Wang-tile sampler: key = the record's lower level l0 (255 = invalid), the tile
+// histogram fused as in bin_keys_kernel, then one stable 8-bit radix pass -> permutation.  Lanes of a
+// warp then sample footprints of the same size, whose row loops have similar trip counts.
+__global__ void __launch_bounds__(kRsThreads) level_keys_kernel(const QParams p, const pndf_query* __restrict__ q,
+                                                                int64_t n, uint32_t* keys, uint32_t* counts,
+                                                                int64_t ntiles) {
+    __shared__ uint32_t h[256];
+    for (int d = threadIdx.x; d < 256; d += kRsThreads) h[d] = 0;
+    __syncthreads();
+    const int64_t t0 = (int64_t)blockIdx.x * kRsTile;
+    for (int i = 0; i < kRsItems; ++i) {
+        const int64_t k = t0 + (int64_t)i * kRsThreads + threadIdx.x;
+        if (k >= n) continue;
+        const pndf_query rec = ldg_query(q + k);
+        int x1, x2, y1, y2;
+        uint32_t key = 255u;
+        if (record_valid(p, rec, x1, x2, y1, y2)) {
+            int l0;
+            float t;
+            level_select(p, rec.size, l0, t);
+            key = (uint32_t)l0;
+        }
+        keys[k] = key;
+        atomicAdd(&h[key], 1u);
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < 256; d += kRsThreads) counts[(int64_t)d * ntiles + blockIdx.x] = h[d];
+}
+
+cudaError_t launch_level_sort(const QParams& p, const pndf_query* q, int64_t n, BinScratch& sc, cudaStream_t st,
+                              int* launches, const uint32_t** perm) {
+    const int64_t ntiles = radix_tiles(n);
+    level_keys_kernel<<<(unsigned)ntiles, kRsThreads, 0, st>>>(p, q, n, sc.keys[0], sc.counts, ntiles);
+    radix_pass<8>(sc.keys[0], nullptr, n, 0, sc, ntiles, nullptr, sc.vals[1], true, st);
+    *launches += 5;
+    *perm = sc.vals[1];
+    return cudaGetLastError();
+}
+
 int64_t bin_key_space(int64_t P, int* half) {
     // half-cell keys (4 per cell) when they fit in 32 bits, else cell keys
     *half = (4 * P + 1 < (int64_t)0xffffffffLL) ? 1 : 0;

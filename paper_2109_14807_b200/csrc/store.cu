@@ -786,7 +786,7 @@ pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const f
 pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
                               pndf_sample* d_out, int32_t* d_tile, uint32_t opts, void* cuda_stream) {
     if (!s || n < 0 || (n > 0 && (!d_queries || !d_xi || !d_out))) return PNDF_EINVAL;
-    if (opts & ~PNDF_TIMING) return PNDF_EINVAL;  // tiled batches are never binned
+    if (opts & ~(PNDF_TIMING | PNDF_BIN_OFF)) return PNDF_EINVAL;
     if (!s->tiled) return PNDF_EINVAL;
     if (n == 0) return PNDF_OK;
     if ((uintptr_t)d_queries % 16 != 0 || (uintptr_t)d_out % 16 != 0 || (uintptr_t)d_xi % 4 != 0 ||
@@ -796,10 +796,15 @@ pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const f
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const bool timing = (opts & PNDF_TIMING) != 0;
-    if (timing) {
-        CK(cudaEventRecord(s->ev[0], st));
-        CK(cudaEventRecord(s->ev[1], st));
+    // level sort (default for batches >= 64K): lanes of a warp then sample footprints of one size,
+    // so their tile-row loops have similar trip counts; PNDF_BIN_OFF samples in the caller's order
+    const bool sorted = !(opts & PNDF_BIN_OFF) && n >= (int64_t(1) << 16);
+    const int64_t step = int64_t(1) << 30;
+    if (sorted) {
+        pndf_status r = ensure_scratch(s->main, std::min(n, step), st);
+        if (r != PNDF_OK) return r;
     }
+    if (timing) CK(cudaEventRecord(s->ev[0], st));
     // lanes per sample as in pndf_sample_batch: 8 float4 per lane with U32 SATs (the Wang workload, R = 32:
     // one lane per sample, 4.8e8 vs 3.1e8 samples/s at the query kernel's 8 lanes); pndf_set_lanes overrides
     int sg = s->G, snv = s->NV;
@@ -807,17 +812,21 @@ pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const f
         sg = s->Rp / 32;
         snv = 8;
     }
-    const int64_t step = int64_t(1) << 30;
     int launches = 0;
+    bool first = true;
     for (int64_t a = 0; a < n; a += step) {
         const int64_t m = std::min(step, n - a);
-        CK(launch_tiled_sample(s->qp, s->tp, sg, snv, d_queries + a, d_xi + (size_t)a * 11, m, d_out + a,
+        const uint32_t* perm = nullptr;
+        if (sorted) CK(launch_level_sort(s->qp, d_queries + a, m, s->main, st, &launches, &perm));
+        if (timing && first) CK(cudaEventRecord(s->ev[1], st));
+        CK(launch_tiled_sample(s->qp, s->tp, sg, snv, d_queries + a, d_xi + (size_t)a * 11, perm, m, d_out + a,
                                d_tile ? d_tile + 2 * a : nullptr, s->num_sms, st));
         launches += 1;
+        first = false;
     }
     if (timing) CK(cudaEventRecord(s->ev[2], st));
     s->stats.kernel_launches += (uint64_t)launches;
-    s->stats.last_binned = 0;
+    s->stats.last_binned = sorted ? 1 : 0;
     s->timing_pending = timing;
     return PNDF_OK;
 }

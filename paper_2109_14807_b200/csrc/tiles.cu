@@ -194,7 +194,8 @@ __device__ __forceinline__ float group_sum_m(float v, unsigned gmask) {
 template <int G, int NV, bool U32>
 __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, const TileParams tp,
                                                            const pndf_query* __restrict__ q,
-                                                           const float* __restrict__ xi, int64_t n,
+                                                           const float* __restrict__ xi,
+                                                           const uint32_t* __restrict__ idx, int64_t n,
                                                            pndf_sample* __restrict__ out,
                                                            int32_t* __restrict__ tile_out) {
     constexpr int QPW = 32 / G;
@@ -210,13 +211,14 @@ __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, cons
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t base = gw * QPW; base < n; base += nw * QPW) {  // warp-uniform trip count
-        const int64_t si = base + grp;
-        const bool active = si < n;
-        const pndf_query rec = ldg_query(q + (active ? si : 0));
+        const int64_t qi = base + grp;
+        const bool active = qi < n;
+        const int64_t si = active ? (idx ? (int64_t)__ldg(idx + qi) : qi) : 0;  // record (level-sorted order)
+        const pndf_query rec = ldg_query(q + si);
         int x1, x2, y1, y2;
         bool valid = active && record_valid(p, rec, x1, x2, y1, y2);
         if (!valid) x1 = x2 = y1 = y2 = 0;
-        const float* sxi = xi + (size_t)(active ? si : 0) * 11;
+        const float* sxi = xi + (size_t)si * 11;
         int l0;
         float t;
         level_select(p, valid ? rec.size : 1.f, l0, t);
@@ -471,49 +473,50 @@ __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, cons
 }
 
 template <int G, int NV, bool U>
-static cudaError_t launch_ts(const QParams& p, const TileParams& tp, const pndf_query* q, const float* xi, int64_t n,
-                             pndf_sample* out, int32_t* tile_out, int num_sms, cudaStream_t st) {
+static cudaError_t launch_ts(const QParams& p, const TileParams& tp, const pndf_query* q, const float* xi,
+                             const uint32_t* idx, int64_t n, pndf_sample* out, int32_t* tile_out, int num_sms,
+                             cudaStream_t st) {
     const int64_t spb = 8 * (32 / G);
     int64_t grid = (n + spb - 1) / spb;
     if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
     if (grid < 1) grid = 1;
-    tiled_sample_kernel<G, NV, U><<<(unsigned)grid, 256, 0, st>>>(p, tp, q, xi, n, out, tile_out);
+    tiled_sample_kernel<G, NV, U><<<(unsigned)grid, 256, 0, st>>>(p, tp, q, xi, idx, n, out, tile_out);
     return cudaGetLastError();
 }
 
 template <int G, bool U>
 static cudaError_t ts_nv(int NV, const QParams& p, const TileParams& tp, const pndf_query* q, const float* xi,
-                         int64_t n, pndf_sample* out, int32_t* to, int sms, cudaStream_t st) {
+                         const uint32_t* ix, int64_t n, pndf_sample* out, int32_t* to, int sms, cudaStream_t st) {
     switch (NV) {
-        case 1: return launch_ts<G, 1, U>(p, tp, q, xi, n, out, to, sms, st);
-        case 2: return launch_ts<G, 2, U>(p, tp, q, xi, n, out, to, sms, st);
-        case 3: return launch_ts<G, 3, U>(p, tp, q, xi, n, out, to, sms, st);
-        case 4: return launch_ts<G, 4, U>(p, tp, q, xi, n, out, to, sms, st);
-        case 8: return launch_ts<G, 8, U>(p, tp, q, xi, n, out, to, sms, st);
+        case 1: return launch_ts<G, 1, U>(p, tp, q, xi, ix, n, out, to, sms, st);
+        case 2: return launch_ts<G, 2, U>(p, tp, q, xi, ix, n, out, to, sms, st);
+        case 3: return launch_ts<G, 3, U>(p, tp, q, xi, ix, n, out, to, sms, st);
+        case 4: return launch_ts<G, 4, U>(p, tp, q, xi, ix, n, out, to, sms, st);
+        case 8: return launch_ts<G, 8, U>(p, tp, q, xi, ix, n, out, to, sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
 template <bool U>
 static cudaError_t ts_g(int G, int NV, const QParams& p, const TileParams& tp, const pndf_query* q, const float* xi,
-                        int64_t n, pndf_sample* out, int32_t* to, int sms, cudaStream_t st) {
+                        const uint32_t* ix, int64_t n, pndf_sample* out, int32_t* to, int sms, cudaStream_t st) {
     switch (G) {
-        case 1: return ts_nv<1, U>(NV, p, tp, q, xi, n, out, to, sms, st);
-        case 2: return ts_nv<2, U>(NV, p, tp, q, xi, n, out, to, sms, st);
-        case 4: return ts_nv<4, U>(NV, p, tp, q, xi, n, out, to, sms, st);
-        case 8: return ts_nv<8, U>(NV, p, tp, q, xi, n, out, to, sms, st);
-        case 16: return ts_nv<16, U>(NV, p, tp, q, xi, n, out, to, sms, st);
-        case 32: return ts_nv<32, U>(NV, p, tp, q, xi, n, out, to, sms, st);
+        case 1: return ts_nv<1, U>(NV, p, tp, q, xi, ix, n, out, to, sms, st);
+        case 2: return ts_nv<2, U>(NV, p, tp, q, xi, ix, n, out, to, sms, st);
+        case 4: return ts_nv<4, U>(NV, p, tp, q, xi, ix, n, out, to, sms, st);
+        case 8: return ts_nv<8, U>(NV, p, tp, q, xi, ix, n, out, to, sms, st);
+        case 16: return ts_nv<16, U>(NV, p, tp, q, xi, ix, n, out, to, sms, st);
+        case 32: return ts_nv<32, U>(NV, p, tp, q, xi, ix, n, out, to, sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
 cudaError_t launch_tiled_sample(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
-                                const float* xi, int64_t n, pndf_sample* out, int32_t* tile_out, int num_sms,
-                                cudaStream_t st) {
+                                const float* xi, const uint32_t* idx, int64_t n, pndf_sample* out,
+                                int32_t* tile_out, int num_sms, cudaStream_t st) {
     if (4 * G * NV != p.Rp) return cudaErrorInvalidValue;
-    if (p.prefix_u32) return ts_g<true>(G, NV, p, tp, q, xi, n, out, tile_out, num_sms, st);
-    return ts_g<false>(G, NV, p, tp, q, xi, n, out, tile_out, num_sms, st);
+    if (p.prefix_u32) return ts_g<true>(G, NV, p, tp, q, xi, idx, n, out, tile_out, num_sms, st);
+    return ts_g<false>(G, NV, p, tp, q, xi, idx, n, out, tile_out, num_sms, st);
 }
 
 template <int G, int NV, bool U>

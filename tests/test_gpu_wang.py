@@ -110,3 +110,30 @@ def test_tiled_sample_parity(prefix):
     assert st.sync(raise_on_query_error=False) == pndf.EQUERY
     assert np.isnan(out[0, 2].item())
     st.free()
+
+
+def test_tiled_sample_level_sort_is_bitwise_neutral():
+    """Batches >= 65536 are sampled in footprint-level order (pndf_sample_tiles' level sort): every
+    record's sample, pdf and chosen tile must be bitwise those of the unsorted (PNDF_BIN_OFF) run."""
+    pndf = _pndf()
+    tc = synth.TileConfig(T=128)
+    f = synth.wang_factors(tc, synth.wang_tiles(tc))
+    n = 200_000
+    recs = _tile_queries(tc, n, 9)
+    recs["rect"][::3] = synth.pack_rect(0, tc.A - 1, 0, tc.A - 1)
+    recs["size"][5] = float("nan")  # one invalid record: NaN wherever it lands in the sorted order
+    xi = torch.from_numpy(np.random.default_rng(10).random((n, 11), dtype=np.float32)).cuda()
+    st = pndf.load_tiles(pndf.make_tile_desc(tc.T, tc.s0, tc.L, tc.margin, tc.A, tc.R, tc.seed), f.C, f.X, f.Y, f.Z)
+    outs = []
+    for opts in (0, pndf.BIN_OFF):
+        out = torch.full((n, 4), -1.0, dtype=torch.float32, device="cuda")
+        tile = torch.full((n, 2), -99, dtype=torch.int32, device="cuda")
+        st.sample_tiles(torch_records(recs), xi, out, tile, opts)
+        assert st.sync(raise_on_query_error=False) == pndf.EQUERY
+        outs.append((out.cpu().numpy(), tile.cpu().numpy()))
+        if opts == 0:
+            assert st.stats()["last_binned"] == 1
+    assert outs[0][0].tobytes() == outs[1][0].tobytes()
+    assert np.array_equal(outs[0][1], outs[1][1])
+    assert np.isnan(outs[0][0][5, 2]) and (outs[0][0][:, 3].view(np.uint32) != 0xffffffff).sum() > n // 4
+    st.free()
