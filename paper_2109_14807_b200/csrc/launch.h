@@ -38,8 +38,8 @@ cudaError_t launch_sample_hilo_clamp(int G, int NV, const QParams& p, const pndf
                                   const uint32_t* idx, int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
 
 // Wang-tiled query (tiles.cu).
-cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q, int64_t n,
-                               float* out, int num_sms, cudaStream_t st);
+cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
+                               const uint32_t* idx, int64_t n, float* out, int num_sms, cudaStream_t st);
 cudaError_t launch_tiled_sample(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
                                 const float* xi, const uint32_t* idx, int64_t n, pndf_sample* out,
                                 int32_t* tile_out, int num_sms, cudaStream_t st);

@@ -195,14 +195,24 @@ pndf_status enqueue(pndf_store_s* s, Scratch& sc, const pndf_query* q, int64_t n
         s->stats.last_binned = 0;
         return PNDF_OK;
     }
-    if (s->tiled) {  // Wang-tiled world queries: one kernel, never binned
+    if (s->tiled) {  // Wang-tiled world queries: not binned by cell; batches >= 64K sorted by level
         if (opts & PNDF_BIN_ON) return PNDF_EINVAL;
+        // level sort (as in pndf_sample_tiles): the lanes of a warp then serve footprints of one size,
+        // whose tile-row loops have similar trip counts; PNDF_BIN_OFF keeps the caller's order
+        const bool sorted = !(opts & PNDF_BIN_OFF) && n >= (int64_t(1) << 16) && n <= (int64_t(1) << 30);
+        int launches = 1;
+        const uint32_t* perm = nullptr;
+        if (sorted) {
+            pndf_status r = ensure_scratch(sc, n, st);
+            if (r != PNDF_OK) return r;
+        }
         if (timing) CK(cudaEventRecord(s->ev[0], st));
+        if (sorted) CK(launch_level_sort(p, q, n, sc, st, &launches, &perm));
         if (timing) CK(cudaEventRecord(s->ev[1], st));
-        CK(launch_tiled_query(p, s->tp, s->G, s->NV, q, n, out, s->num_sms, st));
+        CK(launch_tiled_query(p, s->tp, s->G, s->NV, q, perm, n, out, s->num_sms, st));
         if (timing) CK(cudaEventRecord(s->ev[2], st));
-        s->stats.kernel_launches += 1;
-        s->stats.last_binned = 0;
+        s->stats.kernel_launches += (uint64_t)launches;
+        s->stats.last_binned = sorted ? 1 : 0;
         return PNDF_OK;
     }
     const bool binned = want_bins(s, n, opts);

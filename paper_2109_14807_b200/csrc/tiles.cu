@@ -34,7 +34,8 @@ __device__ __forceinline__ int tile_of(uint64_t seed_mixed, int64_t cx, int64_t 
 
 template <int G, int NV, bool U32>
 __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const TileParams tp,
-                                                          const pndf_query* __restrict__ q, int64_t n,
+                                                          const pndf_query* __restrict__ q,
+                                                          const uint32_t* __restrict__ idx, int64_t n,
                                                           float* __restrict__ out) {
     constexpr int QPW = 32 / G;
     constexpr int RP = 4 * G * NV;
@@ -52,9 +53,10 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
     const int64_t gw = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t base = gw * QPW; base < n; base += nw * QPW) {
-        const int64_t qi = base + grp;
-        const bool active = qi < n;
-        const pndf_query rec = ldg_query(q + (active ? qi : 0));
+        const int64_t qo = base + grp;
+        const bool active = qo < n;
+        const int64_t qi = active ? (idx ? (int64_t)__ldg(idx + qo) : qo) : 0;  // record (level-sorted order)
+        const pndf_query rec = ldg_query(q + qi);
         int x1, x2, y1, y2;
         const bool valid = active && record_valid(p, rec, x1, x2, y1, y2);
         float4 zh[NV];
@@ -520,48 +522,48 @@ cudaError_t launch_tiled_sample(const QParams& p, const TileParams& tp, int G, i
 }
 
 template <int G, int NV, bool U>
-static cudaError_t launch_t(const QParams& p, const TileParams& tp, const pndf_query* q, int64_t n, float* out,
-                            int num_sms, cudaStream_t st) {
+static cudaError_t launch_t(const QParams& p, const TileParams& tp, const pndf_query* q, const uint32_t* idx,
+                            int64_t n, float* out, int num_sms, cudaStream_t st) {
     const int64_t qpb = 8 * (32 / G);
     int64_t grid = (n + qpb - 1) / qpb;
     if (grid > (int64_t)num_sms * 8) grid = (int64_t)num_sms * 8;
     if (grid < 1) grid = 1;
-    tiled_query_kernel<G, NV, U><<<(unsigned)grid, 256, 0, st>>>(p, tp, q, n, out);
+    tiled_query_kernel<G, NV, U><<<(unsigned)grid, 256, 0, st>>>(p, tp, q, idx, n, out);
     return cudaGetLastError();
 }
 
 template <int G, bool U>
-static cudaError_t t_nv(int NV, const QParams& p, const TileParams& tp, const pndf_query* q, int64_t n, float* out,
-                        int sms, cudaStream_t st) {
+static cudaError_t t_nv(int NV, const QParams& p, const TileParams& tp, const pndf_query* q, const uint32_t* ix,
+                        int64_t n, float* out, int sms, cudaStream_t st) {
     switch (NV) {
-        case 1: return launch_t<G, 1, U>(p, tp, q, n, out, sms, st);
-        case 2: return launch_t<G, 2, U>(p, tp, q, n, out, sms, st);
-        case 3: return launch_t<G, 3, U>(p, tp, q, n, out, sms, st);
-        case 4: return launch_t<G, 4, U>(p, tp, q, n, out, sms, st);
-        case 8: return launch_t<G, 8, U>(p, tp, q, n, out, sms, st);
+        case 1: return launch_t<G, 1, U>(p, tp, q, ix, n, out, sms, st);
+        case 2: return launch_t<G, 2, U>(p, tp, q, ix, n, out, sms, st);
+        case 3: return launch_t<G, 3, U>(p, tp, q, ix, n, out, sms, st);
+        case 4: return launch_t<G, 4, U>(p, tp, q, ix, n, out, sms, st);
+        case 8: return launch_t<G, 8, U>(p, tp, q, ix, n, out, sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
 template <bool U>
-static cudaError_t t_g(int G, int NV, const QParams& p, const TileParams& tp, const pndf_query* q, int64_t n,
-                       float* out, int sms, cudaStream_t st) {
+static cudaError_t t_g(int G, int NV, const QParams& p, const TileParams& tp, const pndf_query* q,
+                       const uint32_t* ix, int64_t n, float* out, int sms, cudaStream_t st) {
     switch (G) {
-        case 1: return t_nv<1, U>(NV, p, tp, q, n, out, sms, st);
-        case 2: return t_nv<2, U>(NV, p, tp, q, n, out, sms, st);
-        case 4: return t_nv<4, U>(NV, p, tp, q, n, out, sms, st);
-        case 8: return t_nv<8, U>(NV, p, tp, q, n, out, sms, st);
-        case 16: return t_nv<16, U>(NV, p, tp, q, n, out, sms, st);
-        case 32: return t_nv<32, U>(NV, p, tp, q, n, out, sms, st);
+        case 1: return t_nv<1, U>(NV, p, tp, q, ix, n, out, sms, st);
+        case 2: return t_nv<2, U>(NV, p, tp, q, ix, n, out, sms, st);
+        case 4: return t_nv<4, U>(NV, p, tp, q, ix, n, out, sms, st);
+        case 8: return t_nv<8, U>(NV, p, tp, q, ix, n, out, sms, st);
+        case 16: return t_nv<16, U>(NV, p, tp, q, ix, n, out, sms, st);
+        case 32: return t_nv<32, U>(NV, p, tp, q, ix, n, out, sms, st);
         default: return cudaErrorInvalidValue;
     }
 }
 
-cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q, int64_t n,
-                               float* out, int num_sms, cudaStream_t st) {
+cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
+                               const uint32_t* idx, int64_t n, float* out, int num_sms, cudaStream_t st) {
     if (4 * G * NV != p.Rp) return cudaErrorInvalidValue;
-    if (p.prefix_u32) return t_g<true>(G, NV, p, tp, q, n, out, num_sms, st);
-    return t_g<false>(G, NV, p, tp, q, n, out, num_sms, st);
+    if (p.prefix_u32) return t_g<true>(G, NV, p, tp, q, idx, n, out, num_sms, st);
+    return t_g<false>(G, NV, p, tp, q, idx, n, out, num_sms, st);
 }
 
 }  // namespace pndf

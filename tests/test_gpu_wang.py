@@ -137,3 +137,24 @@ def test_tiled_sample_level_sort_is_bitwise_neutral():
     assert np.array_equal(outs[0][1], outs[1][1])
     assert np.isnan(outs[0][0][5, 2]) and (outs[0][0][:, 3].view(np.uint32) != 0xffffffff).sum() > n // 4
     st.free()
+
+
+def test_tiled_query_level_sort_is_bitwise_neutral():
+    """Tiled query batches >= 65536 run in footprint-level order; results must be bitwise those of the
+    caller's-order run (PNDF_BIN_OFF), including the NaN of an invalid record."""
+    pndf = _pndf()
+    tc = synth.TileConfig(T=128)
+    f = synth.wang_factors(tc, synth.wang_tiles(tc))
+    n = 200_000
+    recs = _tile_queries(tc, n, 11)
+    recs["size"][7] = -2.0
+    st = pndf.load_tiles(pndf.make_tile_desc(tc.T, tc.s0, tc.L, tc.margin, tc.A, tc.R, tc.seed), f.C, f.X, f.Y, f.Z)
+    res = []
+    for opts in (0, pndf.BIN_OFF):
+        out = torch.full((n,), -1.0, dtype=torch.float32, device="cuda")
+        st.query_batch(torch_records(recs), out, opts)
+        assert st.sync(raise_on_query_error=False) == pndf.EQUERY
+        assert st.stats()["last_binned"] == (1 if opts == 0 else 0)
+        res.append(out.cpu().numpy())
+    assert res[0].tobytes() == res[1].tobytes() and np.isnan(res[0][7])
+    st.free()
