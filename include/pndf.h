@@ -186,7 +186,7 @@ typedef struct {
     int32_t prefix_format;    /* 0 = HILO, 1 = U32                              */
     int64_t range_table_bytes;/* bytes of the narrow-range difference table DT  */
     int32_t range_table_width;/* W: ranges of <= W bins read one DT row (0 = no table) */
-    int32_t pad;
+    int32_t tile_reach;       /* tiled stores: cells beyond a tile holding a nonzero row (else 0) */
 } pndf_store_stats;
 pndf_status pndf_store_stats_get(pndf_store s, pndf_store_stats* out);
 pndf_status pndf_store_stats_reset(pndf_store s);
@@ -223,9 +223,18 @@ typedef struct {
 } pndf_tile_desc;
 
 /* Build a tiled store (Z = [16 * P_ext][R], other arguments as pndf_load_factors).
- * pndf_query_batch / pndf_query_batch_host answer world-space queries on it
- * (never binned); pndf_sample_batch returns PNDF_EINVAL for tiled stores (use
- * pndf_sample_tiles). */
+ * The load measures the store's reach: the largest distance (in cells of its
+ * level, beyond the tile's own n_l x n_l cells) of any row with a nonzero entry,
+ * 0 <= reach <= margin (pndf_store_stats.tile_reach).  Rows further out are all
+ * zero, so the kernels skip them and the sum over every tile whose extended grid
+ * holds a neighbour stays exact for any margin.
+ * pndf_query_batch / pndf_query_batch_host answer world-space queries on it;
+ * they are not binned by cell, but device batches of >= 65536 records are first
+ * sorted by footprint level (one stable radix pass; results bitwise identical to
+ * the caller's order, which PNDF_BIN_OFF keeps, and which the host entry
+ * pndf_query_batch_host always uses).  A batch captured into a CUDA graph before
+ * the store has sort scratch for its size runs unsorted.  pndf_sample_batch
+ * returns PNDF_EINVAL for tiled stores (use pndf_sample_tiles). */
 pndf_status pndf_load_tiles(const pndf_tile_desc* desc, const float* C, const float* X, const float* Y,
                             const float* Z, int device, void* cuda_stream, pndf_store* out);
 
@@ -236,7 +245,8 @@ pndf_status pndf_load_tiles(const pndf_tile_desc* desc, const float* C, const fl
  * s must be a tiled store (else PNDF_EINVAL).  Record i as in pndf_sample_batch
  * (world footprint; rect = the sampling domain).  The covered tile instances
  * are the world cells (tx, ty) holding a row the tiled query reads with
- * positive weight (a neighbour within 2 cells of the tile), ordered by
+ * positive weight and positive domain mass (a neighbour within `reach` cells
+ * of the tile; PNDF_EINVAL if the store's reach exceeds 4), ordered by
  * (ty, tx); the c-th is chosen with c = floor(xi[i][10] * count) (fp32),
  * then the hierarchical descent of pndf_sample_batch runs on that tile's
  * partial NDF with xi[i][0..7] and jitters with xi[i][8], xi[i][9].  pdf is

@@ -48,6 +48,8 @@ struct TileParams {
     int32_t margin;   // extended cells per side
     int64_t p_ext;    // rows per tile
     uint64_t seed;    // vertex-hash seed
+    int32_t reach;    // cells beyond the tile border that hold a nonzero row (<= margin), measured at
+                      // load: rows further out are all zero, so skipping them is exact
 };
 
 // Blocked / clustered store (blocks.cu).

@@ -43,6 +43,10 @@ cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, in
 cudaError_t launch_tiled_sample(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
                                 const float* xi, const uint32_t* idx, int64_t n, pndf_sample* out,
                                 int32_t* tile_out, int num_sms, cudaStream_t st);
+// Reach of a tiled store (tiles.cu): the largest distance, in cells beyond the tile's own grid
+// (0 = inside), of any row with a nonzero entry, over all tiles and levels -> *reach (device).
+cudaError_t launch_tile_reach(const float* Zc, int Rp, const TileParams& tp, int n0, int L, uint32_t* reach,
+                              cudaStream_t st);
 // Stable sort of a batch by footprint level (query.cu): perm = records in level order.
 cudaError_t launch_level_sort(const QParams& p, const pndf_query* q, int64_t n, BinScratch& sc, cudaStream_t st,
                               int* launches, const uint32_t** perm);

@@ -25,9 +25,9 @@ struct __align__(16) QDesc {
 };
 static_assert(sizeof(QDesc) == 96, "QDesc layout");
 
-// returns the reuse key (0xffffffff = never equal to a neighbour's)
+// returns false for an invalid record (its descriptor then yields NaN)
 template <bool WRAP, bool USE_DT>  // USE_DT: narrow ranges read the range table (not with TMA staging)
-__device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& rec, int32_t out_index, QDesc& d) {
+__device__ __forceinline__ bool decode(const QParams& p, const pndf_query& rec, int32_t out_index, QDesc& d) {
     int x1, x2, y1, y2;
     if (!record_valid(p, rec, x1, x2, y1, y2)) {
         atomicOr(p.err, 1u);
@@ -41,12 +41,11 @@ __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& r
         d.mode = 0;
         d.div = __int_as_float(0x7fc00000);
         d.out = out_index;
-        return 0xffffffffu;
+        return false;
     }
     int l0;
     float t;
     level_select(p, rec.size, l0, t);
-    int r0 = 0, r3 = 0, r4 = 0, r7 = 0;
 #pragma unroll
     for (int dl = 0; dl < 2; ++dl) {
         const int l = l0 + dl;
@@ -61,13 +60,6 @@ __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& r
         d.row[4 * dl + 1] = off + j0 * n + i1;
         d.row[4 * dl + 2] = off + j1 * n + i0;
         d.row[4 * dl + 3] = off + j1 * n + i1;
-        if (dl == 0) {
-            r0 = off + j0 * n + i0;
-            r3 = off + j1 * n + i1;
-        } else {
-            r4 = off + j0 * n + i0;
-            r7 = off + j1 * n + i1;
-        }
         const float wa = wl * (1.f - a), wb = wl * a;
         d.w[4 * dl + 0] = wa * (1.f - b);
         d.w[4 * dl + 1] = wb * (1.f - b);
@@ -89,9 +81,39 @@ __device__ __forceinline__ uint32_t decode(const QParams& p, const pndf_query& r
     }
     d.div = p.mean ? (float)((x2 - x1 + 1) * (y2 - y1 + 1)) : 1.f;
     d.out = out_index;
-    if (WRAP) return cell_key(p, rec, l0, 1) & 0x7fffffffu;
-    // clamped borders: (i0, j0, i1, j1) on both levels pin the 8 rows; hash them
-    return (uint32_t)(r0 * 0x9E3779B1u ^ r3 * 0x85EBCA77u ^ r4 * 0xC2B2AE3Du ^ r7 * 0x27D4EB2Fu) & 0x7fffffffu;
+    return true;
+}
+
+// Which of a warp's 32 decoded queries repeat the previous query's Zc rows, per level:
+// bit j of *same_lo = query j has query j-1's 4 level-l0 rows, *same_hi likewise for level l0+1.
+// A level's 4 rows are fixed by its first and last row: (i0, j0) and (i1, j1) give (i1, j0) and
+// (i0, j1).  With wrapped borders the first alone fixes them (i1 = i0 + 1 mod n), but clamped borders
+// map f in [-1/2, 0) to cells (0, 0) and f in [0, 1) to (0, 1): same first row, different others,
+// so CLAMP compares both.  Equal rows imply the same level (levels own disjoint row ranges).
+template <bool WRAP>
+__device__ __forceinline__ void reuse_masks(const QDesc& d, bool valid, bool first_ok, int32_t prev_lo,
+                                            int32_t prev_lo3, int32_t prev_hi, int32_t prev_hi3,
+                                            uint32_t* same_lo, uint32_t* same_hi, int32_t (&mine)[4]) {
+    mine[0] = valid ? d.row[0] : -1;
+    mine[1] = valid ? d.row[3] : -1;
+    mine[2] = valid ? d.row[4] : -1;
+    mine[3] = valid ? d.row[7] : -1;
+    int32_t plo = __shfl_up_sync(0xffffffffu, mine[0], 1), phi = __shfl_up_sync(0xffffffffu, mine[2], 1);
+    int32_t plo3 = 0, phi3 = 0;
+    if (!WRAP) {
+        plo3 = __shfl_up_sync(0xffffffffu, mine[1], 1);
+        phi3 = __shfl_up_sync(0xffffffffu, mine[3], 1);
+    }
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) {  // the query before lane 0 (previous 32-query batch of a segment; -1 = none)
+        plo = prev_lo;
+        plo3 = prev_lo3;
+        phi = prev_hi;
+        phi3 = prev_hi3;
+    }
+    const bool ok = first_ok && valid;
+    *same_lo = __ballot_sync(0xffffffffu, ok && mine[0] == plo && (WRAP || mine[1] == plo3));
+    *same_hi = __ballot_sync(0xffffffffu, ok && mine[2] == phi && (WRAP || mine[3] == phi3));
 }
 
 // Reduce NB per-lane partials v[0..NB) over the G lanes of each group by
@@ -238,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
     const int64_t wlen = (((chunk + kWarpsPerBlock - 1) / kWarpsPerBlock) + 31) / 32 * 32;
     const int64_t ws = c0 + (int64_t)warp * wlen;
     const int64_t c1 = min(min(n, c0 + chunk), ws + wlen);
-    int32_t prev_lo = -1, prev_hi = -1;
+    int32_t prev_r[4] = {-1, -1, -1, -1};
     for (int64_t base = ws; base < c1; base += 32) {
 #else
     const int64_t c1 = min(n, c0 + chunk);
@@ -247,12 +269,12 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
         // 1. decode 32 records, one per lane
         {
             const int64_t qi = base + lane;
-            uint32_t key = 0xffffffffu;
+            bool valid = false;
             if (qi < c1) {
                 // binned: idx is the radix-sorted permutation; gather the record through it
                 const int64_t src = BINNED ? (int64_t)__ldg(idx + qi) : qi;
                 const pndf_query rec = ldg_query(q + src);
-                key = decode<WRAP, !TMA>(p, rec, (int32_t)src, wd[lane]);
+                valid = decode<WRAP, !TMA>(p, rec, (int32_t)src, wd[lane]);
             } else {
                 wd[lane].out = -1;
 #pragma unroll
@@ -265,34 +287,24 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
                 wd[lane].mode = 0;
                 wd[lane].div = 1.f;
             }
-#if PNDF_PREUSE
-            // the 4 rows of each level are fixed by the level's first row: reuse per level when it
-            // repeats (same l0 cell -> rows 0-3, same l0+1 cell -> rows 4-7)
-            const bool kv = key != 0xffffffffu;
-            const int32_t klo = kv ? wd[lane].row[0] : -1, khi = kv ? wd[lane].row[4] : -1;
-            int32_t plo = __shfl_up_sync(0xffffffffu, klo, 1), phi = __shfl_up_sync(0xffffffffu, khi, 1);
+            uint32_t same_lo, same_hi;
+            int32_t mine[4];
 #if PNDF_WSEG
-            if (lane == 0) {  // the previous batch's last query (its rows are still in zc)
-                plo = prev_lo;
-                phi = prev_hi;
-            }
-            prev_lo = __shfl_sync(0xffffffffu, klo, 31);
-            prev_hi = __shfl_sync(0xffffffffu, khi, 31);
-            const bool first_ok = true;
+            // the previous batch's last query (its rows are still in zc)
+            reuse_masks<WRAP>(wd[lane], valid, true, prev_r[0], prev_r[1], prev_r[2], prev_r[3], &same_lo,
+                              &same_hi, mine);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) prev_r[e] = __shfl_sync(0xffffffffu, mine[e], 31);
 #else
-            const bool first_ok = lane > 0;
+            reuse_masks<WRAP>(wd[lane], valid, lane > 0, -1, -1, -1, -1, &same_lo, &same_hi, mine);
 #endif
-            const uint32_t same_lo = __ballot_sync(0xffffffffu, first_ok && kv && klo == plo);
-            const uint32_t same_hi = __ballot_sync(0xffffffffu, first_ok && kv && khi == phi);
+#if !PNDF_PREUSE
+            same_lo = same_hi = same_lo & same_hi;  // all 8 rows or none
+#endif
             if (lane == 0) {
                 sreuse[2 * warp] = same_lo;
                 sreuse[2 * warp + 1] = same_hi;
             }
-#else
-            const uint32_t prev = __shfl_up_sync(0xffffffffu, key, 1);
-            const uint32_t same = __ballot_sync(0xffffffffu, lane > 0 && key == prev && key != 0xffffffffu);
-            if (lane == 0) sreuse[2 * warp] = sreuse[2 * warp + 1] = same;
-#endif
         }
         __syncwarp();
         const uint32_t reuse_mask = (G == 32) ? (sreuse[2 * warp] & sreuse[2 * warp + 1]) : 0u;

@@ -153,11 +153,14 @@ void choose_lanes(int R, int* G, int* NV) {
     *NV = nv;
 }
 
+bool capturing(cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    return st && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone;
+}
+
 pndf_status ensure_scratch(Scratch& s, int64_t n, cudaStream_t st) {
     if (s.cap >= n && s.counts) return PNDF_OK;
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    if (st && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone)
-        return PNDF_EINVAL;  // no allocation while a CUDA graph is being captured
+    if (capturing(st)) return PNDF_EINVAL;  // no allocation while a CUDA graph is being captured
     s.release();
     const int64_t nb = radix_tiles(n) * 512;
     for (int i = 0; i < 2; ++i) {
@@ -199,7 +202,10 @@ pndf_status enqueue(pndf_store_s* s, Scratch& sc, const pndf_query* q, int64_t n
         if (opts & PNDF_BIN_ON) return PNDF_EINVAL;
         // level sort (as in pndf_sample_tiles): the lanes of a warp then serve footprints of one size,
         // whose tile-row loops have similar trip counts; PNDF_BIN_OFF keeps the caller's order
-        const bool sorted = !(opts & PNDF_BIN_OFF) && n >= (int64_t(1) << 16) && n <= (int64_t(1) << 30);
+        // (results are bitwise identical either way, so a batch captured into a CUDA graph before the
+        // sort scratch exists -- no allocation during capture -- simply runs unsorted)
+        const bool sorted = !(opts & PNDF_BIN_OFF) && n >= (int64_t(1) << 16) && n <= (int64_t(1) << 30) &&
+                            (sc.cap >= n || !capturing(st));
         int launches = 1;
         const uint32_t* perm = nullptr;
         if (sorted) {
@@ -342,7 +348,27 @@ pndf_status pndf_load_tiles(const pndf_tile_desc* td, const float* C, const floa
     s->tp.margin = td->margin;
     s->tp.p_ext = pext;
     s->tp.seed = td->seed;
+    s->tp.reach = td->margin;
     s->qp.wrap = 0;
+    {  // measured reach: rows beyond it are all zero, so the kernels skip them exactly
+        cudaStream_t st = (cudaStream_t)cuda_stream;
+        DeviceGuard guard(device);
+        cudaError_t e = cudaMemsetAsync(s->err + 1, 0, sizeof(uint32_t), st);
+        if (e == cudaSuccess) e = launch_tile_reach(s->Zc, s->Rp, s->tp, (int)(td->tile_size / td->base_stride),
+                                                    td->num_levels, s->err + 1, st);
+        uint32_t reach = 0;
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (e == cudaSuccess) e = cudaMemcpy(&reach, s->err + 1, sizeof(uint32_t), cudaMemcpyDeviceToHost);
+        if (e == cudaSuccess) e = cudaMemsetAsync(s->err + 1, 0, sizeof(uint32_t), st);
+        if (e != cudaSuccess) {
+            destroy(s);
+            *out = nullptr;
+            return cuda_fail(e, "tile reach");
+        }
+        s->tp.reach = (int32_t)reach;
+        s->stats.tile_reach = (int32_t)reach;
+        s->stats.kernel_launches += 1;
+    }
     return PNDF_OK;
 }
 
@@ -806,9 +832,12 @@ pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const f
     DeviceGuard g(s->device);
     cudaStream_t st = (cudaStream_t)cuda_stream;
     const bool timing = (opts & PNDF_TIMING) != 0;
+    if (s->tp.reach > 4) return PNDF_EINVAL;  // candidate tiles exceed the kernel's 128-bit mask
     // level sort (default for batches >= 64K): lanes of a warp then sample footprints of one size,
     // so their tile-row loops have similar trip counts; PNDF_BIN_OFF samples in the caller's order
-    const bool sorted = !(opts & PNDF_BIN_OFF) && n >= (int64_t(1) << 16);
+    // (bitwise identical results, so a graph capture without sort scratch runs unsorted)
+    const bool sorted = !(opts & PNDF_BIN_OFF) && n >= (int64_t(1) << 16) &&
+                        (s->main.cap >= std::min(n, int64_t(1) << 30) || !capturing(st));
     const int64_t step = int64_t(1) << 30;
     if (sorted) {
         pndf_status r = ensure_scratch(s->main, std::min(n, step), st);

@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
                 const float wa = wl * (1.f - a), wb = wl * a;
                 const float wk4[4] = {wa * (1.f - b), wb * (1.f - b), wa * b, wb * b};
                 // candidate tiles of all 4 neighbours lie in one small box: hash each cell once
-                const int MA = M < 2 ? M : 2;
+                const int MA = tp.reach;  // rows beyond it are zero (measured at load)
                 const int bx0 = (iu - (nl + MA) + 1) >> sh, bx1 = (iu + 1 + MA) >> sh;
                 const int by0 = (iv - (nl + MA) + 1) >> sh, by1 = (iv + 1 + MA) >> sh;
                 const int bw = bx1 - bx0 + 1;
@@ -101,9 +101,9 @@ __global__ void __launch_bounds__(256) tiled_query_kernel(const QParams p, const
                 for (int k = 0; k < 4; ++k) {
                     const int iw = iu + (k & 1), jw = iv + (k >> 1);
                     const float wk = wk4[k];
-                    // tiles whose texels this centre's footprint reaches: local cell il in [-2, nl + 1]
-                    // (support +-4 sigma = +-1.73 cells around the centre at (il + 1/2) cells); rows
-                    // further out in the extended grid are zero and skipped (exact: they add +0)
+                    // tiles whose extended grid holds this centre with a possibly nonzero row: local cell
+                    // il in [-reach, nl + reach - 1]; rows further out are all zero (checked at load) and
+                    // skipped, which is exact (they would add +0)
                     const int tx0 = (iw - (nl + MA) + 1) >> sh, tx1 = (iw + MA) >> sh;
                     const int ty0 = (jw - (nl + MA) + 1) >> sh, ty1 = (jw + MA) >> sh;
                     for (int ty = ty0; ty <= ty1; ++ty)
@@ -203,7 +203,7 @@ __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, cons
     constexpr int QPW = 32 / G;
     constexpr int RP = 4 * G * NV;
     constexpr int PSTRIDE = U32 ? RP : 2 * RP;
-    constexpr int REACH = 2;  // stored rows reach 2 cells past the tile (+-4 sigma support)
+    const int REACH = tp.reach;  // rows beyond it are zero (measured at load; <= 4 for sampling)
     const int lane = threadIdx.x & 31, gl = lane % G, grp = lane / G;
     const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (grp * G));
     const float* __restrict__ PX = p.PXY;
@@ -256,7 +256,9 @@ __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, cons
             }
         }
         const int bw = bx1 - bx0 + 1;
-        if (valid && bw * (by1 - by0 + 1) > 64) valid = false;  // cannot happen for s0 2^l strides; guard
+        // the union box is at most 2 reach + 2 tiles per side: <= 100 candidates for reach <= 4
+        // (pndf_sample_tiles rejects larger reaches), held in a 128-bit mask
+        if (valid && bw * (by1 - by0 + 1) > 128) valid = false;
         // full-domain angular factor sum_x X_r sum_y Y_r (C folded into Zc)
         float4 full[NV];
         {
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, cons
         float4 zt[NV], za[NV];
 #pragma unroll
         for (int v = 0; v < NV; ++v) zt[v] = za[v] = make_float4(0.f, 0.f, 0.f, 0.f);
-        uint64_t mask = 0;
+        uint64_t mask = 0, mask_hi = 0;  // bits 0-63, 64-127 of the candidate box
 #pragma unroll
         for (int dl = 0; dl < 2; ++dl) {
             if (!use[dl]) continue;
@@ -311,18 +313,26 @@ __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, cons
                             m = fmaf(full[v].w, zr.w, m);
                         }
                         m = group_sum_m<G>(m, gmask);
-                        if (m > 0.f) mask |= 1ull << ((ty - by0) * bw + (tx - bx0));
+                        const int bit = (ty - by0) * bw + (tx - bx0);
+                        if (m > 0.f) {
+                            if (bit < 64)
+                                mask |= 1ull << bit;
+                            else
+                                mask_hi |= 1ull << (bit - 64);
+                        }
                     }
             }
         }
-        const int count = __popcll(mask);
+        const int count_lo = __popcll(mask);
+        const int count = count_lo + __popcll(mask_hi);
         int ptx = 0, pty = 0;
         if (count > 0) {
             int c = (int)floorf(__fmul_rn(__ldg(sxi + 10), (float)count));
             if (c > count - 1) c = count - 1;
-            uint64_t mm = mask;
-            for (int j = 0; j < c; ++j) mm &= mm - 1;  // drop the c lowest set bits
-            const int bit = __ffsll((long long)mm) - 1;
+            const bool in_lo = c < count_lo;
+            uint64_t mm = in_lo ? mask : mask_hi;
+            for (int j = in_lo ? c : c - count_lo; j > 0; --j) mm &= mm - 1;  // drop the lower set bits
+            const int bit = __ffsll((long long)mm) - 1 + (in_lo ? 0 : 64);
             ptx = bx0 + bit % bw;
             pty = by0 + bit / bw;
             // pass 2: Z-hat of the chosen tile (its rows only)
@@ -472,6 +482,45 @@ __global__ void __launch_bounds__(256) tiled_sample_kernel(const QParams p, cons
             }
         }
     }
+}
+
+// One thread per row of the 16 tiles' extended grids: a row with any nonzero entry raises *reach to
+// its distance beyond the tile's own cells (Chebyshev, in cells of its level).
+__global__ void tile_reach_kernel(const float* __restrict__ Zc, int Rp, TileParams tp, int n0, int L,
+                                  uint32_t* reach) {
+    const int64_t rows = 16 * tp.p_ext;
+    const int M = tp.margin;
+    for (int64_t z = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; z < rows; z += (int64_t)gridDim.x * blockDim.x) {
+        const float4* r4 = reinterpret_cast<const float4*>(Zc + (size_t)z * Rp);
+        bool nz = false;
+        for (int c = 0; c < Rp / 4 && !nz; ++c) {
+            const float4 v = __ldg(r4 + c);
+            nz = v.x != 0.f || v.y != 0.f || v.z != 0.f || v.w != 0.f;
+        }
+        if (!nz) continue;
+        int64_t k = z % tp.p_ext;
+        int l = 0;
+        int64_t ne = (int64_t)n0 + 2 * M;
+        while (l + 1 < L && k >= ne * ne) {
+            k -= ne * ne;
+            ++l;
+            ne = (int64_t)(n0 >> l) + 2 * M;
+        }
+        const int nl = n0 >> l;
+        const int il = (int)(k % ne) - M, jl = (int)(k / ne) - M;
+        const int d = max(max(max(-il, il - (nl - 1)), max(-jl, jl - (nl - 1))), 0);
+        if (d > 0) atomicMax(reach, (uint32_t)d);
+    }
+}
+
+cudaError_t launch_tile_reach(const float* Zc, int Rp, const TileParams& tp, int n0, int L, uint32_t* reach,
+                              cudaStream_t st) {
+    const int64_t rows = 16 * tp.p_ext;
+    int64_t grid = (rows + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    if (grid < 1) grid = 1;
+    tile_reach_kernel<<<(unsigned)grid, 256, 0, st>>>(Zc, Rp, tp, n0, L, reach);
+    return cudaGetLastError();
 }
 
 template <int G, int NV, bool U>

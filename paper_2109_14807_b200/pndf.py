@@ -60,7 +60,7 @@ class StoreStats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_uint64), ("timed_batches", ctypes.c_uint64),
                 ("query_ms", ctypes.c_double), ("bin_ms", ctypes.c_double), ("last_binned", ctypes.c_int32),
                 ("prefix_format", ctypes.c_int32),
-                ("range_table_bytes", ctypes.c_int64), ("range_table_width", ctypes.c_int32), ("pad", ctypes.c_int32)]
+                ("range_table_bytes", ctypes.c_int64), ("range_table_width", ctypes.c_int32), ("tile_reach", ctypes.c_int32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

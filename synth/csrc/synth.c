@@ -409,7 +409,7 @@ typedef struct {
     int32_t size_mix;        /* 0: log2 S ~ U[lg_lo, lg_hi]; 1: 50/50 of [lg_lo,lg_hi] and [lg_lo2,lg_hi2] */
     int32_t side_mode;       /* 0: sides ~ U{side_lo..side_hi}; 1: half-width w ~ U[w_lo,w_hi], side = max(1, floor(2w+1/2)) */
     int32_t side_lo, side_hi;
-    int32_t centre_mode;     /* 0: uniform placement; 1: centred on a random texel's bin w.p. p_texel (+-jitter);
+    int32_t centre_mode;     /* 0: uniform placement; 1: centred w.p. p_texel on the bin of the texel under the footprint centre (+-jitter);
                                 2: centred on the bin of a Beckmann(alpha_h) half vector */
     int32_t jitter;
     double lg_lo, lg_hi, lg_lo2, lg_hi2;
@@ -462,8 +462,9 @@ EXPORT void synth_gen_queries(const synth_qdist* q, uint64_t seed, int64_t i0, i
         int x1, x2, y1, y2;
         int centred = 0, cx = 0, cy = 0;
         if (q->centre_mode == 1 && bins && rng_unit(seed, 6, g) < q->p_texel) {
-            int64_t t = (int64_t)floor(rng_unit(seed, 7, g) * (double)N * (double)N);
-            if (t >= (int64_t)N * N) t = (int64_t)N * N - 1;
+            /* the normal of the texel under the footprint centre: the footprint's NDF holds it with
+               positive weight, so the rectangle sits on the footprint's own NDF support (glint queries) */
+            const int64_t t = (int64_t)r.v * N + (int64_t)r.u;
             cx = bins[t] % A; cy = bins[t] / A;
             if (q->jitter) {
                 cx += uniform_int(seed, 9, g, -q->jitter, q->jitter);

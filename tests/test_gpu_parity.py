@@ -39,6 +39,8 @@ SHAPES = [  # N, s0, L, A, R, wrap
     (8, 1, 4, 1, 1, True), (16, 1, 5, 5, 3, False), (64, 2, 6, 32, 8, True), (32, 1, 6, 64, 17, True),
     (128, 1, 8, 128, 64, False), (64, 1, 7, 256, 100, True), (32, 1, 6, 16, 256, True),
     (16, 1, 5, 8, 1024, True), (256, 4, 7, 8, 33, True), (64, 1, 3, 20, 12, False),
+    # clamped borders at G = 32 lanes (Rp >= 128), where consecutive queries reuse Zc rows per level
+    (64, 1, 7, 64, 128, False), (32, 1, 6, 48, 256, False), (64, 2, 5, 32, 200, False),
 ]
 
 
@@ -62,6 +64,40 @@ def test_random_store_parity(shape, mode):
             assert_parity(got, ref, f"{shape} opts={opts} prefix={prefix}")
 
 
+@pytest.mark.parametrize("R", [128, 256])
+def test_clamp_border_row_reuse(R):
+    """Clamped borders (P:274-276 neighbours, reading 4): f in [-1/2, 0) maps to cells (0, 0) and f in
+    [0, 1) to (0, 1), so two consecutive queries can share a level's first row but not its others.  The
+    G = 32 kernel keeps the previous query's rows in registers; it must not reuse them here.  Queries
+    alternate between the two sides of each border (both axes, both levels), in caller order (BIN_OFF)
+    and binned, at R = 128 (one float4 per lane) and 256 (two)."""
+    N, s0, L, A = 32, 1, 6, 16
+    P = sum((N >> l) ** 2 for l in range(L))
+    f = synth.random_factors(A, R, P, seed=R, sparsity=0.3)
+    rng = np.random.default_rng(R)
+    us, vs, Ss = [], [], []
+    for lg in np.linspace(0.0, L - 1.0, 11):
+        S = float(2.0 ** lg)
+        s_l = s0 * 2.0 ** np.floor(lg)
+        for edge in (0.0, float(N)):  # lower border, upper border (f in [n-1, n-1/2) vs [n-1/2, n))
+            for _ in range(6):
+                lo = rng.uniform(0.0, 0.5) * s_l if edge == 0.0 else N - rng.uniform(0.0, 0.5) * s_l
+                hi = rng.uniform(0.5, 1.5) * s_l if edge == 0.0 else N - rng.uniform(0.5, 1.5) * s_l
+                w = rng.uniform(0, N)
+                for a, b in ((lo, w), (hi, w), (w, lo), (w, hi), (lo, lo), (hi, hi), (lo, hi), (hi, lo)):
+                    us.append(a); vs.append(b); Ss.append(S)
+    n = len(us)
+    x1 = rng.integers(0, A, n); y1 = rng.integers(0, A, n)
+    recs = synth.make_records(np.array(us), np.array(vs), np.array(Ss), x1,
+                              np.minimum(A - 1, x1 + rng.integers(0, 4, n)), y1,
+                              np.minimum(A - 1, y1 + rng.integers(0, 4, n)))
+    ref = oracle.query_batch(oracle.make_desc(N, s0, L, A, R, False), f.C, f.X, f.Y, f.Z, recs)
+    for opts in (4, 2):  # BIN_OFF (caller order), BIN_ON
+        got, st = run_gpu(dict(N=N, s0=s0, L=L, A=A, R=R, wrap=False), f, recs, opts)
+        assert st == 0
+        assert_parity(got, ref, f"clamp reuse R={R} opts={opts}")
+
+
 @pytest.mark.parametrize("k", [1, 2])
 def test_config_full_parity(k):
     """Configs 1-2: every query of the batch, in both SAT formats."""
@@ -74,7 +110,10 @@ def test_config_full_parity(k):
         got, st = run_gpu(desc_args(cfg), f, recs, 0, prefix=prefix, want_format=want)
         assert st == 0
         stats = assert_parity(got, ref, f"config {k} prefix={prefix}")
-        assert stats["zeros"] < 0.9 * stats["n"]  # not dominated by blank-region queries
+        # not dominated by blank-region queries: >= 45% of the results are nonzero (measured: config 1
+        # 62%, config 2 50% -- half the rectangles sit on the bin of the texel under the footprint centre)
+        assert stats["zeros"] <= 0.55 * stats["n"]
+        assert stats["max_rel_nonzero"] <= 1e-4
         got_b, _ = run_gpu(desc_args(cfg), f, recs, 2, prefix=prefix)
         assert got_b.tobytes() == got.tobytes()  # binning never changes a bit
 

@@ -158,3 +158,106 @@ def test_tiled_query_level_sort_is_bitwise_neutral():
         res.append(out.cpu().numpy())
     assert res[0].tobytes() == res[1].tobytes() and np.isnan(res[0][7])
     st.free()
+
+
+def _random_tile_store(T, s0, L, margin, A, R, seed, outer_zero_beyond=None):
+    """Random nonnegative tiled factors whose rows are nonzero out to the whole margin (or, with
+    outer_zero_beyond = d, zero beyond d cells past the tile)."""
+    P_ext = sum(((T // s0 >> l) + 2 * margin) ** 2 for l in range(L))
+    f = synth.random_factors(A, R, 16 * P_ext, seed=seed, sparsity=0.3)
+    if outer_zero_beyond is not None:
+        Z = f.Z.reshape(16, P_ext, R)
+        off = 0
+        for l in range(L):
+            nl = T // s0 >> l
+            ne = nl + 2 * margin
+            jl, il = np.divmod(np.arange(ne * ne), ne)
+            il, jl = il - margin, jl - margin
+            d = np.maximum(np.maximum(np.maximum(-il, il - (nl - 1)), np.maximum(-jl, jl - (nl - 1))), 0)
+            Z[:, off + np.flatnonzero(d > outer_zero_beyond), :] = 0
+            off += ne * ne
+    return f
+
+
+@pytest.mark.parametrize("margin,zero_beyond", [(3, None), (4, None), (4, 1), (6, None)])
+def test_tiled_store_full_margin(margin, zero_beyond):
+    """pndf.h: a tiled query sums every tile whose extended grid holds each neighbour ("all
+    overlapping Wang tiles").  A random store with nonzero rows out to the whole margin (the synthetic
+    flake tiles stop at 2 cells) must match the oracle, which sums every margin row; the measured reach
+    is the margin (or the zeroed ring's inner edge).  The sampler covers reach <= 4 and rejects larger."""
+    pndf = _pndf()
+    T, s0, L, A, R, seed = 8, 1, 4, 16, 8, 5
+    f = _random_tile_store(T, s0, L, margin, A, R, seed=margin, outer_zero_beyond=zero_beyond)
+    want_reach = margin if zero_beyond is None else zero_beyond
+    rng = np.random.default_rng(margin)
+    n = 6000
+    world = 40 * T
+    x1 = rng.integers(0, A, n)
+    y1 = rng.integers(0, A, n)
+    recs = synth.make_records(rng.uniform(0, world, n), rng.uniform(0, world, n), np.exp2(rng.uniform(0, L + 1, n)),
+                              x1, np.minimum(A - 1, x1 + rng.integers(0, 5, n)), y1,
+                              np.minimum(A - 1, y1 + rng.integers(0, 5, n)))
+    td_o = oracle.TilesDesc(T=T, s0=s0, L=L, margin=margin, A=A, R=R, seed=seed)
+    ref = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, recs)
+    for prefix in (0, 2):
+        st = pndf.load_tiles(pndf.make_tile_desc(T, s0, L, margin, A, R, seed, prefix=prefix), f.C, f.X, f.Y, f.Z)
+        assert st.stats()["tile_reach"] == want_reach
+        out = torch.full((n,), float("nan"), dtype=torch.float32, device="cuda")
+        st.query_batch(torch_records(recs), out, 0)
+        st.sync()
+        assert_parity(out.cpu().numpy(), ref, f"tiled margin={margin} prefix={prefix}")
+        xi_np = np.random.default_rng(margin + 1).random((n, 11), dtype=np.float32)
+        xi = torch.from_numpy(xi_np).cuda()
+        so = torch.full((n, 4), float("nan"), dtype=torch.float32, device="cuda")
+        tile = torch.full((n, 2), -99, dtype=torch.int32, device="cuda")
+        if want_reach > 4:
+            with pytest.raises(pndf.PndfError):
+                st.sample_tiles(torch_records(recs), xi, so, tile)
+            st.free()
+            continue
+        st.sample_tiles(torch_records(recs), xi, so, tile)
+        st.sync()
+        st.free()
+        sref = oracle.tiled_sample_batch(td_o, f.C, f.X, f.Y, f.Z, recs, xi_np)
+        np.testing.assert_array_equal(tile.cpu().numpy(), sref["tile"])  # tile choice: exact
+        o = so.cpu().numpy()
+        pixel = o[:, 3].view(np.uint32)
+        ok = pixel != 0xffffffff
+        assert np.array_equal(~ok, sref["pixel"][:, 0] < 0)
+        gx, gy = (pixel & 0xffff).astype(np.int64), (pixel >> 16).astype(np.int64)
+        firm = ok & (sref["margin"] > 1e-4)
+        assert firm.sum() > 0.9 * ok.sum()
+        assert np.array_equal(gx[firm], sref["pixel"][firm, 0]) and np.array_equal(gy[firm], sref["pixel"][firm, 1])
+        pix = recs[ok].copy()
+        pix["rect"] = synth.pack_rect(gx[ok], gx[ok], gy[ok], gy[ok])
+        num = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, pix, mean=False)
+        den = oracle.tiled_query_batch(td_o, f.C, f.X, f.Y, f.Z, recs[ok], mean=False)
+        assert_parity(o[ok, 2].astype(np.float64), num / den * (A * A / 4.0), f"tiled pdf margin={margin}")
+
+
+def test_tiled_capture_without_scratch_runs_unsorted():
+    """A tiled batch >= 65536 captured into a CUDA graph before the store has sort scratch runs in the
+    caller's order (no allocation during capture) and gives the same bits as the sorted run."""
+    pndf = _pndf()
+    tc = synth.TileConfig(T=128)
+    f = synth.wang_factors(tc, synth.wang_tiles(tc))
+    n = 100_000
+    recs = _tile_queries(tc, n, 21)
+    st = pndf.load_tiles(pndf.make_tile_desc(tc.T, tc.s0, tc.L, tc.margin, tc.A, tc.R, tc.seed), f.C, f.X, f.Y, f.Z)
+    assert st.stats()["tile_reach"] == 2
+    q = torch_records(recs)
+    out = torch.zeros(n, dtype=torch.float32, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s):
+            st.query_batch(q, out, 0, stream=s)
+        g.replay()
+        s.synchronize()
+    captured = out.cpu().numpy().copy()
+    out2 = torch.zeros(n, dtype=torch.float32, device="cuda")
+    st.query_batch(q, out2, 0)
+    st.sync()
+    assert st.stats()["last_binned"] == 1
+    assert captured.tobytes() == out2.cpu().numpy().tobytes()
+    st.free()

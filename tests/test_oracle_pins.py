@@ -428,3 +428,86 @@ def test_full_domain_normalisation_config1_als():
                               0, cfg.A - 1, 0, cfg.A - 1)
     q = oracle.query_batch(oracle.desc_of(cfg), f.C, f.X, f.Y, f.Z, recs, mean=False)
     np.testing.assert_allclose(q, 1.0, rtol=3e-6)
+
+
+# ----------------------------------------------------- helper-path pins --
+@pytest.mark.parametrize("wrap", [True, False])
+def test_neighbours_reproduce_position_and_level(wrap):
+    """oracle.neighbours (steps 1-2 on their own, used to pick the rows of sparse samples): the 8 weights
+    are a partition of unity split (1-t, t) between the two levels (t linear in log2 S, P:276/P:327,
+    clamped at the pyramid ends); each row lies in its level's range; and bilinear weights have
+    linear precision: at each level, sum_k w_k centre_k = (u, v) for interior points, with
+    centre (i+1/2, j+1/2) s_l decoded from the row index (so a wrong offset, axis swap or phase fails)."""
+    N, s0, L = 64, 2, 6
+    d = _store_desc(N, s0, L, 4, 1, wrap)
+    offs = np.cumsum([0] + [(N // s0 >> l) ** 2 for l in range(L)])
+    rng = np.random.default_rng(11)
+    n = 4000
+    lgS = rng.uniform(-1.0, L + 1.0, n)
+    S = np.exp2(lgS).astype(np.float32)
+    lstar = np.clip(np.log2(S.astype(np.float64) / s0), 0, L - 1)
+    l0 = np.minimum(np.floor(lstar), L - 2).astype(np.int64)
+    t = lstar - l0
+    s_hi = (s0 << (l0 + 1)).astype(np.float64)  # interior margin at the coarser level
+    u = (rng.uniform(0, 1, n) * np.maximum(N - 2 * s_hi, 0) + np.minimum(s_hi, N / 2)).astype(np.float32)
+    v = (rng.uniform(0, 1, n) * np.maximum(N - 2 * s_hi, 0) + np.minimum(s_hi, N / 2)).astype(np.float32)
+    recs = synth.make_records(u, v, S, 0, 0, 0, 0)
+    rows, w = oracle.neighbours(d, recs)
+    np.testing.assert_allclose(w.sum(1), 1.0, rtol=0, atol=1e-12)
+    np.testing.assert_allclose(w[:, :4].sum(1), 1.0 - t, rtol=0, atol=1e-12)
+    for dl in (0, 1):
+        l = l0 + dl
+        r = rows[:, 4 * dl:4 * dl + 4]
+        assert ((r >= offs[l][:, None]) & (r < offs[l + 1][:, None])).all()
+        n_l = (N // s0) >> l
+        k = r - offs[l][:, None]
+        ci = (k % n_l[:, None] + 0.5) * (s0 << l)[:, None]
+        cj = (k // n_l[:, None] + 0.5) * (s0 << l)[:, None]
+        ww = w[:, 4 * dl:4 * dl + 4]
+        tot = ww.sum(1)
+        m = (tot > 1e-9) & (N - 2 * s_hi > 0)  # interior points exist below the top level
+        np.testing.assert_allclose((ww * ci).sum(1)[m] / tot[m], u[m].astype(np.float64), rtol=0, atol=1e-9)
+        np.testing.assert_allclose((ww * cj).sum(1)[m] / tot[m], v[m].astype(np.float64), rtol=0, atol=1e-9)
+    bad = synth.make_records([np.nan], [1.0], [1.0], 0, 0, 0, 0)
+    rb, wb = oracle.neighbours(d, bad)
+    assert (rb == -1).all() and np.isnan(wb).all()
+
+
+def test_sparse_z_path_equals_dense():
+    """The sparse-Z path (zmap: only the rows a sample touches, used by the config-5 parity and bench
+    samples) returns the dense path's bits, for rows gathered by oracle.neighbours; a record needing a row
+    the sample lacks is NaN (never a silent zero)."""
+    cfg, bins = synth.CONFIGS[2], None
+    nxy = synth.make_map(cfg)
+    bins = synth.bin_map(cfg, nxy)
+    f = synth.build_factors(cfg, nxy, bins)
+    recs = synth.gen_queries(cfg, bins, 0, 30_000)
+    d = oracle.desc_of(cfg)
+    dense = oracle.query_batch(d, f.C, f.X, f.Y, f.Z, recs)
+    rows, _ = oracle.neighbours(d, recs)
+    Zs, zmap = oracle.sparse_z(rows.ravel(), cfg.P, lambda u: f.Z[u])
+    assert Zs.shape[0] < cfg.P // 2
+    sparse = oracle.query_batch(d, f.C, f.X, f.Y, Zs, recs, zmap=zmap)
+    assert sparse.tobytes() == dense.tobytes()
+    # drop one needed row: exactly the records that use it become NaN
+    drop = rows[0, 0]
+    zmap2 = zmap.copy()
+    zmap2[drop] = -1
+    got = oracle.query_batch(d, f.C, f.X, f.Y, Zs, recs, zmap=zmap2)
+    uses = (rows == drop).any(1)
+    assert np.isnan(got[uses]).all() and got[~uses].tobytes() == dense[~uses].tobytes()
+
+
+def test_rectangles_mostly_on_the_footprint_support():
+    """parity must not be dominated by trivially zero blank-region queries.  On configs 1-4
+    (oracle on 20K queries of each stream) at least 45% of the results are nonzero."""
+    for k in (1, 2, 3, 4):
+        cfg = synth.CONFIGS[k]
+        if k >= 3:
+            cfg = cfg.scaled(N=512)
+        nxy = synth.make_map(cfg)
+        bins = synth.bin_map(cfg, nxy)
+        f = synth.build_factors(cfg, nxy, bins)
+        recs = synth.gen_queries(cfg, bins, 0, 20_000)
+        ref = oracle.query_batch(oracle.desc_of(cfg), f.C, f.X, f.Y, f.Z, recs)
+        assert (ref > 0).mean() >= 0.45, (k, (ref > 0).mean())
