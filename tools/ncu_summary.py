@@ -27,6 +27,11 @@ def main(rep, nq=None):
             i = hdr.index(w)
             res[w] = (v[i], units[i])
             print(f"{w:60s} {v[i]:>22s} {units[i]}")
+    stalls = sorted(((float(v[i].replace(",", "") or 0), h) for i, h in enumerate(hdr)
+                     if h.startswith("smsp__average_warps_issue_stalled_") and h.endswith("_per_issue_active.ratio")
+                     and v[i].replace(",", "").replace(".", "").isdigit()), reverse=True)
+    for val, h in stalls[:8]:
+        print(f"  stall {h[len('smsp__average_warps_issue_stalled_'):-len('_per_issue_active.ratio')]:24s} {val:8.3f} per issue")
     if nq:
         ins = float(res["smsp__inst_executed.sum"][0].replace(",", ""))
         print(f"warp-instructions per query: {ins / nq:.1f}")
