@@ -10,10 +10,6 @@ namespace pndf {
 
 bool lanes_supported(int G, int NV);
 
-// PNDF_NORING=1 in the environment: G == 32 launches use query_kernel instead of the ring-staged
-// query_ring_kernel (A/B experiments; results are bitwise identical either way).
-bool ring_disabled();
-
 // Query kernel over n records; idx != nullptr means the records are binned
 // and idx[i] is record i's position in the caller's output.
 cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,

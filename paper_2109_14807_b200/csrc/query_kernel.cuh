@@ -556,338 +556,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
     }
 }
 
-// ------------------------------------- software-pipelined query kernel --
-// The G == 32 path (one query per warp step: Rp >= 128) with a range table.  Same arithmetic, order
-// and reduction tree as query_kernel, so results are bitwise identical to it; what changes is when
-// a5's angular rows are loaded.  query_kernel loads step s's two range-table rows (dx, dy) at step s
-// and stalls on them: its loads cannot be hoisted above step s-1's arithmetic because the per-level
-// Zc reuse branches split the steps into separate basic blocks.  Here step s issues step s+1's
-// rows into the other half of a 2-slot register buffer before its own Zc loads and arithmetic, so
-// one step of FFMA2 work covers their L2 latency.  The 32 extra registers need more than the 128 a
-// 2-CTA launch allows, so the kernel runs 384-thread CTAs, one per SM (170 registers).
-#ifndef PNDF_PF1
-#define PNDF_PF1 0  // 1: G == 32 launches with a range table use query_pf_kernel (measured slower)
-#endif
-#ifndef PNDF_PTHREADS
-#define PNDF_PTHREADS 384
-#endif
-#ifndef PNDF_PMINB
-#define PNDF_PMINB 1
-#endif
-#ifndef PNDF_PFREG
-#define PNDF_PFREG 1  // 1: next step's range-table rows in a register buffer; 0: loaded at their step;
-                      // 2: staged PNDF_CPD - 1 steps ahead in a per-warp shared-memory ring by cp.async
-#endif
-#ifndef PNDF_CPD
-#define PNDF_CPD 4  // PFREG == 2: cp.async ring depth (steps in flight per warp)
-#endif
-#ifndef PNDF_PFD
-#define PNDF_PFD 0  // > 0: prefetch (into L1) the range-table rows PFD steps ahead
-#endif
-#ifndef PNDF_PFZ
-#define PNDF_PFZ 2  // > 0: prefetch (into L1) the Zc rows a step PFZ steps ahead re-reads (no register cost)
-#endif
-#ifndef PNDF_PSTEPS
-#define PNDF_PSTEPS 8  // steps whose partials are reduced together (even)
-#endif
-constexpr int kPThreads = PNDF_PTHREADS;
-constexpr int kPWarps = kPThreads / 32;
-
-template <int NV>
-struct PfLayout {
-    static constexpr int RP = 128 * NV;
-    static constexpr int CPD = PNDF_PFREG == 2 ? PNDF_CPD : 0;  // cp.async ring slots per warp
-    static constexpr size_t DESC = sizeof(QDesc) * kPWarps * 32;
-    static constexpr size_t REUSE = 128 * ((8 * kPWarps + 127) / 128);
-    static constexpr size_t RING = (size_t)kPWarps * CPD * 2 * RP * 4;
-    static constexpr size_t BYTES = DESC + REUSE + RING;
-};
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <int NV, bool WRAP, bool BINNED, bool U32>
-__global__ void __launch_bounds__(kPThreads, PNDF_PMINB)
-    query_pf_kernel(const QParams p, const pndf_query* __restrict__ q, const uint32_t* __restrict__ idx, int64_t n,
-                    int64_t chunk, float* __restrict__ out) {
-    using LY = PfLayout<NV>;
-    constexpr int G = 32;
-    constexpr int RP = 128 * NV;
-    constexpr int SB = PNDF_PSTEPS;
-    static_assert(SB % 2 == 0 && 32 % SB == 0, "PNDF_PSTEPS");
-    static_assert(PNDF_PFREG != 2 || (PNDF_CPD >= 2 && SB % PNDF_CPD == 0), "PNDF_CPD must divide PNDF_PSTEPS");
-    constexpr int PSTRIDE = U32 ? RP : 2 * RP;
-    extern __shared__ __align__(128) unsigned char qsmem[];
-    QDesc(*sdesc)[32] = reinterpret_cast<QDesc(*)[32]>(qsmem);
-    uint32_t* sreuse = reinterpret_cast<uint32_t*>(qsmem + LY::DESC);
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    QDesc* wd = sdesc[warp];
-    const float* __restrict__ Zc = p.Zc;
-    const float* __restrict__ PXl = p.PXY + lane * 4;
-    const float* __restrict__ DTl = p.DT + lane * 4;
-    constexpr int CPD = LY::CPD;
-    // cp.async ring: slot k = [dx row | dy row]; each lane copies (and later reads) only its own
-    // 16-B chunks, so completion needs no more than the lane's own cp.async.wait_group
-    float* wring = reinterpret_cast<float*>(qsmem + LY::DESC + LY::REUSE) + (size_t)warp * CPD * 2 * RP + lane * 4;
-    auto stage = [&](const QDesc& d, int k) {
-        const int m = d.mode;
-        const int rx = (m & 1) ? d.sat[0] : 0, ry = (m & 2) ? d.sat[2] : 0;
-        float* dst = wring + k * 2 * RP;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            cp_async16(dst + v * G * 4, DTl + (int64_t)rx * RP + v * G * 4);
-            cp_async16(dst + RP + v * G * 4, DTl + (int64_t)ry * RP + v * G * 4);
-        }
-    };
-
-    // dbuf[slot][axis][v]: the range-table rows of step s live in slot s & 1
-    float4 dbuf[2][2][NV];
-    // unconditional loads (row 0 stands in for a wide range, whose SAT rows overwrite it at its step),
-    // so no buffer value stays live across steps
-    auto prefetch = [&](const QDesc& d, float4 (&b)[2][NV]) {
-        const int m = d.mode;
-        const int rx = (m & 1) ? d.sat[0] : 0, ry = (m & 2) ? d.sat[2] : 0;
-#pragma unroll
-        for (int v = 0; v < NV; ++v) {
-            b[0][v] = ldg4(DTl + (int64_t)rx * RP + v * G * 4);
-            b[1][v] = ldg4(DTl + (int64_t)ry * RP + v * G * 4);
-        }
-    };
-
-    // L1 prefetch of the rows step t will read, issued by the whole warp (one 128-B line per lane and
-    // instruction): its range-table rows (PFD) and the Zc rows of each level it does not reuse (PFZ)
-    constexpr int LPR = RP / 32;  // 128-B lines per row
-    auto prefetch_rows = [&](int t, uint32_t reuse_lo, uint32_t reuse_hi, bool dt_rows, bool z_rows) {
-        const QDesc& dn = wd[t];
-        if (dt_rows && lane < 2 * LPR) {
-            const int ax = lane / LPR, li = lane % LPR;
-            if ((dn.mode >> ax) & 1) prefetch_l1(p.DT + (size_t)dn.sat[2 * ax] * RP + li * 32);
-        }
-        if (z_rows) {
-            const bool r0 = t > 0 && ((reuse_lo >> t) & 1u), r1 = t > 0 && ((reuse_hi >> t) & 1u);
-#pragma unroll
-            for (int lv = 0; lv < 2; ++lv) {
-                if (lv ? !r1 : !r0) {
-#pragma unroll
-                    for (int i = lane; i < 4 * LPR; i += 32)
-                        prefetch_l1(Zc + (size_t)dn.row[4 * lv + i / LPR] * RP + (i % LPR) * 32);
-                }
-            }
-        }
-    };
-
-    const int64_t c0 = (int64_t)blockIdx.x * chunk;
-    const int64_t c1 = min(n, c0 + chunk);
-    float4 zc[NV][8];
-    for (int64_t base = c0 + (int64_t)warp * 32; base < c1; base += (int64_t)kPWarps * 32) {
-        {  // 1. decode 32 records, one per lane
-            const int64_t qi = base + lane;
-            bool valid = false;
-            QDesc& d = wd[lane];
-            if (qi < c1) {
-                const int64_t src = BINNED ? (int64_t)__ldg(idx + qi) : qi;
-                const pndf_query rec = ldg_query(q + src);
-                valid = decode<WRAP, true>(p, rec, (int32_t)src, d);
-            } else {
-                d.out = -1;
-#pragma unroll
-                for (int k = 0; k < 8; ++k) {
-                    d.row[k] = 0;
-                    d.w[k] = 0.f;
-                }
-#pragma unroll
-                for (int k = 0; k < 4; ++k) d.sat[k] = 0;
-                d.mode = 0;
-                d.div = 1.f;
-            }
-            uint32_t same_lo, same_hi;
-            int32_t mine[4];
-            reuse_masks<WRAP>(d, valid, lane > 0, -1, -1, -1, -1, &same_lo, &same_hi, mine);
-            if (lane == 0) {
-                sreuse[2 * warp] = same_lo;
-                sreuse[2 * warp + 1] = same_hi;
-            }
-        }
-        __syncwarp();
-        const uint32_t reuse_lo = sreuse[2 * warp];
-        const uint32_t reuse_hi = sreuse[2 * warp + 1];
-        if (PNDF_PFREG == 1) prefetch(wd[0], dbuf[0]);
-        if (PNDF_PFREG == 2) {
-#pragma unroll
-            for (int t = 0; t < CPD - 1; ++t) {
-                stage(wd[t], t);
-                cp_async_commit();
-            }
-        }
-        constexpr int PFA = PNDF_PFD > PNDF_PFZ ? PNDF_PFD : PNDF_PFZ;
-#pragma unroll
-        for (int t = 0; t < PFA; ++t) prefetch_rows(t, reuse_lo, reuse_hi, t < PNDF_PFD, t < PNDF_PFZ);
-        float res = 0.f;
-#pragma unroll 1
-        for (int s0 = 0; s0 < 32; s0 += SB) {
-            float part[SB];
-#pragma unroll
-            for (int j = 0; j < SB; ++j) {
-                const int s = s0 + j;
-                const int cur = j & 1;
-                const QDesc& d = wd[s];
-                const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
-                const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
-                const int dmode = d.mode;
-                const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
-                const bool reuse0 = s > 0 && ((reuse_lo >> s) & 1u);
-                const bool reuse1 = s > 0 && ((reuse_hi >> s) & 1u);
-                if (__builtin_expect(!(reuse0 && reuse1), 0)) {
-                    if (!reuse0) {
-                        const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
-                        const int row[4] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w};
-#pragma unroll
-                        for (int v = 0; v < NV; ++v)
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                zc[v][kk] = ldg4_stream(Zc + (size_t)row[kk] * RP + (lane + v * G) * 4);
-                    }
-                    if (!reuse1) {
-                        const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
-                        const int row[4] = {(int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
-#pragma unroll
-                        for (int v = 0; v < NV; ++v)
-#pragma unroll
-                            for (int kk = 0; kk < 4; ++kk)
-                                zc[v][4 + kk] = ldg4_stream(Zc + (size_t)row[kk] * RP + (lane + v * G) * 4);
-                    }
-                }
-                // loads are issued oldest-needed first (a warp's loads return in issue order): this step's
-                // Zc rows above, then this step's range-table rows (PFREG=0) or the next step's (PFREG=1),
-                // then the L1 prefetches of later steps
-                if (PNDF_PFREG == 0) prefetch(d, dbuf[0]);
-                if (PNDF_PFREG == 1 && s + 1 < 32) prefetch(wd[s + 1], dbuf[cur ^ 1]);
-                if (PNDF_PFREG == 2) {
-                    if (s + CPD - 1 < 32) stage(wd[s + CPD - 1], (j + CPD - 1) % (CPD > 0 ? CPD : 1));
-                    cp_async_commit();
-                    cp_async_wait<(CPD > 0 ? CPD - 1 : 0)>();  // this step's group has landed
-                    const float* sl = wring + (j % (CPD > 0 ? CPD : 1)) * 2 * RP;
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        dbuf[0][0][v] = *reinterpret_cast<const float4*>(sl + v * G * 4);
-                        dbuf[0][1][v] = *reinterpret_cast<const float4*>(sl + RP + v * G * 4);
-                    }
-                }
-                if (PNDF_PFD > 0 && s + PNDF_PFD < 32) prefetch_rows(s + PNDF_PFD, reuse_lo, reuse_hi, true, false);
-                if (PNDF_PFZ > 0 && s + PNDF_PFZ < 32) prefetch_rows(s + PNDF_PFZ, reuse_lo, reuse_hi, false, true);
-                float4 (&dv)[2][NV] = dbuf[PNDF_PFREG == 1 ? cur : 0];
-                if (__builtin_expect(dmode != 3, 0)) {  // a wide range: its two SAT rows, read now
-                    const int4 so = *reinterpret_cast<const int4*>(&d.sat[0]);
-#pragma unroll
-                    for (int v = 0; v < NV; ++v) {
-                        const int cv = v * G * 4;
-                        if (!(dmode & 1)) {
-                            const float* px0 = PXl + (int64_t)so.x * PSTRIDE;
-                            const float* px1 = PXl + (int64_t)so.y * PSTRIDE;
-                            if (U32) {
-                                const uint4 qx1 = ldg_sat(px1 + cv), qx0 = ldg_sat(px0 + cv);
-                                dv[0][v] = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
-                                                       __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
-                            } else {
-                                const float4 xh1 = ldg4(px1 + cv), xh0 = ldg4(px0 + cv);
-                                const float4 xl1 = ldg4(px1 + RP + cv), xl0 = ldg4(px0 + RP + cv);
-                                dv[0][v] = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
-                                                       (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
-                            }
-                        }
-                        if (!(dmode & 2)) {
-                            const float* py0 = PXl + (int64_t)so.z * PSTRIDE;
-                            const float* py1 = PXl + (int64_t)so.w * PSTRIDE;
-                            if (U32) {
-                                const uint4 qy1 = ldg_sat(py1 + cv), qy0 = ldg_sat(py0 + cv);
-                                dv[1][v] = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
-                                                       __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
-                            } else {
-                                const float4 yh1 = ldg4(py1 + cv), yh0 = ldg4(py0 + cv);
-                                const float4 yl1 = ldg4(py1 + RP + cv), yl0 = ldg4(py0 + RP + cv);
-                                dv[1][v] = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
-                                                       (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
-                            }
-                        }
-                    }
-                }
-                float2 acc2 = make_float2(0.f, 0.f);
-#pragma unroll
-                for (int v = 0; v < NV; ++v) {
-                    const float4 dx = dv[0][v], dy = dv[1][v];
-                    float2 zxy = make_float2(0.f, 0.f), zzw = make_float2(0.f, 0.f);
-#pragma unroll
-                    for (int kk = 0; kk < 8; ++kk) {
-                        const float2 wk = make_float2(w[kk], w[kk]);
-                        zxy = __ffma2_rn(wk, make_float2(zc[v][kk].x, zc[v][kk].y), zxy);
-                        zzw = __ffma2_rn(wk, make_float2(zc[v][kk].z, zc[v][kk].w), zzw);
-                    }
-                    acc2 = __ffma2_rn(__fmul2_rn(make_float2(dx.x, dx.y), make_float2(dy.x, dy.y)), zxy, acc2);
-                    acc2 = __ffma2_rn(__fmul2_rn(make_float2(dx.z, dx.w), make_float2(dy.z, dy.w)), zzw, acc2);
-                }
-                part[j] = acc2.x + acc2.y;
-            }
-            group_reduce<G, SB>(part, lane);
-            // lane gl holds the total of slot j = its halving path; route it to lane s0 + j
-            const int j = lane - s0;
-            int src_gl = 0;
-            {
-                int nv = SB, o = G / 2, rem = j;
-                while (nv > 1 && o > 0) {
-                    nv >>= 1;
-                    if (rem >= nv) {
-                        src_gl |= o;
-                        rem -= nv;
-                    }
-                    o >>= 1;
-                }
-            }
-            const float got = __shfl_sync(0xffffffffu, part[0], src_gl & 31);
-            if (j >= 0 && j < SB) res = got;
-        }
-        const QDesc& mine = wd[lane];
-        const int32_t oi = mine.out;
-        const float div = mine.div;
-        __syncwarp();
-        if (oi >= 0) out[oi] = res / div;
-    }
-}
-
 // ----------------------------------------------------------- launchers --
-template <int NV, bool W, bool B, bool U>
-static cudaError_t launch_pf(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
-                             int num_sms, cudaStream_t st) {
-    constexpr size_t smem = PfLayout<NV>::BYTES;
-    auto* kfn = query_pf_kernel<NV, W, B, U>;
-    static int occ = -1;
-    if (occ < 0) {
-        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kPThreads, smem) != cudaSuccess || occ < 1)
-            occ = 1;
-    }
-    int64_t grid = (int64_t)num_sms * occ;
-    const int64_t need = (n + kPThreads - 1) / kPThreads;
-    if (grid > need) grid = need;
-    if (grid < 1) grid = 1;
-    int64_t chunk = (n + grid - 1) / grid;
-    chunk = (chunk + 31) / 32 * 32;
-    grid = (n + chunk - 1) / chunk;
-    kfn<<<(unsigned)grid, kPThreads, smem, st>>>(p, q, idx, n, chunk, out);
-    return cudaGetLastError();
-}
-
 template <int G, int NV, bool W, bool B, bool U>
 static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
                             int num_sms, cudaStream_t st) {
-    if constexpr (G == 32 && PNDF_PF1 > 0 && NV <= 2) {
-        if (p.DT && p.dt_w > 0 && !ring_disabled()) return launch_pf<NV, W, B, U>(p, q, idx, n, out, num_sms, st);
-    }
     constexpr size_t smem = QLayout<G, NV, U>::BYTES;
     cudaFuncSetAttribute(query_kernel<G, NV, W, B, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     static int occ = -1;

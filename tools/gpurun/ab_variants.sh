@@ -1,16 +1,15 @@
 #!/bin/bash
-# parity tests of the default library, then config-5 bench of each library variant (VARIANTS="a b ..."; "base" = libpndf.so,
-# "noring" = libpndf.so with PNDF_NORING=1)
+# parity tests of the default library, then config-5 bench of each library variant
+# (VARIANTS="a b ..."; "base" = libpndf.so, NAME = libpndf_NAME.so from build.py --variant=NAME:DEFS)
 mkdir -p gpurun_out
 if [ -z "$NOTEST" ]; then
 timeout 900 python -m pytest tests/test_gpu_parity.py -q -x > gpurun_out/pytest_parity.log 2>&1; echo rc=$? >> gpurun_out/pytest_parity.log
 tail -2 gpurun_out/pytest_parity.log
 fi
 B="python bench.py --steps 3 --warmup 3 --no-e2e --no-cpu-baseline ${BARGS}"
-for v in ${VARIANTS:-base noring}; do
+for v in ${VARIANTS:-base}; do
   case $v in
     base) env="" ;;
-    noring) env="PNDF_NORING=1" ;;
     *) env="PNDF_LIB=$PWD/paper_2109_14807_b200/libpndf_$v.so" ;;
   esac
   env $env timeout 600 $B > gpurun_out/ab_$v.log 2>&1
