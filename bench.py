@@ -71,6 +71,11 @@ def workload_name(cfg) -> str:
             f"L={cfg.L} levels (P={cfg.P} rows){s0}, {cfg.n_queries:.0e} queries")
 
 
+def max_side(cfg) -> int:
+    """Widest query rectangle side of the config's generator."""
+    return {1: 8, 2: 8, 3: 16, 4: 3, 5: 16}.get(cfg.idx, cfg.A)
+
+
 def bytes_per_query(R: int) -> int:
     """record 16 B + result 4 B + 8 Z rows + 4 prefix rows of R fp32 = 20 + 48 R."""
     return 20 + 48 * R
@@ -81,6 +86,41 @@ def measured_peaks():
     if os.path.exists(p):
         return json.load(open(p)), "measured"
     return {"hbm_gbs": 6650.0}, "fallback"
+
+
+FLOP_RANK_QUERY = 19  # a4 8 FMA (16 flop) + a6 dx*dy (1) + FMA into the rank sum (2), per rank and query
+
+
+def fp32_peak_tflops():
+    """FP32 ceiling of the SMs: SMs x 128 FP32 lanes x 2 flop (FMA) x max SM clock.  On B200:
+    148 x 128 x 2 x 1965 MHz = 74.4 TFLOP/s (unit counts and clock from B200_PROFILING.md / MEASURED_PEAKS.json;
+    packed FFMA2 issues 2 FMAs per lane every 2 cycles, B300_MICROARCH.md 'pipe rates', so it reaches it)."""
+    import torch
+    peaks, _ = measured_peaks()
+    mhz = float(peaks.get("sm_max_mhz", 1965.0))
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return sms * 128 * 2 * mhz * 1e6 / 1e12
+
+
+def issue_ceiling(inst_per_unit):
+    """Units/s at one warp instruction per cycle on each of the 4 SMSPs of every SM (max SM clock)."""
+    import torch
+    peaks, _ = measured_peaks()
+    sms = torch.cuda.get_device_properties(torch.cuda.current_device()).multi_processor_count
+    return sms * 4 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / inst_per_unit if inst_per_unit else None
+
+
+def alu_roof(flop_per_unit, units, k_ms, kernel, unit_name, **extra):
+    """`roofline` object against the FP32 ALU ceiling (the binding roof of these gather-and-reduce kernels
+    once binning keeps the Zc rows on chip: DESIGN.md §5)."""
+    peak = fp32_peak_tflops()
+    achieved = flop_per_unit * units / (k_ms * 1e-3) / 1e12
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+            "traffic": None, "kernel": kernel, "kernel_ms": k_ms, f"flop_per_{unit_name}": flop_per_unit,
+            "peak_source": "derived: SMs x 128 FP32 lanes x 2 flop x sm_max_mhz (MEASURED_PEAKS.json), "
+                           "DESIGN.md §5"}
+    roof.update(extra)
+    return roof
 
 
 def ncu_traffic(cfg_idx: int):
@@ -272,7 +312,7 @@ def run_reference(args, cfg, rank, world):
     n_total = args.queries or cfg.n_queries
     probe = synth.gen_queries(cfg, bins, 0, 2000)
     r0 = oracle_sample_rate(cfg, f, probe)[0]
-    per_step = max(2000, int(r0 * min(20.0, 150.0 / max(1, args.steps + args.warmup))))
+    per_step = max(2000, int(r0 * min(20.0, args.cpu_seconds, 150.0 / max(1, args.steps + args.warmup))))
     per_step = min(per_step, n_total, MAX_SAMPLE)
     times = []
     for s in range(args.warmup + args.steps):
@@ -378,6 +418,34 @@ def run_ours(args, cfg, rank, world, local_rank):
     (ms_step, q_ms_max, b_ms_max), checksum = reduce_times_and_checksum([ms_rank, q_ms, b_ms], checksum, dev)
     value = (n if args.as_shard else n_total) / (ms_step * 1e-3)  # --as-shard: this shard's own rate
 
+    # ---- N > 1: the same job index-sharded too (rank k answers the k-th contiguous range of the stream)
+    index_sh = None
+    if world > 1 and args.shard == "spatial" and not args.as_shard:
+        j0, j1 = shard_range(n_total, rank, world)
+        h_qi = torch.empty((j1 - j0, 4), dtype=torch.int32, pin_memory=True)
+        synth.gen_queries(cfg, bins, j0, j1, out=h_qi.numpy().view(synth.QREC).reshape(-1))
+        d_qi = h_qi.to(dev)
+        d_oi = torch.empty(j1 - j0, dtype=torch.float32, device=dev)
+        for _ in range(args.warmup):
+            store.query_batch(d_qi, d_oi, opts)
+            store.sync()
+        dist.barrier()
+        torch.cuda.synchronize()
+        ia, ib = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ia.record()
+        for _ in range(args.steps):
+            store.query_batch(d_qi, d_oi, opts)
+            store.sync()
+        ib.record()
+        torch.cuda.synchronize()
+        dist.barrier()
+        (ims,), ichk = reduce_times_and_checksum([ia.elapsed_time(ib) / args.steps],
+                                                 float(d_oi.double().sum().item()), dev)
+        index_sh = {"value": n_total / (ims * 1e-3), "unit": UNIT, "ms_per_step": ims, "checksum": ichk,
+                    "note": "rank k answers queries [k n/N, (k+1) n/N) of the stream: no partition step, but each "
+                            "rank's batch is 1/N as dense per Zc row, so binning finds less reuse"}
+        del d_qi, d_oi, h_qi
+
     # ---- launch-bound small batches: steady state of GRAPH_BATCHES back-to-back
     # batches captured in one CUDA graph, beside the single-batch step time above
     graph = None
@@ -435,21 +503,34 @@ def run_ours(args, cfg, rank, world, local_rank):
         return 0
 
     peaks, peak_src = measured_peaks()
-    Bq = bytes_per_query(cfg.R)
-    achieved = Bq * n / (q_ms * 1e-3) / 1e9  # algorithmic GB/s of the query kernel on rank 0
+    hbm = peaks["hbm_gbs"]
     tr = ncu_traffic(cfg.idx)
     traffic = None if tr is None else int(tr["dram_bytes_per_query"] * n)
-    roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
-            "kernel": "pndf::query_kernel", "kernel_ms": q_ms, "bytes_per_query": Bq,
-            "peak_source": f"{peak_src} (MEASURED_PEAKS.json hbm_gbs, copy benchmark, burst)"
-            if peak_src == "measured" else "fallback 6.65 TB/s (B200_PROFILING.md)",
-            "l2_peak_gbs_measured": l2_gbs, "frac_of_l2": (achieved / l2_gbs) if l2_gbs else None,
-            "traffic_source": None if tr is None else tr.get("source"),
-            "note": "achieved counts the method's bytes (8 Zc + 4 prefix rows of R fp32 + record + result "
-                    "per query); binned queries reuse Zc rows from registers/L1/L2, so DRAM traffic is far "
-                    "below it and frac > 1 vs HBM; frac_of_l2 is against this run's measured L2 read BW",
-            "binning_ms": b_ms, "query_share_of_step": q_ms / ms_rank if ms_rank else None}
+    # compulsory HBM bytes of the batch: every distinct Zc row once + record and result (+ permutation)
+    d_rows = torch.zeros(1, dtype=torch.int64, device=dev)
+    store.rows_touched(d_q, d_rows)
+    rows_u = int(d_rows.item())
+    comp = rows_u * st["rank_padded"] * 4 + n * (20 + (4 if st["last_binned"] else 0))
+    Rp = st["rank_padded"]
+    ang_rows = 2 if max_side(cfg) <= min(48, cfg.A) else 4  # range-table rows (sides <= 48 bins) else SAT rows
+    ceil = {"fp32_alu": fp32_peak_tflops() * 1e12 / (FLOP_RANK_QUERY * cfg.R),
+            "l2_angular_rows": (l2_gbs * 1e9 / (ang_rows * 4 * Rp)) if l2_gbs else None,
+            "hbm_compulsory": hbm * 1e9 / (comp / n),
+            "issue": issue_ceiling(tr.get("warp_instructions_per_query")) if tr else None}
+    roof = alu_roof(FLOP_RANK_QUERY * cfg.R, n, q_ms, "pndf::query_kernel", "query",
+                    traffic=traffic, traffic_source=None if tr is None else tr.get("source"),
+                    ceilings_queries_per_s=ceil, achieved_queries_per_s=n / (q_ms * 1e-3),
+                    hbm_compulsory={"bytes": comp, "distinct_zc_rows": rows_u, "gbs": comp / (q_ms * 1e-3) / 1e9,
+                                    "frac_of_hbm": comp / (q_ms * 1e-3) / 1e9 / hbm,
+                                    "peak_source": f"{peak_src} MEASURED_PEAKS.json hbm_gbs"},
+                    l2={"peak_gbs_measured": l2_gbs, "angular_row_bytes_per_query": ang_rows * 4 * Rp,
+                        "frac": (n * ang_rows * 4 * Rp / (q_ms * 1e-3) / 1e9 / l2_gbs) if l2_gbs else None,
+                        "ncu_l2_read_bytes_per_query": tr.get("l2_read_bytes_per_query") if tr else None},
+                    touched_bytes_per_query=bytes_per_query(cfg.R),
+                    note="frac = FP32 work (19 flop per rank and query) over the FP32 ceiling; the other ceilings "
+                         "beside it; touched_bytes_per_query (20 + 48R, the method's 12 look-ups) is not a roof: "
+                         "binned queries reuse Zc rows from registers",
+                    binning_ms=b_ms, query_share_of_step=q_ms / ms_rank if ms_rank else None)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, f, bins, i0, args.cpu_seconds)
@@ -460,6 +541,9 @@ def run_ours(args, cfg, rank, world, local_rank):
             "config": {"workload": workload_name(cfg), "queries_total": n_total, "queries_per_rank": n,
                        "parallelism": f"query-sharded x{world} ({args.shard if world > 1 else 'whole stream'}), "
                                       "factors replicated",
+                       "stream": ("pre-partitioned by vertical map strip (screen-space tiles of a renderer); the "
+                                  "partition is untimed setup" if world > 1 and args.shard == "spatial" else
+                                  "index-sharded" if world > 1 else "whole stream on one GPU"),
                        "binning": args.bin, "binned": bool(st["last_binned"]),
                        "lanes_per_query": st["lanes_per_query"], "rank_padded": st["rank_padded"],
                        "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]],
@@ -469,7 +553,7 @@ def run_ours(args, cfg, rank, world, local_rank):
                         "this config by L2); no flush" % (st["zc_bytes"] / 1e6, n * 16 / 1e6)),
                        "setup_s": round(setup_s, 1)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
-            "graph_steady_state": graph,
+            "graph_steady_state": graph, "index_sharding": index_sh,
             "parity_sample": parity,
             "clocks": clk, "checksum": checksum}
     print(json.dumps(line), flush=True)
@@ -565,6 +649,13 @@ def sample_bytes(R: int, A: int) -> int:
     return 72 + 4 * R * (8 + 4 + 2 * levels)
 
 
+def sample_flop(R: int, A: int) -> int:
+    """Method flops per sample: Z-hat interpolation 16R, the root range query 3R (dx*dy, FMA), then per level of
+    the quad descent 4 quadrant range queries of 3R each."""
+    levels = max(1, (A - 1).bit_length())
+    return 16 * R + 3 * R + levels * 4 * 3 * R
+
+
 def run_sample_op(args, cfg, rank, world, local_rank):
     """--op sample: pndf_sample_batch over the shard (domain = whole image), same timing rules."""
     import torch
@@ -622,9 +713,7 @@ def run_sample_op(args, cfg, rank, world, local_rank):
     if rank != 0:
         store.free()
         return 0
-    peaks, _ = measured_peaks()
     Bs = sample_bytes(cfg.R, cfg.A)
-    achieved = Bs * n / (k_ms * 1e-3) / 1e9
     # parity on a sample of the timed batch (oracle sampler on the same variates)
     idx = np.unique(np.random.default_rng(3).integers(0, n, min(n, 2000)))
     rs = recs[idx]
@@ -648,9 +737,10 @@ def run_sample_op(args, cfg, rank, world, local_rank):
             "config": {"workload": workload_name(cfg) + "; importance sampling over the whole A x A image",
                        "samples_total": n_total, "binned": bool(st["last_binned"]),
                        "sat_format": ["fp32 hi/lo", "u32 fixed point"][st["prefix_format"]]},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "pndf::sample_kernel",
-                         "kernel_ms": k_ms, "bytes_per_sample": Bs},
+            "roofline": alu_roof(sample_flop(cfg.R, cfg.A), n, k_ms, "pndf::sample_kernel", "sample",
+                                 touched_bytes_per_sample=Bs,
+                                 note="flop = Z-hat (16R) + root range query (3R) + 4 quadrant range queries "
+                                      "(3R each) per descent level (P:385-389); touched bytes are not a roof"),
             "cpu_baseline": {"value": cpu_rate, "unit": "samples/s", "cores": oracle.max_threads(),
                              "kind": "oracle", "sample": f"{rs.shape[0]} samples of the timed batch"},
             "gpu_launches": int(st["kernel_launches"] - l0), "clocks": clk,
@@ -717,9 +807,7 @@ def run_sg_op(args, cfg, rank, world, local_rank):
     if rank != 0:
         store.free()
         return 0
-    peaks, _ = measured_peaks()
     Bq = bytes_per_query(cfg.R) + 32 + 16  # + SG record read, generated record write
-    achieved = Bq * n / (ms_rank * 1e-3) / 1e9
     h_q = d_q.cpu().numpy().view(synth.QREC).reshape(-1)
     idx = np.unique(np.random.default_rng(4).integers(0, n, min(n, 4096)))
     ref_r = oracle.sg_rects(sg[idx], cfg.A)
@@ -738,10 +826,8 @@ def run_sg_op(args, cfg, rank, world, local_rank):
             "config": {"workload": workload_name(cfg) + "; SG lights: lambda log-U[10,1000], A U[0.5,2], "
                                                          "half vector Beckmann 0.3, eps 0.3",
                        "queries_total": n_total, "binned": bool(st["last_binned"])},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
-                         "kernel": "sg_rect_kernel + pndf::query_kernel", "query_kernel_ms": q_ms,
-                         "bytes_per_query": Bq},
+            "roofline": alu_roof(FLOP_RANK_QUERY * cfg.R, n, q_ms, "pndf::query_kernel (after sg_rect_kernel)",
+                                 "query", touched_bytes_per_query=Bq, step_ms=ms_rank),
             "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
                              "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
             "gpu_launches": int(st["kernel_launches"] - l0) + args.steps, "clocks": clk,
@@ -878,13 +964,14 @@ def run_wang_op(args, cfg, rank, world, local_rank):
     Rp, levels = st["rank_padded"], int(round(math.log2(tc.A)))
     Bq = (32 + 4 * Rp * (rows_mean + 4 + 2 * levels)) if sample else (20 + 4 * Rp * (rows_mean + 2))
     k_ms = st["query_ms"] / max(1, st["timed_batches"])
-    hbm = measured_peaks()[0]["hbm_gbs"]
-    achieved = Bq * n / (k_ms * 1e-3) / 1e9
-    wang_roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-                 "traffic": None, "kernel": kern, "kernel_ms": k_ms, "bytes_per_query": Bq,
-                 "zc_rows_per_query_mean": rows_mean,
-                 "note": "16 tiles' Zc %.0f MB (> L2); bytes per record from the positive-weight Zc rows (all "
-                         "overlapped tiles' rows), measured on the parity sample" % (st["zc_bytes"] / 1e6)}
+    # method flops per record: 2R per positive-weight (tile, neighbour) Zc row into Z-hat, then the rank
+    # product 3R (query) or the descent's root + 4 quadrant queries per level (sampling)
+    R = tc.R
+    fl = 2 * R * rows_mean + (3 * R + levels * 12 * R if sample else 3 * R)
+    wang_roof = alu_roof(fl, n, k_ms, kern, "record", touched_bytes_per_record=Bq, zc_rows_per_query_mean=rows_mean,
+                         level_sort_ms=st["bin_ms"] / max(1, st["timed_batches"]),
+                         note="16 tiles' Zc %.0f MB (> L2); rows per record = the positive-weight Zc rows of all "
+                              "overlapped tiles, measured on the parity sample" % (st["zc_bytes"] / 1e6))
     line = {"metric": WANG_SAMPLE_METRIC if sample else WANG_METRIC, "value": n_total / (ms_step * 1e-3),
             "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -897,7 +984,7 @@ def run_wang_op(args, cfg, rank, world, local_rank):
             "roofline": wang_roof,
             "cpu_baseline": {"value": cpu_rate, "unit": unit, "cores": oracle.max_threads(),
                              "kind": "oracle", "sample": f"{idx.shape[0]} records of the timed batch"},
-            "gpu_launches": args.steps, "clocks": clk,
+            "gpu_launches": int(st["kernel_launches"]), "clocks": clk,
             "parity_sample": {"checked": int(idx.shape[0]), "pass": passed},
             "e2e": None}
     print(json.dumps(line), flush=True)
@@ -912,13 +999,11 @@ def blocked_roofline(cfg, n, k_ms):
     """Algorithmic bytes of the blocked query: record + result, and per bilinear neighbour of both levels one
     block's slab pointer + group set (8 B), its Zc row (4R) and 8 HILO prefix rows (32R).  Counts one
     non-blank block per neighbour: rectangles that cross block borders read more, blank blocks less."""
-    peaks, src = measured_peaks()
     Bq = 20 + 8 * (8 + 36 * cfg.R)
-    achieved = Bq * n / (k_ms * 1e-3) / 1e9
-    return {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-            "frac": achieved / peaks["hbm_gbs"], "traffic": None, "kernel": "pndf::blocked_query_kernel",
-            "kernel_ms": k_ms, "bytes_per_query": Bq, "peak_source": src,
-            "note": blocked_roofline.__doc__.split("\n")[0].strip()}
+    # per neighbour (8): its block's X-bar, Y-bar from hi/lo prefix rows (2 x 3 FADD per rank), the rank
+    # product dx*dy*z (3 flop per rank), then the weighted blend
+    return alu_roof(8 * 9 * cfg.R + 16, n, k_ms, "pndf::blocked_query_kernel", "query", touched_bytes_per_query=Bq,
+                    note=blocked_roofline.__doc__.split("\n")[0].strip())
 
 
 ALS_METRIC = "CP-ALS sweeps/sec of the GPU factor builder (P:308; footprint NDF tensor P x A x A, rank R)"
@@ -981,7 +1066,9 @@ def run_als_op(args, cfg, rank, world, local_rank):
         return 0
     peaks, src = measured_peaks()
     dbytes = cfg.P * cfg.A * cfg.A * 4
-    achieved = 3 * dbytes / (ms_step * 1e-3) / 1e9
+    mttkrp_flop = 3 * 2 * cfg.P * cfg.A * cfg.A * cfg.R  # three MTTKRPs of the full tensor per sweep
+    tf32_peak = peaks.get("bf16_tflops", 2250.0) * (1.1 / 2.25)  # measured bf16 x nominal tf32/bf16 (B200_PROFILING)
+    achieved = mttkrp_flop / (ms_step * 1e-3) / 1e12
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         from oracle import als as oals
@@ -1006,12 +1093,17 @@ def run_als_op(args, cfg, rank, world, local_rank):
                        "step_includes": "one pndf_cp_als call of K sweeps: per-call setup (~2.5 ms: allocations, "
                                         "||D||^2 pass) amortised over the K sweeps; steady sweep = kernel sum",
                        "inputs": "D (2 x tensor) resident in HBM, larger than L2: no flush needed"},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                         "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+            "roofline": {"bound": "hbm", "achieved": 3 * dbytes / (ms_step * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": 3 * dbytes / (ms_step * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                         "traffic": None,
                          "kernel": "pndf::als::mttkrp_gemm_kernel (3 per sweep) + HALS/Gram kernels",
                          "bytes_per_sweep": 3 * dbytes, "peak_source": src,
-                         "note": "achieved = the 3 tensor reads a sweep must make (modes Z, X on D, mode Y on Dt) "
-                                 "over the whole sweep time (includes the HALS, Gram and host-sync steps)"},
+                         "tensor": {"flop_per_sweep": mttkrp_flop, "tflops": achieved, "peak_tflops": tf32_peak,
+                                    "frac": achieved / tf32_peak,
+                                    "peak_source": "MEASURED_PEAKS bf16_tflops x 1.1/2.25 (tf32/bf16 nominal)"},
+                         "note": "achieved = the 3 reads of D a sweep must make (modes Z, X on D, mode Y on Dt) over "
+                                 "the whole sweep time (HALS, Gram and host-sync steps included): at R = 32 the "
+                                 "MTTKRP is bound by streaming D, not by the tensor cores (tensor.frac)"},
             "cpu_baseline": cpu,
             # one pndf_cp_als call of K sweeps = 12 setup/teardown launches + 21 per sweep (3 tcgen05 GEMMs,
             # 3 HALS + 3 Gram sums, 2 operand splits + 1 Khatri-Rao, 2 partial reductions, error, balance,
@@ -1100,11 +1192,29 @@ def run_blocked_op(args, cfg, rank, world, local_rank):
     return 0
 
 
+def spawn_ranks(n: int) -> int:
+    """`python bench.py --gpus N` without a launcher: re-run this command under torch.distributed.run, one
+    process per GPU on this node (rendezvous on 127.0.0.1), and return its exit code."""
+    import socket
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        return spawn_ranks(args.gpus)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; launch one process per GPU\n")
+        return 2
     cfg = synth.CONFIGS[args.config]
     if args.s0:
         cfg = cfg.scaled(s0=args.s0)
@@ -1114,7 +1224,7 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
+        dist.init_process_group("nccl")  # timing / checksum reductions only, after each timed region
     try:
         if args.op == "sample":
             return run_sample_op(args, cfg, rank, world, local_rank)

@@ -305,6 +305,13 @@ pndf_status pndf_load_blocked(const pndf_block_desc* desc, const float* C, const
 pndf_status pndf_bin_permutation(pndf_store s, const pndf_query* d_queries, int64_t n, uint32_t* d_perm,
                                  uint32_t* d_keys);
 
+/* Measurement support (bench.py roofline): *d_rows_out (device int64) = the number of
+ * DISTINCT Zc rows that the query kernel reads for the n device records, i.e. the 8 trilinear
+ * neighbours of each valid record (the kernel loads all 8 even at zero weight).  Multiplied by
+ * Rp x 4 B this is the batch's compulsory Zc traffic from HBM.  Global stores only (EINVAL for tiled or
+ * blocked stores).  Scratch: a P-bit bitmap allocated and freed inside the call.  Synchronous. */
+pndf_status pndf_rows_touched(pndf_store s, const pndf_query* d_queries, int64_t n, int64_t* d_rows_out);
+
 /* Tuning knob (bench / tests): lanes per query G in {1,2,4,8,16,32} with
  * G*4 dividing Rp; 0 restores the default chosen at load. */
 pndf_status pndf_set_lanes(pndf_store s, int32_t lanes);

@@ -62,6 +62,11 @@ cudaError_t launch_block_build(const float* X, const float* Y, int sets, int t, 
 cudaError_t launch_sg_rects(const pndf_sg_light* in, int64_t n, float eps, int A, pndf_query* out, int num_sms,
                             cudaStream_t st);
 
+// Distinct Zc rows the query kernel reads for n records (query.cu): bitmap [ceil(P/32)] words, zeroed by
+// the caller; *count (device) receives the popcount.
+cudaError_t launch_rows_touched(const QParams& p, const pndf_query* q, int64_t n, int64_t P, uint32_t* bitmap,
+                                int64_t* count, int num_sms, cudaStream_t st);
+
 int64_t scan_blocks(int64_t nb);
 int64_t radix_tiles(int64_t n);
 

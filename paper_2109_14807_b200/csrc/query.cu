@@ -36,6 +36,59 @@ cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, c
                   : launch_query_hilo_clamp(G, NV, p, q, idx, n, out, num_sms, st);
 }
 
+// -------------------------------------------------------- rows touched --
+// Measurement helper: mark the 8 neighbour rows of each valid record (a2/a3 exactly as the query
+// kernel decodes them), then count the marked bits.
+template <bool WRAP>
+__global__ void mark_rows_kernel(const QParams p, const pndf_query* __restrict__ q, int64_t n,
+                                 uint32_t* __restrict__ bitmap) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const pndf_query rec = ldg_query(q + i);
+        int x1, x2, y1, y2;
+        if (!record_valid(p, rec, x1, x2, y1, y2)) continue;
+        int l0;
+        float t;
+        level_select(p, rec.size, l0, t);
+        for (int dl = 0; dl < 2; ++dl) {
+            const int l = l0 + dl;
+            int i0, i1, j0, j1;
+            float a, b;
+            axis_cells<WRAP>(p, rec.u, l, i0, i1, a);
+            axis_cells<WRAP>(p, rec.v, l, j0, j1, b);
+            const int64_t nl = p.n0 >> l, off = level_offset(p.n0, l);
+            const int64_t rows[4] = {off + j0 * nl + i0, off + j0 * nl + i1, off + j1 * nl + i0, off + j1 * nl + i1};
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t bit = 1u << (rows[k] & 31);
+                uint32_t* w = bitmap + (rows[k] >> 5);
+                if (!(*w & bit)) atomicOr(w, bit);
+            }
+        }
+    }
+}
+
+__global__ void popcount_kernel(const uint32_t* __restrict__ bitmap, int64_t words, int64_t* count) {
+    int64_t c = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < words; i += (int64_t)gridDim.x * blockDim.x)
+        c += __popc(bitmap[i]);
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(reinterpret_cast<unsigned long long*>(count), (unsigned long long)c);
+}
+
+cudaError_t launch_rows_touched(const QParams& p, const pndf_query* q, int64_t n, int64_t P, uint32_t* bitmap,
+                                int64_t* count, int num_sms, cudaStream_t st) {
+    const unsigned grid = (unsigned)num_sms * 8;
+    if (n > 0) {
+        if (p.wrap)
+            mark_rows_kernel<true><<<grid, 256, 0, st>>>(p, q, n, bitmap);
+        else
+            mark_rows_kernel<false><<<grid, 256, 0, st>>>(p, q, n, bitmap);
+    }
+    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int64_t), st);
+    if (e != cudaSuccess) return e;
+    popcount_kernel<<<grid, 256, 0, st>>>(bitmap, (P + 31) / 32, count);
+    return cudaGetLastError();
+}
+
 // ------------------------------------------------------------ binning --
 // a1: key = the record's half cell on its lower level l0 (Z-order within the
 // level), so queries that share all 8 Zc rows get equal keys and queries that

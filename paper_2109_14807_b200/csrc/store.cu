@@ -1026,6 +1026,23 @@ pndf_status pndf_bin_permutation(pndf_store s, const pndf_query* d_queries, int6
     return PNDF_OK;
 }
 
+pndf_status pndf_rows_touched(pndf_store s, const pndf_query* d_queries, int64_t n, int64_t* d_rows_out) {
+    if (!s || n < 0 || !d_rows_out || (n > 0 && !d_queries)) return PNDF_EINVAL;
+    if (s->tiled || s->blocked) return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    uint32_t* bitmap = nullptr;
+    const int64_t words = (s->P + 31) / 32;
+    CK(cudaMalloc(&bitmap, sizeof(uint32_t) * words));
+    cudaError_t e = cudaMemsetAsync(bitmap, 0, sizeof(uint32_t) * words, nullptr);
+    if (e == cudaSuccess) e = launch_rows_touched(s->qp, d_queries, n, s->P, bitmap, d_rows_out, s->num_sms, nullptr);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(nullptr);
+    cudaFree(bitmap);
+    CK(e);
+    s->stats.kernel_launches += n > 0 ? 2 : 1;
+    return PNDF_OK;
+}
+
 pndf_status pndf_set_lanes(pndf_store s, int32_t lanes) {
     if (!s) return PNDF_EINVAL;
     std::lock_guard<std::mutex> lk(s->mu);

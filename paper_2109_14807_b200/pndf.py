@@ -73,7 +73,7 @@ EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_s
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
            "pndf_sg_queries", "pndf_load_tiles", "pndf_load_blocked", "pndf_hist_tensor", "pndf_cp_als",
-           "pndf_mttkrp")
+           "pndf_mttkrp", "pndf_rows_touched")
 
 ALS_NORMALISE = 1
 
@@ -130,6 +130,8 @@ def lib():
                                         ctypes.POINTER(P)]
         L.pndf_sg_queries.restype = i32
         L.pndf_sg_queries.argtypes = [P, i64, ctypes.c_float, i32, P, P]
+        L.pndf_rows_touched.restype = i32
+        L.pndf_rows_touched.argtypes = [P, P, i64, P]
         L.pndf_set_lanes.restype = i32
         L.pndf_set_lanes.argtypes = [P, i32]
         L.pndf_hist_tensor.restype = i32
@@ -274,6 +276,11 @@ class Store:
         """Test support: binning pass only -> permutation (and sorted keys) in device buffers."""
         _check(lib().pndf_bin_permutation(self.handle, _ptr(queries), perm.shape[0], _ptr(perm), _ptr(keys)),
                "pndf_bin_permutation")
+
+    def rows_touched(self, queries, out, n: int | None = None):
+        """Measurement support: distinct Zc rows the query kernel reads for these records -> out (device int64 [1])."""
+        n = queries.shape[0] if n is None else n
+        _check(lib().pndf_rows_touched(self.handle, _ptr(queries), n, _ptr(out)), "pndf_rows_touched")
 
     def set_lanes(self, lanes: int):
         _check(lib().pndf_set_lanes(self.handle, lanes), "pndf_set_lanes")

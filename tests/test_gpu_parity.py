@@ -438,3 +438,24 @@ def test_range_table_widths(prefix):
     st.free()
     ref = oracle.query_batch(oracle.make_desc(N, s0, L, A, R, True), f.C, f.X, f.Y, f.Z, recs)
     assert_parity(out.cpu().numpy(), ref, "range table widths")
+
+
+@pytest.mark.parametrize("k,wrap", [(2, True), (1, False)])
+def test_rows_touched_counts_distinct_neighbour_rows(k, wrap):
+    """pndf_rows_touched (the bench's compulsory-HBM count) = the number of distinct rows among the 8
+    neighbours (oracle.neighbours) of the valid records; invalid records add nothing."""
+    pndf = _pndf()
+    cfg, bins, f = config_inputs(k)
+    if not wrap:
+        cfg = cfg.scaled(wrap=False)
+    recs = synth.gen_queries(cfg, bins, 0, 200_000)
+    recs["rect"][::97] = synth.pack_rect(3, 1, 0, 0)  # invalid: x1 > x2
+    st = pndf.load_factors(pndf.make_desc(**desc_args(cfg)), f.C, f.X, f.Y, f.Z)
+    d_rows = torch.zeros(1, dtype=torch.int64, device="cuda")
+    st.rows_touched(torch_records(recs), d_rows)
+    rows, _ = oracle.neighbours(oracle.desc_of(cfg), recs)
+    valid = np.ones(recs.shape[0], bool)
+    valid[::97] = False
+    want = np.unique(rows[valid].reshape(-1)).shape[0]
+    assert int(d_rows.item()) == want
+    st.free()

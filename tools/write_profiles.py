@@ -84,7 +84,10 @@ def summarize(rep, nq, title, idx=0, unit="query"):
         lines += ["", f"opcode mix (per {unit}) and share of warp-stall samples:"]
         for op, k in sorted(c.items(), key=lambda x: -x[1])[:16]:
             lines.append(f"  {op:10s} {k / nq:8.2f}/q   stall {s[op] / tot * 100:5.1f}%")
-    return "\n".join(lines) + "\n", dram / nq
+    per = {"dram": dram / nq,
+           "l2_read": float(vals['lts__t_sectors_srcunit_tex_op_read.sum'][0].replace(',', '')) * 32 / nq,
+           "inst": float(vals['smsp__inst_executed.sum'][0].replace(',', '')) / nq}
+    return "\n".join(lines) + "\n", per
 
 
 def launches(path):
@@ -121,7 +124,8 @@ def main():
     if os.path.exists(q):
         txt, dpq = summarize(q, nq, "pndf::query_kernel, config 5, binned, U32 SATs")
         open(os.path.join(OUT, f"{rnd}_query_kernel_ncu.txt"), "w").write(txt)
-        traffic["config5"] = {"dram_bytes_per_query": dpq,
+        traffic["config5"] = {"dram_bytes_per_query": dpq["dram"], "l2_read_bytes_per_query": dpq["l2_read"],
+                              "warp_instructions_per_query": dpq["inst"],
                               "source": f"profiles/{rnd}_query_kernel_ncu.txt (ncu --set full, {nq:.0e} queries, "
                                         "same launch configuration as bench.py)"}
     sc = os.path.join(GP, "prof_scatter_full.ncu-rep")
