@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang", "wang_sample", "blocked", "als",
+                                                      "als_map",
                                                       "sweep"],
                     help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
@@ -1118,6 +1119,106 @@ def run_als_op(args, cfg, rank, world, local_rank):
     return 0
 
 
+ALS_MAP_METRIC = ("CP-ALS sweeps/sec of the map-domain GPU factor builder (P:308; exact footprint tensor P x A x A "
+                  "never formed)")
+
+
+def map_sweep_flop(cfg) -> int:
+    """fp64 FMA work of one map-domain sweep x 2: per level l (stride s, window wf, grid n) the
+    Z-mode pass along u (N n wf taps) and along v (n^2 wf), the adjoint along v (N n wf/s) and along u
+    (N^2 wf/s), then the X and Y modes (N^2 each), every tap over R ranks."""
+    N, R = cfg.N, cfg.R
+    taps = 2 * N * N
+    for l in range(cfg.L):
+        s = cfg.s0 << l
+        n = N // s
+        sigma = 1.5 * s / math.sqrt(12.0)
+        c = 0.5 * (1.0 - s)
+        wf = min(math.floor(4.0 * sigma - c) - math.ceil(-4.0 * sigma - c) + 1, N)
+        per = math.ceil(wf / s)
+        taps += N * n * wf + n * n * wf + N * n * per + N * N * per
+    return 2 * taps * R
+
+
+def run_als_map_op(args, cfg, rank, world, local_rank):
+    """--op als_map (SURVEY §8(f) row 3 at config 3 scale): HALS CP-ALS of the config's footprint tensor with
+    map-domain MTTKRPs (pndf_cp_als_map).  A step = one sweep; `e2e` = the whole builder at the paper's settings
+    (tol 1e-4, <= 500 sweeps) from host bins to host factors.  Replicas only (one map per GPU)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2109_14807_b200 import pndf
+    from paper_2109_14807_b200.shard import reduce_times_and_checksum
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    bins = synth.bin_map(cfg, synth.make_map(cfg))
+    desc = pndf.make_desc(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.R, True)
+    d_bins = torch.from_numpy(bins.view(np.int16)).to(dev)
+    rng = np.random.default_rng(1)
+    init = [rng.random((cfg.P, cfg.R)).astype(np.float32), rng.random((cfg.A, cfg.R)).astype(np.float32),
+            rng.random((cfg.A, cfg.R)).astype(np.float32)]
+    fz, fx, fy = (torch.from_numpy(a).to(dev) for a in init)
+    pndf.cp_als_map(desc, d_bins, fz, fx, fy, max_sweeps=max(3, args.warmup), tol=0.0)
+    clocks = ClockSampler(bus_id_of(dev))
+    clocks.start()
+    pndf.cp_als_map(desc, d_bins, fz, fx, fy, max_sweeps=2, tol=0.0)  # re-warm after the sampler's start
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    err = pndf.cp_als_map(desc, d_bins, fz, fx, fy, max_sweeps=args.steps, tol=0.0)
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    ms_rank = e0.elapsed_time(e1) / args.steps
+    (ms_step,), _ = reduce_times_and_checksum([ms_rank], float(err[-1]), dev)
+    e2e = None
+    if not args.no_e2e:
+        t0 = time.perf_counter()
+        d_b2 = torch.from_numpy(bins.view(np.int16)).to(dev)
+        gz, gx, gy = (torch.from_numpy(a).to(dev) for a in init)
+        gc = torch.empty(cfg.R, dtype=torch.float32, device=dev)
+        hist = pndf.cp_als_map(desc, d_b2, gz, gx, gy, gc, max_sweeps=500, tol=1e-4, normalise=True)
+        out = [t.cpu() for t in (gc, gx, gy, gz)]
+        e2e_s = time.perf_counter() - t0
+        e2e = {"value": len(hist) / e2e_s, "unit": "sweeps/s", "h2d_bytes_per_step": int(bins.nbytes),
+               "d2h_bytes_per_step": int(sum(t.numel() * 4 for t in out)), "builder_seconds": e2e_s,
+               "sweeps": int(len(hist)), "fit_error": float(hist[-1]),
+               "note": "whole builder at P:308 settings, host bins in, host factors out; the paper quotes "
+                       "10-60 minutes per 2K x 2K map on its CPU (P:311)"}
+    if rank != 0:
+        return 0
+    peaks, src = measured_peaks()
+    import torch as _t
+    sms = _t.cuda.get_device_properties(dev).multi_processor_count
+    fp64_peak = sms * 64 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    fl = map_sweep_flop(cfg)
+    achieved = fl / (ms_step * 1e-3) / 1e12
+    dense = 3 * 2 * cfg.P * cfg.A * cfg.A * cfg.R
+    line = {"metric": ALS_MAP_METRIC, "value": 1e3 / ms_step, "unit": "sweeps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (MTTKRP passes, HALS)", "data": "synthetic",
+            "config": {"workload": f"config{cfg.idx} map {cfg.N}^2, P = {cfg.P} footprints, A = {cfg.A}, R = {cfg.R}; "
+                                   f"the dense tensor would be {cfg.P * cfg.A * cfg.A * 4 / 1e9:.0f} GB",
+                       "fit_error_after_timed_sweeps": float(err[-1]),
+                       "inputs": "map bins + factors resident in HBM; pass buffers (N^2 R fp64) larger than L2"},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
+                         "frac": achieved / fp64_peak, "traffic": None,
+                         "kernel": "pndf::als::{mz_h,mz_v,u_g,u_h,mxy}_kernel + HALS/Gram kernels",
+                         "flop_per_sweep": fl, "dense_tensor_flop_per_sweep": dense,
+                         "peak_source": "derived: SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (B200 FP64 37 TFLOP/s)",
+                         "note": "achieved = the map-domain passes' fp64 FMA work over the whole sweep time (HALS, "
+                                 "Gram, error and host sync included); the dense-tensor formulation would need "
+                                 "dense_tensor_flop_per_sweep"},
+            # one pndf_cp_als_map call of K sweeps: 10 setup launches (factor loads, ||D||^2, Gram) + 25 per sweep
+            # (4 Z-mode passes, 4 adjoint passes, 2 x 2 X/Y-mode, 3 x 2 HALS + Gram sums, error, balance, 5 scalings)
+            "cpu_baseline": None, "gpu_launches": 10 + 25 * args.steps, "clocks": clk, "e2e": e2e}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def run_blocked_op(args, cfg, rank, world, local_rank):
     """--op blocked: the config's queries on the paper-faithful blocked / clustered store (exact-rank groups)."""
     import torch
@@ -1236,6 +1337,8 @@ def main():
             return run_blocked_op(args, cfg, rank, world, local_rank)
         if args.op == "sweep":
             return run_sweep_op(args, synth.CONFIGS[3], rank, world, local_rank)
+        if args.op == "als_map":
+            return run_als_map_op(args, cfg if args.config != 5 else synth.CONFIGS[3], rank, world, local_rank)
         if args.op == "als":
             return run_als_op(args, cfg if cfg.idx in (1, 2) else synth.CONFIGS[2], rank, world, local_rank)
         return run_ours(args, cfg, rank, world, local_rank)

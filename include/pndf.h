@@ -355,6 +355,24 @@ pndf_status pndf_cp_als(const pndf_desc* desc, const float* d_D, const float* d_
 pndf_status pndf_mttkrp(const pndf_desc* desc, const float* d_D, const float* d_Dt, const float* d_Z,
                         const float* d_X, const float* d_Y, int32_t mode, double* d_M, void* cuda_stream);
 
+/* ---- Map-domain factor builder (no tensor in memory; configs 3-4 scale) -------------------------------
+ * The same nonnegative CP-ALS as pndf_cp_als (HALS, modes Z, X, Y, norm balance, stopping rule, normalise),
+ * of the EXACT footprint tensor D = count / total (no tf32 rounding), but D is never formed: it is a
+ * separable Gaussian blur of the texels' one-hot angular histograms (Eq. 2), so each MTTKRP
+ * contracts over the N x N texels (fp64, ~3.5 N^2 L R FMAs per mode) instead of over P x A x A entries --
+ * e.g. config 3 (P = 5.6M, A = 128) would need a 366 GB tensor.  ||D||^2 comes from exact integer bin
+ * counts per footprint window.  Limits: periodic map (PNDF_WRAP), A a power of two <= 256, R <= 256, and
+ * device memory for Z, M_Z (P x R fp64 each) plus two N^2 x R fp64 pass buffers; PNDF_ENOMEM otherwise.
+ * d_bins [N][N] uint16 as for pndf_hist_tensor; factors, opts, h_err, sweeps_out as for pndf_cp_als.
+ * Results are reproducible up to the order of fp64 shared-memory atomics in the X / Y modes.
+ * pndf_mttkrp_map (test support): one MTTKRP (mode 0 = Z [P][R], 1 = X [A][R], 2 = Y [A][R]) into d_M
+ * (fp64, device) and, if h_sumsq is not NULL, ||D||^2 into *h_sumsq.  Synchronous. */
+pndf_status pndf_cp_als_map(const pndf_desc* desc, const uint16_t* d_bins, float* d_C, float* d_X, float* d_Y,
+                            float* d_Z, const pndf_als_opts* opts, double* h_err, int32_t* sweeps_out,
+                            void* cuda_stream);
+pndf_status pndf_mttkrp_map(const pndf_desc* desc, const uint16_t* d_bins, const float* d_Z, const float* d_X,
+                            const float* d_Y, int32_t mode, double* d_M, double* h_sumsq, void* cuda_stream);
+
 #ifdef __cplusplus
 }
 #endif

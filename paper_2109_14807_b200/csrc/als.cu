@@ -703,6 +703,263 @@ __global__ void rows_to_f64_kernel(const float* __restrict__ in, int64_t rows, i
         out[e] = (double)in[(e / R) * RP + e % R];
 }
 
+
+// ---------------------------------------------------------------- map-domain MTTKRP (no D) --
+// The footprint tensor is a blur of the texels' one-hot angular histograms (Eq. 2: D[z][x][y] =
+// sum over z's window of w_p w_q [bin(t) = (x, y)] / tot), so every MTTKRP contracts over TEXELS instead of
+// over the P x A x A tensor, and D is never formed (DESIGN.md §5 "Factor builder"):
+//   mode Z  M_Z[z] = (1/tot) sum_q w_q sum_p w_p  X[bx(t)] o Y[by(t)],   t = texel (p, q) of z's window
+//   mode X  M_X[x] = sum_{t: bx(t) = x} Y[by(t)] o U[t],   U[t] = sum_z (1/tot) w_p w_q Z[z]  (the adjoint)
+//   mode Y  M_Y[y] = sum_{t: by(t) = y} X[bx(t)] o U[t]
+// Both blurs are separable: a pass along u at the level's stride, then one along v.  Work per sweep is
+// ~3 x 3.5 N^2 L R FMAs instead of 3 P A^2 R, all in fp64 (the GEMM path's tf32(D) rounding is gone).
+// Warps own one output row; lane k handles rank c0 + k of the 32-rank chunk blockIdx.y.
+struct MapLevel {
+    int64_t off;      // first Zc row of the level
+    int64_t hoff;     // first row of the level's [N][n] block in the pass buffer
+    int32_t s, n, qmin, wf, woff;
+    double inv_tot;   // 1 / (sum w)^2
+};
+
+// level of row g among levels [l0, l1) (pass-buffer rows when by_hoff, else Zc rows)
+__device__ __forceinline__ int map_level(const MapLevel* lv, int l0, int l1, int64_t g, bool by_hoff) {
+    int l = l0;
+    while (l + 1 < l1 && g >= (by_hoff ? lv[l + 1].hoff : lv[l + 1].off)) ++l;
+    return l;
+}
+
+// H[hoff + v n + i][r] = sum_p w_p X[bx][r] Y[by][r] over texels (v, (i s + qmin + p) mod N), levels [l0, l1)
+__global__ void __launch_bounds__(256) mz_h_kernel(const uint16_t* __restrict__ bins, int N, int A, int ash,
+                                                   const MapLevel* __restrict__ lv, int l0, int l1,
+                                                   const uint32_t* __restrict__ wtab, const double* __restrict__ X,
+                                                   const double* __restrict__ Y, int R, double* __restrict__ H) {
+    extern __shared__ double xs[];  // [2][A][32]: X, Y columns of this rank chunk
+    double* ys = xs + A * 32;
+    const int c0 = blockIdx.y * 32, lane = threadIdx.x & 31;
+    for (int e = threadIdx.x; e < A * 32; e += blockDim.x) {
+        const int r = c0 + (e & 31);
+        xs[e] = r < R ? X[(e >> 5) * R + r] : 0.0;
+        ys[e] = r < R ? Y[(e >> 5) * R + r] : 0.0;
+    }
+    __syncthreads();
+    const int64_t g0 = lv[l0].hoff, g1 = lv[l1 - 1].hoff + (int64_t)N * lv[l1 - 1].n;
+    const int r = c0 + lane;
+    for (int64_t g = g0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); g < g1;
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const MapLevel h = lv[map_level(lv, l0, l1, g, true)];
+        const int64_t c = g - h.hoff;
+        const int v = (int)(c / h.n), i = (int)(c % h.n);
+        int u = (int)((((int64_t)i * h.s + h.qmin) % N + N) % N);
+        const uint16_t* brow = bins + (int64_t)v * N;
+        const uint32_t* w = wtab + h.woff;
+        double acc = 0.0;
+        for (int p = 0; p < h.wf; ++p) {
+            const int b = __ldg(brow + u);
+            acc = fma((double)__ldg(w + p), xs[(b & (A - 1)) * 32 + lane] * ys[(b >> ash) * 32 + lane], acc);
+            if (++u == N) u = 0;
+        }
+        if (r < R) H[g * R + r] = acc;
+    }
+}
+
+// M[z][r] = inv_tot sum_q w_q H[hoff + ((j s + qmin + q) mod N) n + i][r], rows z of levels [l0, l1)
+__global__ void __launch_bounds__(256) mz_v_kernel(int N, const MapLevel* __restrict__ lv, int l0, int l1,
+                                                   const uint32_t* __restrict__ wtab, const double* __restrict__ H,
+                                                   int R, double* __restrict__ M) {
+    const int r = blockIdx.y * 32 + (threadIdx.x & 31);
+    const int64_t z0 = lv[l0].off, z1 = lv[l1 - 1].off + (int64_t)lv[l1 - 1].n * lv[l1 - 1].n;
+    for (int64_t z = z0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); z < z1;
+         z += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const MapLevel h = lv[map_level(lv, l0, l1, z, false)];
+        const int64_t c = z - h.off;
+        const int j = (int)(c / h.n), i = (int)(c % h.n);
+        int v = (int)((((int64_t)j * h.s + h.qmin) % N + N) % N);
+        const uint32_t* w = wtab + h.woff;
+        double acc = 0.0;
+        if (r < R)
+            for (int q = 0; q < h.wf; ++q) {
+                acc = fma((double)__ldg(w + q), H[(h.hoff + (int64_t)v * h.n + i) * R + r], acc);
+                if (++v == N) v = 0;
+            }
+        if (r < R) M[z * R + r] = acc * h.inv_tot;
+    }
+}
+
+// adjoint along v: G[hoff + v n + i][r] = inv_tot sum_j sum_q [(j s + qmin + q) = v mod N] w_q Z[off + j n + i][r]
+// (for d = (v - qmin) mod N the terms are q = d mod s + k s, j = d div s - k mod n, k = 0, 1, ... while q < wf)
+__global__ void __launch_bounds__(256) u_g_kernel(int N, const MapLevel* __restrict__ lv, int l0, int l1,
+                                                  const uint32_t* __restrict__ wtab, const double* __restrict__ Z,
+                                                  int R, double* __restrict__ G) {
+    const int r = blockIdx.y * 32 + (threadIdx.x & 31);
+    const int64_t g0 = lv[l0].hoff, g1 = lv[l1 - 1].hoff + (int64_t)N * lv[l1 - 1].n;
+    for (int64_t g = g0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); g < g1;
+         g += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const MapLevel h = lv[map_level(lv, l0, l1, g, true)];
+        const int64_t c = g - h.hoff;
+        const int v = (int)(c / h.n), i = (int)(c % h.n);
+        const int d = (int)((((int64_t)v - h.qmin) % N + N) % N);
+        int j = d / h.s;
+        const uint32_t* w = wtab + h.woff;
+        double acc = 0.0;
+        if (r < R)
+            for (int q = d % h.s; q < h.wf; q += h.s) {
+                acc = fma((double)__ldg(w + q), Z[(h.off + (int64_t)j * h.n + i) * R + r], acc);
+                if (--j < 0) j = h.n - 1;
+            }
+        if (r < R) G[g * R + r] = acc * h.inv_tot;
+    }
+}
+
+// adjoint along u, summed over levels [l0, l1): U[v N + u][r] (+)= sum_l sum_k w_{p0 + k s} G_l[v][i0 - k mod n][r]
+__global__ void __launch_bounds__(256) u_h_kernel(int N, const MapLevel* __restrict__ lv, int l0, int l1,
+                                                  const uint32_t* __restrict__ wtab, const double* __restrict__ G,
+                                                  int R, int accumulate, double* __restrict__ U) {
+    const int r = blockIdx.y * 32 + (threadIdx.x & 31);
+    const int64_t nt = (int64_t)N * N;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        if (r >= R) continue;
+        const int v = (int)(t / N), u = (int)(t % N);
+        double acc = accumulate ? U[t * R + r] : 0.0;
+        for (int l = l0; l < l1; ++l) {
+            const MapLevel h = lv[l];
+            const int d = (int)((((int64_t)u - h.qmin) % N + N) % N);
+            int i = d / h.s;
+            const uint32_t* w = wtab + h.woff;
+            const double* Gv = G + (h.hoff + (int64_t)v * h.n) * R + r;
+            for (int p = d % h.s; p < h.wf; p += h.s) {
+                acc = fma((double)__ldg(w + p), Gv[(int64_t)i * R], acc);
+                if (--i < 0) i = h.n - 1;
+            }
+        }
+        U[t * R + r] = acc;
+    }
+}
+
+// mode X (key = bx, other = Y[by]) or Y (key = by, other = X[bx]): per-CTA partial sums over its texels,
+// part[blockIdx.x][key][r] (smem fp64 atomics; the partials are then summed in a fixed order)
+__global__ void __launch_bounds__(256) mxy_kernel(const uint16_t* __restrict__ bins, int N, int A, int ash, int mode,
+                                                  const double* __restrict__ O, const double* __restrict__ U, int R,
+                                                  double* __restrict__ part) {
+    extern __shared__ double sacc[];  // [A][32] accumulators, then [A][32] other factor
+    double* so = sacc + A * 32;
+    const int c0 = blockIdx.y * 32, lane = threadIdx.x & 31, r = c0 + lane;
+    for (int e = threadIdx.x; e < A * 32; e += blockDim.x) {
+        sacc[e] = 0.0;
+        const int rr = c0 + (e & 31);
+        so[e] = rr < R ? O[(e >> 5) * R + rr] : 0.0;
+    }
+    __syncthreads();
+    const int64_t nt = (int64_t)N * N;
+    if (r < R)
+        for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt;
+             t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+            const int b = __ldg(bins + t);
+            const int x = b & (A - 1), y = b >> ash;
+            const int key = mode == 1 ? x : y, oth = mode == 1 ? y : x;
+            atomicAdd(&sacc[key * 32 + lane], so[oth * 32 + lane] * U[t * R + r]);
+        }
+    __syncthreads();
+    for (int e = threadIdx.x; e < A * 32; e += blockDim.x) {
+        const int rr = c0 + (e & 31);
+        if (rr < R) part[((int64_t)blockIdx.x * A + (e >> 5)) * R + rr] = sacc[e];
+    }
+}
+
+// ||D||^2 = sum_z sum_b (cnt_b / tot)^2 without forming D: exact uint64 bin counts of each footprint in
+// shared memory, read back (and cleared) by a second walk of the same window -- so a row costs O(window),
+// not O(A^2); bins with y in [y0, y0 + AS) per slab when A^2 counts exceed shared memory.
+__global__ void __launch_bounds__(256) sumsq_rows_kernel(const uint16_t* __restrict__ bins, int N, int A, int ash,
+                                                         int AS, const MapLevel* __restrict__ lv, int L,
+                                                         const uint32_t* __restrict__ wtab, int64_t P,
+                                                         double* __restrict__ part) {
+    extern __shared__ unsigned long long cnt[];  // [AS][A]
+    for (int e = threadIdx.x; e < AS * A; e += blockDim.x) cnt[e] = 0ull;
+    __syncthreads();
+    double acc = 0.0;
+    for (int64_t z = blockIdx.x; z < P; z += gridDim.x) {
+        const MapLevel h = lv[map_level(lv, 0, L, z, false)];
+        const int64_t c = z - h.off;
+        const int i = (int)(c % h.n), j = (int)(c / h.n);
+        const int bu = (int)((((int64_t)i * h.s + h.qmin) % N + N) % N);
+        const int bv = (int)((((int64_t)j * h.s + h.qmin) % N + N) % N);
+        const uint32_t* w = wtab + h.woff;
+        const int nwin = h.wf * h.wf;
+        double rs = 0.0;
+        for (int y0 = 0; y0 < A; y0 += AS) {
+            for (int pass = 0; pass < 2; ++pass) {
+                for (int t = threadIdx.x; t < nwin; t += blockDim.x) {
+                    const int q = t / h.wf, p = t - q * h.wf;
+                    int v = bv + q, u = bu + p;
+                    if (v >= N) v -= N;
+                    if (u >= N) u -= N;
+                    const int b = bins[(int64_t)v * N + u];
+                    const int y = (b >> ash) - y0;
+                    if (y < 0 || y >= AS) continue;
+                    unsigned long long* cp = &cnt[y * A + (b & (A - 1))];
+                    if (pass == 0) {
+                        atomicAdd(cp, (unsigned long long)__ldg(w + q) * (unsigned long long)__ldg(w + p));
+                    } else {
+                        const unsigned long long k = atomicExch(cp, 0ull);
+                        if (k) rs = fma((double)k, (double)k, rs);
+                    }
+                }
+                __syncthreads();
+            }
+        }
+        acc = fma(rs, h.inv_tot * h.inv_tot, acc);
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// HALS column pass for R > 128 (G = G1 * G2 too large for shared memory: read from global / L2)
+template <int KR>
+__global__ void __launch_bounds__(256) hals_global_kernel(double* __restrict__ F, int64_t rows, int R,
+                                                          const double* __restrict__ Md,
+                                                          const double* __restrict__ G1,
+                                                          const double* __restrict__ G2) {
+    const int lane = threadIdx.x & 31;
+    const int64_t w0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t z = w0; z < rows; z += nw) {
+        double f[KR];
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int s = lane + 32 * k;
+            f[k] = s < R ? F[z * R + s] : 0.0;
+        }
+        for (int r = 0; r < R; ++r) {
+            double dot = 0.0;
+#pragma unroll
+            for (int k = 0; k < KR; ++k) {
+                const int s = lane + 32 * k;
+                if (s < R) dot = fma(f[k], __ldg(G1 + s * R + r) * __ldg(G2 + s * R + r), dot);
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+            const double grr = G1[r * R + r] * G2[r * R + r];
+            if (grr > 0.0 && lane == (r & 31)) {
+                const double m = Md[z * R + r];
+#pragma unroll
+                for (int k = 0; k < KR; ++k)
+                    if (k == (r >> 5)) f[k] = fmax(kEps, f[k] + (m - dot) / grr);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < KR; ++k) {
+            const int s = lane + 32 * k;
+            if (s < R) F[z * R + s] = f[k];
+        }
+    }
+}
+
 }  // namespace als
 }  // namespace pndf
 
@@ -915,15 +1172,8 @@ struct Builder {
         Z = buf.alloc<double>(P * R);
         X = buf.alloc<double>((size_t)A * R);
         Y = buf.alloc<double>((size_t)A * R);
-        Zf = buf.alloc<float>(P * RP);
-        kr_hi = buf.alloc<float>((size_t)RP * A * A);
-        kr_lo = buf.alloc<float>((size_t)RP * A * A);
-        t_hi = buf.alloc<float>((size_t)RP * A);
-        t_lo = buf.alloc<float>((size_t)RP * A);
-        Mz = buf.alloc<float>(P * RP);
         Mx = buf.alloc<double>((size_t)A * R);
         My = buf.alloc<double>((size_t)A * R);
-        part = buf.alloc<float>((size_t)sms * BM * RP);
         GZ = buf.alloc<double>((size_t)R * R);
         GX = buf.alloc<double>((size_t)R * R);
         GY = buf.alloc<double>((size_t)R * R);
@@ -932,6 +1182,18 @@ struct Builder {
         sc = buf.alloc<double>((size_t)3 * R);
         terms = buf.alloc<double>(2);
         bad = buf.alloc<uint32_t>(1);
+        if (!D) {  // map-domain builder (pndf_cp_als_map): no tensor, no GEMM operands
+            Zf = nullptr;
+            Mz = nullptr;
+            return;
+        }
+        Zf = buf.alloc<float>(P * RP);
+        kr_hi = buf.alloc<float>((size_t)RP * A * A);
+        kr_lo = buf.alloc<float>((size_t)RP * A * A);
+        t_hi = buf.alloc<float>((size_t)RP * A);
+        t_lo = buf.alloc<float>((size_t)RP * A);
+        Mz = buf.alloc<float>(P * RP);
+        part = buf.alloc<float>((size_t)sms * BM * RP);
         mD_z = make_map(D, (uint64_t)P, (uint64_t)A * A, BM);
         const int64_t bres_b = (int64_t)(A / BK) * 2 * RP * BK * sizeof(float);  // resident B (hi + lo)
         kbs_xy = (A / BK > 1 && bres_b <= 64 * 1024) ? A / BK : 1;
@@ -1020,9 +1282,154 @@ struct Builder {
         if (KR <= 4) {
             ACK(cudaFuncSetAttribute(hals_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             hals_kernel<4><<<grid, 256, sm, st>>>(F, rows, R, g.RP, Mf, Md, G1, G2, Ff);
+        } else {  // R <= 256 (map-domain builder only: Md in fp64, no fp32 copy)
+            hals_global_kernel<8><<<grid, 256, 0, st>>>(F, rows, R, Md, G1, G2);
         }
         ACK(cudaGetLastError());
         gram(F, rows, Gout);
+    }
+};
+
+
+// Geometry of the map-domain builder: as check_desc, plus A <= 256, R <= 256 and no P * A limit (no GEMM)
+pndf_status check_desc_map(const pndf_desc* d, Geometry& g) {
+    if (!d || d->abi_version != PNDF_ABI_VERSION) return PNDF_EINVAL;
+    const int N = d->map_size, s0 = d->base_stride, L = d->num_levels, A = d->ang_res, R = d->rank;
+    auto pow2 = [](int64_t x) { return x > 0 && (x & (x - 1)) == 0; };
+    if (!pow2(N) || !pow2(s0) || s0 > N || L < 2 || L > 24 || (N / s0) < (1 << (L - 1))) return PNDF_EINVAL;
+    if (!pow2(A) || A < 2 || A > 256 || R < 1 || R > 256 || N > 32768 || !(d->flags & PNDF_WRAP)) return PNDF_EINVAL;
+    g.N = N;
+    g.s0 = s0;
+    g.L = L;
+    g.A = A;
+    g.R = R;
+    g.RP = (R + 31) / 32 * 32;
+    g.a_shift = ilog2i(A);
+    g.P = 0;
+    g.off.clear();
+    for (int l = 0; l < L; ++l) {
+        g.off.push_back(g.P);
+        const int64_t n = N / ((int64_t)s0 << l);
+        g.P += n * n;
+    }
+    return PNDF_OK;
+}
+
+// integer footprint weights of every level (reading 11; oracle/als.py footprint_weights): w is
+// the concatenated table, lv[l] = {qmin, wf, woff, tot = (sum w)^2} of level l
+void level_weights(const Geometry& g, std::vector<uint32_t>& w, std::vector<int64_t>& qmin, std::vector<int>& wf,
+                   std::vector<int>& woff, std::vector<double>& tot) {
+    for (int l = 0; l < g.L; ++l) {
+        const int sl = g.s0 << l;
+        const double sigma = 1.5 * sl / sqrt(12.0), c = 0.5 * (1.0 - sl);
+        const int64_t q0 = (int64_t)ceil(-4.0 * sigma - c), q1 = (int64_t)floor(4.0 * sigma - c);
+        const int f = (int)std::min<int64_t>(q1 - q0 + 1, g.N);
+        const size_t w0 = w.size();
+        w.resize(w0 + f, 0u);
+        for (int64_t q = q0; q <= q1; ++q) {
+            const double d = (double)q + c;
+            w[w0 + (size_t)((q - q0) % f)] += (uint32_t)llround(65536.0 * exp(-d * d / (2.0 * sigma * sigma)));
+        }
+        uint64_t sw = 0;
+        for (int p = 0; p < f; ++p) sw += w[w0 + p];
+        qmin.push_back(q0);
+        wf.push_back(f);
+        woff.push_back((int)w0);
+        tot.push_back((double)sw * (double)sw);
+    }
+}
+
+// Map-domain MTTKRPs (pndf_cp_als_map / pndf_mttkrp_map): level tables on the device, the pass buffer
+// (level 0's [N][n0] rows, or levels >= 1 stacked), U [N^2][R] and the mode-X/Y partials.
+struct MapOps {
+    const Geometry& g;
+    cudaStream_t st;
+    int sms;
+    const uint16_t* bins;
+    MapLevel* d_lv = nullptr;
+    uint32_t* d_w = nullptr;
+    double *HG = nullptr, *U = nullptr, *part = nullptr;
+    int pgrid = 0;
+    std::vector<MapLevel> lv;
+
+    MapOps(const Geometry& geo, cudaStream_t s, int nsm, Buffers& buf, const uint16_t* b)
+        : g(geo), st(s), sms(nsm), bins(b) {
+        std::vector<uint32_t> w;
+        std::vector<int64_t> qmin;
+        std::vector<int> wf, woff;
+        std::vector<double> tot;
+        level_weights(g, w, qmin, wf, woff, tot);
+        lv.resize(g.L);
+        int64_t hb = 0;  // group A = level 0 at pass row 0; group B = levels >= 1 stacked from row 0
+        for (int l = 0; l < g.L; ++l) {
+            const int sl = g.s0 << l;
+            if (l == 1) hb = 0;
+            lv[l] = MapLevel{g.off[l], hb, sl, g.N / sl, (int)qmin[l], wf[l], woff[l], 1.0 / tot[l]};
+            hb += (int64_t)g.N * (g.N / sl);
+        }
+        const int64_t n0 = g.N / g.s0;
+        const int64_t rows = std::max<int64_t>((int64_t)g.N * n0, hb);
+        d_lv = buf.alloc<MapLevel>(lv.size());
+        d_w = buf.alloc<uint32_t>(w.size());
+        ACK(cudaMemcpyAsync(d_lv, lv.data(), lv.size() * sizeof(MapLevel), cudaMemcpyHostToDevice, st));
+        ACK(cudaMemcpyAsync(d_w, w.data(), w.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, st));
+        HG = buf.alloc<double>((size_t)rows * g.R);
+        U = buf.alloc<double>((size_t)g.N * g.N * g.R);
+        pgrid = 2 * sms;
+        part = buf.alloc<double>((size_t)pgrid * g.A * g.R);
+    }
+    dim3 grid(int64_t warps) const {
+        return dim3((unsigned)std::max<int64_t>(1, std::min<int64_t>((warps + 7) / 8, 16 * sms)), (g.R + 31) / 32);
+    }
+    // M [P][R] = D_(z) (X kr Y), fp64
+    void mz(const double* X, const double* Y, double* M) {
+        const size_t sm = (size_t)2 * g.A * 32 * sizeof(double);
+        ACK(cudaFuncSetAttribute(mz_h_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        for (int grp = 0; grp < 2; ++grp) {
+            const int l0 = grp ? 1 : 0, l1 = grp ? g.L : 1;
+            int64_t hrows = 0, zrows = 0;
+            for (int l = l0; l < l1; ++l) {
+                hrows += (int64_t)g.N * lv[l].n;
+                zrows += (int64_t)lv[l].n * lv[l].n;
+            }
+            mz_h_kernel<<<grid(hrows), 256, sm, st>>>(bins, g.N, g.A, g.a_shift, d_lv, l0, l1, d_w, X, Y, g.R, HG);
+            mz_v_kernel<<<grid(zrows), 256, 0, st>>>(g.N, d_lv, l0, l1, d_w, HG, g.R, M);
+            ACK(cudaGetLastError());
+        }
+    }
+    // U [N^2][R] = the adjoint blur of Z
+    void u(const double* Z) {
+        for (int grp = 0; grp < 2; ++grp) {
+            const int l0 = grp ? 1 : 0, l1 = grp ? g.L : 1;
+            int64_t hrows = 0;
+            for (int l = l0; l < l1; ++l) hrows += (int64_t)g.N * lv[l].n;
+            u_g_kernel<<<grid(hrows), 256, 0, st>>>(g.N, d_lv, l0, l1, d_w, Z, g.R, HG);
+            u_h_kernel<<<grid((int64_t)g.N * g.N), 256, 0, st>>>(g.N, d_lv, l0, l1, d_w, HG, g.R, grp, U);
+            ACK(cudaGetLastError());
+        }
+    }
+    // mode 1: M [A][R] = D_(x) (Z kr Y) with O = Y; mode 2: D_(y) (Z kr X) with O = X (needs u() first)
+    void mxy(int mode, const double* O, double* M, double* sumbuf_unused = nullptr) {
+        (void)sumbuf_unused;
+        const size_t sm = (size_t)2 * g.A * 32 * sizeof(double);
+        ACK(cudaFuncSetAttribute(mxy_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        mxy_kernel<<<dim3(pgrid, (g.R + 31) / 32), 256, sm, st>>>(bins, g.N, g.A, g.a_shift, mode, O, U, g.R, part);
+        sum_parts_kernel<<<g.A * g.R, 128, 0, st>>>(part, pgrid, g.A * g.R, M);
+        ACK(cudaGetLastError());
+    }
+    // ||D||^2 (fp64), synchronous
+    double sumsq(double* scratch /* >= 8 sms + 1 doubles */) {
+        const int AS = std::min(g.A, (int)((128 * 1024) / (8 * g.A)));
+        const size_t sm = (size_t)AS * g.A * sizeof(unsigned long long);
+        ACK(cudaFuncSetAttribute(sumsq_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        const int grid = (int)std::min<int64_t>(g.P, 2 * sms);
+        sumsq_rows_kernel<<<grid, 256, sm, st>>>(bins, g.N, g.A, g.a_shift, AS, d_lv, g.L, d_w, g.P, scratch);
+        sum_parts_kernel<<<1, 128, 0, st>>>(scratch, grid, 1, scratch + grid);
+        ACK(cudaGetLastError());
+        double v = 0.0;
+        ACK(cudaMemcpyAsync(&v, scratch + grid, sizeof(double), cudaMemcpyDeviceToHost, st));
+        ACK(cudaStreamSynchronize(st));
+        return v;
     }
 };
 
@@ -1103,6 +1510,83 @@ extern "C" pndf_status pndf_mttkrp(const pndf_desc* desc, const float* d_D, cons
     return PNDF_OK;
 }
 
+// The sweep loop shared by the tensor (GEMM) and map-domain builders: modes Z, X, Y with HALS updates, fit
+// error, norm balance (oracle/als.py hals_sweep), stopping rule (reading 15), then normalise (reading 16).
+// mz() fills the Z-mode MTTKRP (fp32 Mf or fp64 Md), prep_xy() runs after the Z update, mxy(mode, M) the
+// X / Y modes.
+template <class MZ, class PREP, class MXY>
+void als_loop(Builder& b, double nD2, const pndf_als_opts* o, double* h_err, int32_t* sweeps_out, float* d_C,
+              float* d_X, float* d_Y, float* d_Z, const float* Mf, const double* Md, MZ mz, PREP prep_xy, MXY mxy) {
+    const Geometry& g = b.g;
+    cudaStream_t st = b.st;
+    const int R = g.R, A = g.A;
+    const int64_t P = g.P;
+    double prev = -1.0, terms[2];
+    int sweeps = 0;
+    b.gram(b.X, A, b.GX);
+    b.gram(b.Y, A, b.GY);
+    for (int it = 0; it < o->max_sweeps; ++it) {
+        // Z: M_Z with (X, Y), G = (X'X) * (Y'Y); the pass also yields Z'Z
+        mz();
+        b.hals(b.Z, P, Mf, Md, b.GX, b.GY, b.Zf, b.GZ);
+        prep_xy();
+        // X: M_X with (Z, Y), G = (Z'Z) * (Y'Y)
+        mxy(1, b.Mx);
+        b.hals(b.X, A, nullptr, b.Mx, b.GZ, b.GY, nullptr, b.GX);
+        // Y: M_Y with (Z, X), G = (Z'Z) * (X'X)
+        mxy(2, b.My);
+        b.hals(b.Y, A, nullptr, b.My, b.GZ, b.GX, nullptr, b.GY);
+        err_terms_kernel<<<1, 256, 0, st>>>(b.My, b.Y, A, R, b.GZ, b.GX, b.GY, b.terms);
+        // norm balance; the next sweep's X'X and Y'Y follow by scaling
+        balance_scale_kernel<<<(R + 127) / 128, 128, 0, st>>>(b.GZ, b.GX, b.GY, R, b.sc);
+        scale_cols_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P, R, b.sc, 0, b.Zf, g.RP);
+        scale_cols_kernel<<<1, 256, 0, st>>>(b.X, A, R, b.sc + R, 0, nullptr, g.RP);
+        scale_cols_kernel<<<1, 256, 0, st>>>(b.Y, A, R, b.sc + 2 * R, 0, nullptr, g.RP);
+        scale_gram_kernel<<<(R * R + 255) / 256, 256, 0, st>>>(b.GX, R, b.sc + R);
+        scale_gram_kernel<<<(R * R + 255) / 256, 256, 0, st>>>(b.GY, R, b.sc + 2 * R);
+        ACK(cudaGetLastError());
+        ACK(cudaMemcpyAsync(terms, b.terms, sizeof(terms), cudaMemcpyDeviceToHost, st));
+        ACK(cudaStreamSynchronize(st));
+        const double err = sqrt(std::max(0.0, nD2 - 2.0 * terms[0] + terms[1]) / nD2);
+        if (h_err) h_err[it] = err;
+        sweeps = it + 1;
+        if (prev >= 0.0 && fabs(prev - err) < o->tol * std::max(prev, 1e-300)) break;
+        prev = err;
+    }
+    if (sweeps_out) *sweeps_out = sweeps;
+
+    if (o->flags & PNDF_ALS_NORMALISE) {
+        const int nb = (int)std::min<int64_t>(b.ggrid, std::max<int64_t>(1, P / 64));
+        double* sx = b.sc;           // [R]
+        double* sy = b.sc + R;       // [R]
+        double* sxy = b.sc + 2 * R;  // [R]
+        const int rb = (R + 127) / 128;
+        col_reduce_kernel<<<1, 128, 0, st>>>(b.X, A, R, 0, b.gpart);
+        col_finish_kernel<<<rb, 128, 0, st>>>(b.gpart, 1, R, 0, sx);
+        col_reduce_kernel<<<1, 128, 0, st>>>(b.Y, A, R, 0, b.gpart);
+        col_finish_kernel<<<rb, 128, 0, st>>>(b.gpart, 1, R, 0, sy);
+        mul2_kernel<<<rb, 128, 0, st>>>(sx, sy, R, sxy);
+        scale_cols_kernel<<<1, 256, 0, st>>>(b.X, A, R, sx, 1, nullptr, g.RP);
+        scale_cols_kernel<<<1, 256, 0, st>>>(b.Y, A, R, sy, 1, nullptr, g.RP);
+        scale_cols_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P, R, sxy, 0, nullptr, g.RP);
+        // C_r = max_z Z_r, Z /= C (GX's storage holds C: R doubles)
+        double* C = b.GX;
+        col_reduce_kernel<<<nb, 128, 0, st>>>(b.Z, P, R, 1, b.gpart);
+        col_finish_kernel<<<rb, 128, 0, st>>>(b.gpart, nb, R, 1, C);
+        scale_cols_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P, R, C, 1, nullptr, g.RP);
+        row_renorm_kernel<<<(int)((P + 255) / 256), 256, 0, st>>>(b.Z, P, R, C);
+        if (d_C) to_f32_kernel<<<1, 128, 0, st>>>(C, R, d_C);
+        ACK(cudaGetLastError());
+    } else if (d_C) {
+        fill_kernel<<<(R + 127) / 128, 128, 0, st>>>(d_C, R, 1.f);
+    }
+    to_f32_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P * R, d_Z);
+    to_f32_kernel<<<1, 256, 0, st>>>(b.X, (int64_t)A * R, d_X);
+    to_f32_kernel<<<1, 256, 0, st>>>(b.Y, (int64_t)A * R, d_Y);
+    ACK(cudaGetLastError());
+    ACK(cudaStreamSynchronize(st));
+}
+
 extern "C" pndf_status pndf_cp_als(const pndf_desc* desc, const float* d_D, const float* d_Dt, float* d_C,
                                    float* d_X, float* d_Y, float* d_Z, const pndf_als_opts* o, double* h_err,
                                    int32_t* sweeps_out, void* cuda_stream) {
@@ -1115,7 +1599,7 @@ extern "C" pndf_status pndf_cp_als(const pndf_desc* desc, const float* d_D, cons
     try {
         cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
         Builder b(g, st, d_D, d_Dt);
-        const int R = g.R, A = g.A;
+        const int A = g.A;
         const int64_t P = g.P;
         ACK(cudaMemsetAsync(b.bad, 0, sizeof(uint32_t), st));
         b.load(d_Z, P, b.Z, b.Zf);
@@ -1133,69 +1617,70 @@ extern "C" pndf_status pndf_cp_als(const pndf_desc* desc, const float* d_D, cons
         ACK(cudaMemcpyAsync(&bad, b.bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
         ACK(cudaStreamSynchronize(st));
         if (bad || !(nD2 > 0.0)) return PNDF_EINVAL;
+        als_loop(b, nD2, o, h_err, sweeps_out, d_C, d_X, d_Y, d_Z, b.Mz, nullptr, [&] { b.mttkrp_z(); }, [] {},
+                 [&](int mode, double* M) { b.mttkrp_xy(mode, M); });
+    } catch (const Fail& f) {
+        return f.st;
+    }
+    return PNDF_OK;
+}
 
-        double prev = -1.0, terms[2];
-        int sweeps = 0;
-        b.gram(b.X, A, b.GX);
-        b.gram(b.Y, A, b.GY);
-        for (int it = 0; it < o->max_sweeps; ++it) {
-            // Z: M_Z with (X, Y), G = (X'X) * (Y'Y); the pass also yields Z'Z
-            b.mttkrp_z();
-            b.hals(b.Z, P, b.Mz, nullptr, b.GX, b.GY, b.Zf, b.GZ);
-            // X: M_X with (Z, Y), G = (Z'Z) * (Y'Y)
-            b.mttkrp_xy(1, b.Mx);
-            b.hals(b.X, A, nullptr, b.Mx, b.GZ, b.GY, nullptr, b.GX);
-            // Y: M_Y with (Z, X), G = (Z'Z) * (X'X)
-            b.mttkrp_xy(2, b.My);
-            b.hals(b.Y, A, nullptr, b.My, b.GZ, b.GX, nullptr, b.GY);
-            err_terms_kernel<<<1, 256, 0, st>>>(b.My, b.Y, A, R, b.GZ, b.GX, b.GY, b.terms);
-            // norm balance; the next sweep's X'X and Y'Y follow by scaling
-            balance_scale_kernel<<<1, 128, 0, st>>>(b.GZ, b.GX, b.GY, R, b.sc);
-            scale_cols_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P, R, b.sc, 0, b.Zf, g.RP);
-            scale_cols_kernel<<<1, 256, 0, st>>>(b.X, A, R, b.sc + R, 0, nullptr, g.RP);
-            scale_cols_kernel<<<1, 256, 0, st>>>(b.Y, A, R, b.sc + 2 * R, 0, nullptr, g.RP);
-            scale_gram_kernel<<<(R * R + 255) / 256, 256, 0, st>>>(b.GX, R, b.sc + R);
-            scale_gram_kernel<<<(R * R + 255) / 256, 256, 0, st>>>(b.GY, R, b.sc + 2 * R);
-            ACK(cudaGetLastError());
-            ACK(cudaMemcpyAsync(terms, b.terms, sizeof(terms), cudaMemcpyDeviceToHost, st));
-            ACK(cudaStreamSynchronize(st));
-            const double err = sqrt(std::max(0.0, nD2 - 2.0 * terms[0] + terms[1]) / nD2);
-            if (h_err) h_err[it] = err;
-            sweeps = it + 1;
-            if (prev >= 0.0 && fabs(prev - err) < o->tol * std::max(prev, 1e-300)) break;
-            prev = err;
-        }
-        if (sweeps_out) *sweeps_out = sweeps;
+extern "C" pndf_status pndf_cp_als_map(const pndf_desc* desc, const uint16_t* d_bins, float* d_C, float* d_X,
+                                       float* d_Y, float* d_Z, const pndf_als_opts* o, double* h_err,
+                                       int32_t* sweeps_out, void* cuda_stream) {
+    Geometry g;
+    pndf_status s = check_desc_map(desc, g);
+    if (s != PNDF_OK) return s;
+    if (!d_bins || !d_X || !d_Y || !d_Z || !o || o->abi_version != PNDF_ABI_VERSION || o->max_sweeps < 1 ||
+        !(o->tol >= 0.0))
+        return PNDF_EINVAL;
+    try {
+        cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+        Builder b(g, st, nullptr, nullptr);
+        MapOps m(g, st, b.sms, b.buf, d_bins);
+        double* Mz = b.buf.alloc<double>((size_t)g.P * g.R);
+        ACK(cudaMemsetAsync(b.bad, 0, sizeof(uint32_t), st));
+        b.load(d_Z, g.P, b.Z, nullptr);
+        b.load(d_X, g.A, b.X, nullptr);
+        b.load(d_Y, g.A, b.Y, nullptr);
+        uint32_t bad = 0;
+        ACK(cudaMemcpyAsync(&bad, b.bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
+        const double nD2 = m.sumsq(b.gpart);  // synchronises
+        if (bad || !(nD2 > 0.0)) return PNDF_EINVAL;
+        als_loop(b, nD2, o, h_err, sweeps_out, d_C, d_X, d_Y, d_Z, nullptr, Mz, [&] { m.mz(b.X, b.Y, Mz); },
+                 [&] { m.u(b.Z); }, [&](int mode, double* M) { m.mxy(mode, mode == 1 ? b.Y : b.X, M); });
+    } catch (const Fail& f) {
+        return f.st;
+    }
+    return PNDF_OK;
+}
 
-        if (o->flags & PNDF_ALS_NORMALISE) {
-            const int nb = (int)std::min<int64_t>(b.ggrid, std::max<int64_t>(1, P / 64));
-            double* sx = b.sc;           // [R]
-            double* sy = b.sc + R;       // [R]
-            double* sxy = b.sc + 2 * R;  // [R]
-            col_reduce_kernel<<<1, 128, 0, st>>>(b.X, A, R, 0, b.gpart);
-            col_finish_kernel<<<1, 128, 0, st>>>(b.gpart, 1, R, 0, sx);
-            col_reduce_kernel<<<1, 128, 0, st>>>(b.Y, A, R, 0, b.gpart);
-            col_finish_kernel<<<1, 128, 0, st>>>(b.gpart, 1, R, 0, sy);
-            mul2_kernel<<<1, 128, 0, st>>>(sx, sy, R, sxy);
-            scale_cols_kernel<<<1, 256, 0, st>>>(b.X, A, R, sx, 1, nullptr, g.RP);
-            scale_cols_kernel<<<1, 256, 0, st>>>(b.Y, A, R, sy, 1, nullptr, g.RP);
-            scale_cols_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P, R, sxy, 0, nullptr, g.RP);
-            // C_r = max_z Z_r, Z /= C (GX's storage holds C: R doubles)
-            double* C = b.GX;
-            col_reduce_kernel<<<nb, 128, 0, st>>>(b.Z, P, R, 1, b.gpart);
-            col_finish_kernel<<<1, 128, 0, st>>>(b.gpart, nb, R, 1, C);
-            scale_cols_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P, R, C, 1, nullptr, g.RP);
-            row_renorm_kernel<<<(int)((P + 255) / 256), 256, 0, st>>>(b.Z, P, R, C);
-            if (d_C) to_f32_kernel<<<1, 128, 0, st>>>(C, R, d_C);
-            ACK(cudaGetLastError());
-        } else if (d_C) {
-            fill_kernel<<<(R + 127) / 128, 128, 0, st>>>(d_C, R, 1.f);
+extern "C" pndf_status pndf_mttkrp_map(const pndf_desc* desc, const uint16_t* d_bins, const float* d_Z,
+                                       const float* d_X, const float* d_Y, int32_t mode, double* d_M,
+                                       double* h_sumsq, void* cuda_stream) {
+    Geometry g;
+    pndf_status s = check_desc_map(desc, g);
+    if (s != PNDF_OK) return s;
+    if (!d_bins || !d_Z || !d_X || !d_Y || !d_M || mode < 0 || mode > 2) return PNDF_EINVAL;
+    try {
+        cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+        Builder b(g, st, nullptr, nullptr);
+        MapOps m(g, st, b.sms, b.buf, d_bins);
+        ACK(cudaMemsetAsync(b.bad, 0, sizeof(uint32_t), st));
+        b.load(d_Z, g.P, b.Z, nullptr);
+        b.load(d_X, g.A, b.X, nullptr);
+        b.load(d_Y, g.A, b.Y, nullptr);
+        if (mode == 0) {
+            m.mz(b.X, b.Y, d_M);
+        } else {
+            m.u(b.Z);
+            m.mxy(mode, mode == 1 ? b.Y : b.X, d_M);
         }
-        to_f32_kernel<<<b.blocks(P * R), 256, 0, st>>>(b.Z, P * R, d_Z);
-        to_f32_kernel<<<1, 256, 0, st>>>(b.X, (int64_t)A * R, d_X);
-        to_f32_kernel<<<1, 256, 0, st>>>(b.Y, (int64_t)A * R, d_Y);
-        ACK(cudaGetLastError());
+        uint32_t bad = 0;
+        ACK(cudaMemcpyAsync(&bad, b.bad, sizeof(bad), cudaMemcpyDeviceToHost, st));
         ACK(cudaStreamSynchronize(st));
+        if (bad) return PNDF_EINVAL;
+        if (h_sumsq) *h_sumsq = m.sumsq(b.gpart);
     } catch (const Fail& f) {
         return f.st;
     }

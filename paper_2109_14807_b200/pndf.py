@@ -73,7 +73,7 @@ EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_s
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
            "pndf_sg_queries", "pndf_load_tiles", "pndf_load_blocked", "pndf_hist_tensor", "pndf_cp_als",
-           "pndf_mttkrp", "pndf_rows_touched")
+           "pndf_mttkrp", "pndf_rows_touched", "pndf_cp_als_map", "pndf_mttkrp_map")
 
 ALS_NORMALISE = 1
 
@@ -139,6 +139,11 @@ def lib():
         L.pndf_cp_als.restype = i32
         L.pndf_cp_als.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, P, ctypes.POINTER(AlsOpts), P,
                                   ctypes.POINTER(i32), P]
+        L.pndf_cp_als_map.restype = i32
+        L.pndf_cp_als_map.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, ctypes.POINTER(AlsOpts), P,
+                                      ctypes.POINTER(i32), P]
+        L.pndf_mttkrp_map.restype = i32
+        L.pndf_mttkrp_map.argtypes = [ctypes.POINTER(Desc), P, P, P, P, i32, P, P, P]
         L.pndf_mttkrp.restype = i32
         L.pndf_mttkrp.argtypes = [ctypes.POINTER(Desc), P, P, P, P, P, i32, P, P]
         _lib = L
@@ -356,3 +361,23 @@ def cp_als(desc: Desc, d_D, d_Dt, d_Z, d_X, d_Y, d_C=None, max_sweeps: int = 500
     _check(lib().pndf_cp_als(ctypes.byref(desc), _ptr(d_D), _ptr(d_Dt), _ptr(d_C), _ptr(d_X), _ptr(d_Y),
                              _ptr(d_Z), ctypes.byref(o), _ptr(err), ctypes.byref(n), _stream(stream)), "pndf_cp_als")
     return err[:n.value].copy()
+
+
+def cp_als_map(desc: Desc, d_bins, d_Z, d_X, d_Y, d_C=None, max_sweeps: int = 500, tol: float = 1e-4,
+               normalise: bool = False, stream=None):
+    """pndf_cp_als_map: CP-ALS of the exact footprint tensor without forming it (device bins [N][N] uint16);
+    factors updated in place (device fp32); returns the fit-error history (numpy)."""
+    o = AlsOpts(abi_version=ABI_VERSION, max_sweeps=max_sweeps, tol=tol, flags=ALS_NORMALISE if normalise else 0)
+    err = np.zeros(max_sweeps, np.float64)
+    n = ctypes.c_int32(0)
+    _check(lib().pndf_cp_als_map(ctypes.byref(desc), _ptr(d_bins), _ptr(d_C), _ptr(d_X), _ptr(d_Y), _ptr(d_Z),
+                                 ctypes.byref(o), _ptr(err), ctypes.byref(n), _stream(stream)), "pndf_cp_als_map")
+    return err[:n.value].copy()
+
+
+def mttkrp_map(desc: Desc, d_bins, d_Z, d_X, d_Y, mode: int, d_M, stream=None) -> float:
+    """pndf_mttkrp_map (test support): one map-domain MTTKRP into d_M (fp64, device); returns ||D||^2."""
+    v = ctypes.c_double(0.0)
+    _check(lib().pndf_mttkrp_map(ctypes.byref(desc), _ptr(d_bins), _ptr(d_Z), _ptr(d_X), _ptr(d_Y), mode,
+                                 _ptr(d_M), ctypes.byref(v), _stream(stream)), "pndf_mttkrp_map")
+    return v.value
