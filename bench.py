@@ -1140,6 +1140,17 @@ def map_sweep_flop(cfg) -> int:
     return 2 * taps * R
 
 
+def map_sweep_bytes(cfg) -> int:
+    """Compulsory HBM bytes of one map-domain sweep: each pass buffer written once and read once (Z-mode pass
+    buffer and adjoint pass buffer, 2 N^2 R fp64 each over the level groups; U, N^2 R fp64, written by the two
+    level groups and read by the X and Y modes), the map bins per pass, and the Z-side arrays (Z read by the
+    adjoint, M_Z written then read, Z read and written by HALS: 5 P R fp64)."""
+    N, R, P = cfg.N, cfg.R, cfg.P
+    hb = sum(N * (N // (cfg.s0 << l)) for l in range(cfg.L)) * R * 8
+    u = N * N * R * 8
+    return 2 * 2 * hb + u * (2 + 1 + 2) + 5 * P * R * 8 + 6 * N * N * 2
+
+
 def run_als_map_op(args, cfg, rank, world, local_rank):
     """--op als_map (SURVEY §8(f) row 3 at config 3 scale): HALS CP-ALS of the config's footprint tensor with
     map-domain MTTKRPs (pndf_cp_als_map).  A step = one sweep; `e2e` = the whole builder at the paper's settings
@@ -1195,6 +1206,7 @@ def run_als_map_op(args, cfg, rank, world, local_rank):
     sms = _t.cuda.get_device_properties(dev).multi_processor_count
     fp64_peak = sms * 64 * 2 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
     fl = map_sweep_flop(cfg)
+    mb = map_sweep_bytes(cfg)
     achieved = fl / (ms_step * 1e-3) / 1e12
     dense = 3 * 2 * cfg.P * cfg.A * cfg.A * cfg.R
     line = {"metric": ALS_MAP_METRIC, "value": 1e3 / ms_step, "unit": "sweeps/s", "n_gpus": world,
@@ -1204,14 +1216,18 @@ def run_als_map_op(args, cfg, rank, world, local_rank):
                                    f"the dense tensor would be {cfg.P * cfg.A * cfg.A * 4 / 1e9:.0f} GB",
                        "fit_error_after_timed_sweeps": float(err[-1]),
                        "inputs": "map bins + factors resident in HBM; pass buffers (N^2 R fp64) larger than L2"},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": achieved / fp64_peak, "traffic": None,
+            "roofline": {"bound": "hbm", "achieved": mb / (ms_step * 1e-3) / 1e9, "peak": peaks["hbm_gbs"],
+                         "unit": "GB/s", "frac": mb / (ms_step * 1e-3) / 1e9 / peaks["hbm_gbs"], "traffic": None,
                          "kernel": "pndf::als::{mz_h,mz_v,u_g,u_h,mxy}_kernel + HALS/Gram kernels",
-                         "flop_per_sweep": fl, "dense_tensor_flop_per_sweep": dense,
-                         "peak_source": "derived: SMs x 64 FP64 lanes x 2 flop x sm_max_mhz (B200 FP64 37 TFLOP/s)",
-                         "note": "achieved = the map-domain passes' fp64 FMA work over the whole sweep time (HALS, "
-                                 "Gram, error and host sync included); the dense-tensor formulation would need "
-                                 "dense_tensor_flop_per_sweep"},
+                         "bytes_per_sweep": mb, "hbm_floor_ms": mb / (peaks["hbm_gbs"] * 1e9) * 1e3,
+                         "peak_source": f"{src} MEASURED_PEAKS.json hbm_gbs",
+                         "fp64": {"flop_per_sweep": fl, "tflops": achieved, "peak_tflops": fp64_peak,
+                                  "frac": achieved / fp64_peak,
+                                  "peak_source": "derived: SMs x 64 FP64 lanes x 2 flop x sm_max_mhz"},
+                         "dense_tensor_flop_per_sweep": dense,
+                         "note": "achieved = the compulsory pass-buffer traffic of a sweep (map_sweep_bytes) over "
+                                 "the whole sweep time (HALS, Gram, error and host sync included); the passes are "
+                                 "latency-bound gathers, far from both floors (DESIGN.md §5)"},
             # one pndf_cp_als_map call of K sweeps: 10 setup launches (factor loads, ||D||^2, Gram) + 25 per sweep
             # (4 Z-mode passes, 4 adjoint passes, 2 x 2 X/Y-mode, 3 x 2 HALS + Gram sums, error, balance, 5 scalings)
             "cpu_baseline": None, "gpu_launches": 10 + 25 * args.steps, "clocks": clk, "e2e": e2e}

@@ -753,6 +753,7 @@ __global__ void __launch_bounds__(256) mz_h_kernel(const uint16_t* __restrict__ 
         const uint16_t* brow = bins + (int64_t)v * N;
         const uint32_t* w = wtab + h.woff;
         double acc = 0.0;
+#pragma unroll 4
         for (int p = 0; p < h.wf; ++p) {
             const int b = __ldg(brow + u);
             acc = fma((double)__ldg(w + p), xs[(b & (A - 1)) * 32 + lane] * ys[(b >> ash) * 32 + lane], acc);
@@ -777,6 +778,7 @@ __global__ void __launch_bounds__(256) mz_v_kernel(int N, const MapLevel* __rest
         const uint32_t* w = wtab + h.woff;
         double acc = 0.0;
         if (r < R)
+#pragma unroll 4
             for (int q = 0; q < h.wf; ++q) {
                 acc = fma((double)__ldg(w + q), H[(h.hoff + (int64_t)v * h.n + i) * R + r], acc);
                 if (++v == N) v = 0;
@@ -802,6 +804,7 @@ __global__ void __launch_bounds__(256) u_g_kernel(int N, const MapLevel* __restr
         const uint32_t* w = wtab + h.woff;
         double acc = 0.0;
         if (r < R)
+#pragma unroll 4
             for (int q = d % h.s; q < h.wf; q += h.s) {
                 acc = fma((double)__ldg(w + q), Z[(h.off + (int64_t)j * h.n + i) * R + r], acc);
                 if (--j < 0) j = h.n - 1;
@@ -827,6 +830,7 @@ __global__ void __launch_bounds__(256) u_h_kernel(int N, const MapLevel* __restr
             int i = d / h.s;
             const uint32_t* w = wtab + h.woff;
             const double* Gv = G + (h.hoff + (int64_t)v * h.n) * R + r;
+#pragma unroll 4
             for (int p = d % h.s; p < h.wf; p += h.s) {
                 acc = fma((double)__ldg(w + p), Gv[(int64_t)i * R], acc);
                 if (--i < 0) i = h.n - 1;
@@ -871,13 +875,13 @@ __global__ void __launch_bounds__(256) mxy_kernel(const uint16_t* __restrict__ b
 // not O(A^2); bins with y in [y0, y0 + AS) per slab when A^2 counts exceed shared memory.
 __global__ void __launch_bounds__(256) sumsq_rows_kernel(const uint16_t* __restrict__ bins, int N, int A, int ash,
                                                          int AS, const MapLevel* __restrict__ lv, int L,
-                                                         const uint32_t* __restrict__ wtab, int64_t P,
+                                                         const uint32_t* __restrict__ wtab, int64_t z0, int64_t P,
                                                          double* __restrict__ part) {
     extern __shared__ unsigned long long cnt[];  // [AS][A]
     for (int e = threadIdx.x; e < AS * A; e += blockDim.x) cnt[e] = 0ull;
     __syncthreads();
     double acc = 0.0;
-    for (int64_t z = blockIdx.x; z < P; z += gridDim.x) {
+    for (int64_t z = z0 + blockIdx.x; z < P; z += gridDim.x) {
         const MapLevel h = lv[map_level(lv, 0, L, z, false)];
         const int64_t c = z - h.off;
         const int i = (int)(c % h.n), j = (int)(c / h.n);
@@ -907,6 +911,73 @@ __global__ void __launch_bounds__(256) sumsq_rows_kernel(const uint16_t* __restr
                 __syncthreads();
             }
         }
+        acc = fma(rs, h.inv_tot * h.inv_tot, acc);
+    }
+    __shared__ double red[256];
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
+
+// ||D||^2 over the rows [0, z1) of the small-window levels (wf^2 <= 64): one warp per row, the window's
+// (bin, weight) pairs merged in a 128-slot open-addressing table in the warp's shared memory (exact uint64
+// counts), whose squares are summed and cleared -- no CTA barrier per row.
+__global__ void __launch_bounds__(256) sumsq_small_kernel(const uint16_t* __restrict__ bins, int N,
+                                                          const MapLevel* __restrict__ lv, int L,
+                                                          const uint32_t* __restrict__ wtab, int64_t z1,
+                                                          double* __restrict__ part) {
+    constexpr int TS = 128;
+    __shared__ int skey[8][TS];
+    __shared__ unsigned long long scnt[8][TS];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    int* key = skey[wib];
+    unsigned long long* cnt = scnt[wib];
+    for (int e = lane; e < TS; e += 32) {
+        key[e] = -1;
+        cnt[e] = 0ull;
+    }
+    __syncwarp();
+    double acc = 0.0;
+    for (int64_t z = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; z < z1;
+         z += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const MapLevel h = lv[map_level(lv, 0, L, z, false)];
+        const int64_t c = z - h.off;
+        const int i = (int)(c % h.n), j = (int)(c / h.n);
+        const int bu = (int)((((int64_t)i * h.s + h.qmin) % N + N) % N);
+        const int bv = (int)((((int64_t)j * h.s + h.qmin) % N + N) % N);
+        const uint32_t* w = wtab + h.woff;
+        for (int t = lane; t < h.wf * h.wf; t += 32) {
+            const int q = t / h.wf, p = t - q * h.wf;
+            int v = bv + q, u = bu + p;
+            if (v >= N) v -= N;
+            if (u >= N) u -= N;
+            const int b = bins[(int64_t)v * N + u];
+            const unsigned long long wt = (unsigned long long)__ldg(w + q) * (unsigned long long)__ldg(w + p);
+            int k = (int)(((uint32_t)b * 2654435761u) >> 25);
+            while (true) {
+                const int old = atomicCAS(&key[k], -1, b);
+                if (old == -1 || old == b) {
+                    atomicAdd(&cnt[k], wt);
+                    break;
+                }
+                k = (k + 1) & (TS - 1);
+            }
+        }
+        __syncwarp();
+        double rs = 0.0;
+        for (int e = lane; e < TS; e += 32) {
+            if (key[e] != -1) {
+                const double k = (double)cnt[e];
+                rs = fma(k, k, rs);
+                key[e] = -1;
+                cnt[e] = 0ull;
+            }
+        }
+        __syncwarp();
         acc = fma(rs, h.inv_tot * h.inv_tot, acc);
     }
     __shared__ double red[256];
@@ -1418,16 +1489,20 @@ struct MapOps {
         ACK(cudaGetLastError());
     }
     // ||D||^2 (fp64), synchronous
-    double sumsq(double* scratch /* >= 8 sms + 1 doubles */) {
+    double sumsq(double* scratch /* >= 6 sms + 1 doubles */) {
         const int AS = std::min(g.A, (int)((128 * 1024) / (8 * g.A)));
         const size_t sm = (size_t)AS * g.A * sizeof(unsigned long long);
         ACK(cudaFuncSetAttribute(sumsq_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        const int grid = (int)std::min<int64_t>(g.P, 2 * sms);
-        sumsq_rows_kernel<<<grid, 256, sm, st>>>(bins, g.N, g.A, g.a_shift, AS, d_lv, g.L, d_w, g.P, scratch);
-        sum_parts_kernel<<<1, 128, 0, st>>>(scratch, grid, 1, scratch + grid);
+        int64_t zs = 0;  // rows of the levels whose windows have <= 64 texels (a prefix: wf grows with l)
+        for (int l = 0; l < g.L && (int64_t)lv[l].wf * lv[l].wf <= 64; ++l) zs = lv[l].off + (int64_t)lv[l].n * lv[l].n;
+        const int g1 = (int)std::max<int64_t>(1, std::min<int64_t>((zs + 7) / 8, 4 * sms));
+        const int g2 = (int)std::max<int64_t>(1, std::min<int64_t>(g.P - zs, 2 * sms));
+        sumsq_small_kernel<<<g1, 256, 0, st>>>(bins, g.N, d_lv, g.L, d_w, zs, scratch);
+        sumsq_rows_kernel<<<g2, 256, sm, st>>>(bins, g.N, g.A, g.a_shift, AS, d_lv, g.L, d_w, zs, g.P, scratch + g1);
+        sum_parts_kernel<<<1, 128, 0, st>>>(scratch, g1 + g2, 1, scratch + g1 + g2);
         ACK(cudaGetLastError());
         double v = 0.0;
-        ACK(cudaMemcpyAsync(&v, scratch + grid, sizeof(double), cudaMemcpyDeviceToHost, st));
+        ACK(cudaMemcpyAsync(&v, scratch + g1 + g2, sizeof(double), cudaMemcpyDeviceToHost, st));
         ACK(cudaStreamSynchronize(st));
         return v;
     }
