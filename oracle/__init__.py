@@ -70,6 +70,8 @@ def lib():
                                                 P, P, P, P, P, P]
         L.oracle_blocked_query_batch.argtypes = [ctypes.POINTER(BlockedDesc), P, P, P, P, P, P, P, ctypes.c_int64,
                                                  ctypes.c_int, P]
+        L.oracle_blocked_sample_batch.argtypes = [ctypes.POINTER(BlockedDesc), P, P, P, P, P, P, P, P,
+                                                  ctypes.c_int64, P, P, P, P, P]
         L.oracle_max_threads.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -213,6 +215,30 @@ def blocked_query_batch(cfg, bs, records: np.ndarray, mean: bool = True) -> np.n
     lib().oracle_blocked_query_batch(ctypes.byref(d), *[_ptr(a) for a in arr], _ptr(recs), recs.shape[0],
                                      1 if mean else 0, _ptr(out))
     return out
+
+
+def blocked_sample_batch(cfg, bs, records: np.ndarray, xi: np.ndarray):
+    """Importance sampling on the blocked store (Sec. 5.2), fp64: an angular block of the record's
+    rectangle chosen by the blocks' blended sums (xi[:, 10]), then the quad descent of sample_batch inside it
+    (xi[:, 0:8], jitter xi[:, 8:10]).  Returns dict of pixel int32 [n, 2] (-1 = none), prob (pixel SUM /
+    rectangle SUM), h, margin, block int32 [n] (chosen block, -1 = none)."""
+    d = BlockedDesc(N=cfg.N, s0=cfg.s0, L=cfg.L, A=cfg.A, t=bs.t, region=bs.region, R=bs.R,
+                    wrap=1 if cfg.wrap else 0)
+    recs = np.ascontiguousarray(records)
+    xi = np.ascontiguousarray(xi, np.float32)
+    n = recs.shape[0]
+    assert xi.shape == (n, 11)
+    arr = [np.ascontiguousarray(a, dt) for a, dt in ((bs.C, np.float32), (bs.X, np.float32), (bs.Y, np.float32),
+                                                    (bs.group_set, np.int32), (bs.slab_ptr, np.int64),
+                                                    (bs.Z, np.float32))]
+    pix = np.empty((n, 2), np.int32)
+    prob = np.empty(n, np.float64)
+    h = np.empty((n, 2), np.float64)
+    mg = np.empty(n, np.float64)
+    blk = np.empty(n, np.int32)
+    lib().oracle_blocked_sample_batch(ctypes.byref(d), *[_ptr(a) for a in arr], _ptr(recs), _ptr(xi), n,
+                                      _ptr(pix), _ptr(prob), _ptr(h), _ptr(mg), _ptr(blk))
+    return dict(pixel=pix, prob=prob, h=h, margin=mg, block=blk)
 
 
 def neighbours(desc: Desc, records: np.ndarray):

@@ -706,4 +706,151 @@ EXPORT void oracle_blocked_query_batch(const oracle_blocked* d, const float* C, 
     }
 }
 
+/* ------------------------------------------------------------------------
+ * Importance sampling on the blocked / clustered store (Sec. 5.2):
+ * "we first choose an image block to start, again according to their averaged
+ * NDF values", then the hierarchical quad descent of oracle_sample_batch
+ * inside the chosen block.  Readings (reading 26): the blocks are
+ * the store's t x t angular blocks that the record's rectangle overlaps, in
+ * order b = by * nb + bx; a block's weight is its Eq. 6 SUM over the part of
+ * the rectangle inside it, blended over the footprint's 8 neighbours (= its
+ * average x area: the paper's averages for the equal full blocks of a
+ * whole-image rectangle); xi[10] picks the block (first block with
+ * xi * total < cumulative weight; zero blocks never; rounding fallback = the
+ * last nonzero block); xi[0..] drive the descent levels inside it, xi[8], xi[9]
+ * jitter.  prob = the pixel's SUM / the rectangle's SUM (block pmf x descent
+ * pmf), margin = the smallest relative distance of any variate (block choice
+ * included) to its decision boundary; block[i] = the chosen block (-1 none).
+ */
+typedef struct {
+    int64_t rows[8];
+    double w[8];
+    int64_t reg[8];
+} oracle_bfoot;
+
+/* Eq. 6 SUM over [xa, xb) x [ya, yb) (global bins) restricted to angular block (bx, by), blended over the 8
+ * neighbours of the footprint */
+static double oracle_block_rect_sum(const oracle_blocked* d, const float* C, const float* X, const float* Y,
+                                    const int32_t* group_set, const int64_t* slab_ptr, const float* Z,
+                                    const oracle_bfoot* f, int bx, int by, int xa, int xb, int ya, int yb,
+                                    double* xs, double* ys) {
+    const oracle_desc pd = {d->N, d->s0, d->L, d->A, d->R, d->wrap};
+    const int t = d->t, nb = d->A / d->t, R = d->R;
+    const int lx1 = (xa > bx * t ? xa : bx * t) - bx * t, lx2 = (xb < bx * t + t ? xb : bx * t + t) - bx * t;
+    const int ly1 = (ya > by * t ? ya : by * t) - by * t, ly2 = (yb < by * t + t ? yb : by * t + t) - by * t;
+    if (lx2 <= lx1 || ly2 <= ly1) return 0.0;
+    const int b = by * nb + bx;
+    double sum = 0.0;
+    for (int k = 0; k < 8; ++k) {
+        const int64_t slab = slab_ptr[f->rows[k] * nb * nb + b];
+        if (slab < 0) continue; /* blank block */
+        const int set = group_set[f->reg[k] * nb * nb + b];
+        if (set < 0) continue;
+        for (int r = 0; r < R; ++r) { xs[r] = 0.0; ys[r] = 0.0; }
+        for (int x = lx1; x < lx2; ++x)
+            for (int r = 0; r < R; ++r) xs[r] += (double)X[((int64_t)set * t + x) * R + r];
+        for (int y = ly1; y < ly2; ++y)
+            for (int r = 0; r < R; ++r) ys[r] += (double)Y[((int64_t)set * t + y) * R + r];
+        sum += f->w[k] * oracle_range_sum(&pd, C + (int64_t)set * R, xs, ys, Z + slab * R);
+    }
+    return sum;
+}
+
+EXPORT void oracle_blocked_sample_batch(const oracle_blocked* d, const float* C, const float* X, const float* Y,
+                                        const int32_t* group_set, const int64_t* slab_ptr, const float* Z,
+                                        const oracle_rec* q, const float* xi /* [n][11] */, int64_t n,
+                                        int32_t* pixel /* [n][2] */, double* prob, double* hxy /* [n][2] */,
+                                        double* margin, int32_t* block) {
+    const oracle_desc pd = {d->N, d->s0, d->L, d->A, d->R, d->wrap};
+    const int t = d->t, nb = d->A / d->t;
+    const int64_t nr = d->N / d->region;
+#pragma omp parallel
+    {
+        double xs[4096], ys[4096];
+        double Sb[256];
+#pragma omp for schedule(dynamic, 64)
+        for (int64_t i = 0; i < n; ++i) {
+            oracle_bfoot f;
+            int x1, x2, y1, y2;
+            pixel[2 * i] = pixel[2 * i + 1] = -1;
+            prob[i] = NAN;
+            hxy[2 * i] = hxy[2 * i + 1] = NAN;
+            margin[i] = INFINITY;
+            block[i] = -1;
+            if (!oracle_valid(&pd, &q[i], &x1, &x2, &y1, &y2) || !oracle_neighbours(&pd, &q[i], f.rows, f.w)) continue;
+            for (int k = 0; k < 8; ++k) { /* region of the neighbour's centre (as oracle_blocked_query_batch) */
+                int64_t z = f.rows[k], off = 0;
+                int l = 0;
+                for (;; ++l) {
+                    const int64_t nn = d->N / ((int64_t)d->s0 << l);
+                    if (z < off + nn * nn) break;
+                    off += nn * nn;
+                }
+                const int64_t s = (int64_t)d->s0 << l, nn = d->N / s, c = z - off, ii = c % nn, jj = c / nn;
+                f.reg[k] = (((2 * jj + 1) * s) / (2 * d->region)) * nr + ((2 * ii + 1) * s) / (2 * d->region);
+            }
+            /* 1. block choice by the blocks' weights over the rectangle */
+            const int bx0 = x1 / t, bx1 = x2 / t, by0 = y1 / t, by1 = y2 / t;
+            double total = 0.0;
+            int nbk = 0;
+            for (int by = by0; by <= by1; ++by)
+                for (int bx = bx0; bx <= bx1; ++bx) {
+                    Sb[nbk] = oracle_block_rect_sum(d, C, X, Y, group_set, slab_ptr, Z, &f, bx, by, x1, x2 + 1, y1,
+                                                    y2 + 1, xs, ys);
+                    total += Sb[nbk++];
+                }
+            if (!(total > 0.0)) { prob[i] = 0.0; continue; }
+            double mg = INFINITY, cum = 0.0;
+            const double tb = (double)xi[11 * i + 10] * total;
+            int kb = -1;
+            for (int j = 0; j < nbk; ++j) {
+                if (Sb[j] > 0.0) {
+                    const double dist = fabs(tb - cum) / total;
+                    if (cum > 0.0 && dist < mg) mg = dist;
+                }
+                cum += Sb[j];
+                if (kb < 0 && tb < cum) kb = j;
+            }
+            if (kb < 0) for (int j = nbk - 1; j >= 0; --j) if (Sb[j] > 0.0) { kb = j; break; }
+            const int bx = bx0 + kb % (bx1 - bx0 + 1), by = by0 + kb / (bx1 - bx0 + 1);
+            block[i] = by * nb + bx;
+            /* 2. quad descent inside the chosen block (as oracle_sample_batch) */
+            int xa = x1 > bx * t ? x1 : bx * t, xb = (x2 + 1 < bx * t + t ? x2 + 1 : bx * t + t);
+            int ya = y1 > by * t ? y1 : by * t, yb = (y2 + 1 < by * t + t ? y2 + 1 : by * t + t);
+            const double root = Sb[kb];
+            double last = root;
+            for (int l = 0; xb - xa > 1 || yb - ya > 1; ++l) {
+                const int xm = xa + (xb - xa + 1) / 2, ym = ya + (yb - ya + 1) / 2;
+                const double Q[4] = {
+                    oracle_block_rect_sum(d, C, X, Y, group_set, slab_ptr, Z, &f, bx, by, xa, xm, ya, ym, xs, ys),
+                    oracle_block_rect_sum(d, C, X, Y, group_set, slab_ptr, Z, &f, bx, by, xm, xb, ya, ym, xs, ys),
+                    oracle_block_rect_sum(d, C, X, Y, group_set, slab_ptr, Z, &f, bx, by, xa, xm, ym, yb, xs, ys),
+                    oracle_block_rect_sum(d, C, X, Y, group_set, slab_ptr, Z, &f, bx, by, xm, xb, ym, yb, xs, ys)};
+                const double tot = ((Q[0] + Q[1]) + Q[2]) + Q[3];
+                const double tt = (double)xi[11 * i + l] * tot;
+                double c = 0.0;
+                int k = -1;
+                for (int j = 0; j < 4; ++j) {
+                    if (Q[j] > 0.0) {
+                        const double dist = fabs(tt - c) / tot;
+                        if (c > 0.0 && dist < mg) mg = dist;
+                    }
+                    c += Q[j];
+                    if (k < 0 && tt < c) k = j;
+                }
+                if (k < 0) for (int j = 3; j >= 0; --j) if (Q[j] > 0.0) { k = j; break; }
+                if (k & 1) xa = xm; else xb = xm;
+                if (k & 2) ya = ym; else yb = ym;
+                last = Q[k];
+            }
+            pixel[2 * i] = xa;
+            pixel[2 * i + 1] = ya;
+            prob[i] = last / total;
+            hxy[2 * i] = ((double)xa + (double)xi[11 * i + 8]) * 2.0 / d->A - 1.0;
+            hxy[2 * i + 1] = ((double)ya + (double)xi[11 * i + 9]) * 2.0 / d->A - 1.0;
+            margin[i] = mg;
+        }
+    }
+}
+
 EXPORT int oracle_max_threads(void) { return omp_get_max_threads(); }
