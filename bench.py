@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--config", type=int, default=5, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--op", default="query", choices=["query", "sample", "sg", "wang", "wang_sample", "blocked", "als",
-                                                      "als_map",
+                                                      "als_map", "blocked_sample",
                                                       "sweep"],
                     help="query: the range-query path (default); sample: SURVEY §8(f) row 1, hierarchical "
                          "importance sampling over the whole A x A image; sg: §8(f) row 4, environment-light "
@@ -994,6 +994,8 @@ def run_wang_op(args, cfg, rank, world, local_rank):
 
 
 BLOCKED_METRIC = "NDF range queries/sec on the blocked/clustered store (Sec. 4.2: t=16 blocks, 8x8-texel regions)"
+BLOCKED_SAMPLE_METRIC = ("NDF importance samples/sec on the blocked/clustered store (Sec. 5.2, P:387: block chosen by "
+                         "its averaged NDF, then the quad descent)")
 
 
 def blocked_roofline(cfg, n, k_ms):
@@ -1236,7 +1238,8 @@ def run_als_map_op(args, cfg, rank, world, local_rank):
 
 
 def run_blocked_op(args, cfg, rank, world, local_rank):
-    """--op blocked: the config's queries on the paper-faithful blocked / clustered store (exact-rank groups)."""
+    """--op blocked: the config's queries on the paper-faithful blocked / clustered store (exact-rank groups);
+    --op blocked_sample: importance samples over the whole image on it (block choice + descent)."""
     import torch
     import torch.distributed as dist
     import oracle
@@ -1253,12 +1256,24 @@ def run_blocked_op(args, cfg, rank, world, local_rank):
     store = pndf.load_blocked(cfg.N, cfg.s0, cfg.L, cfg.A, cfg.wrap, bs, device=local_rank)
     if args.lanes:
         store.set_lanes(args.lanes)
+    sample = args.op == "blocked_sample"
     recs = synth.gen_queries(cfg, bins, i0, i1)
+    if sample:
+        recs["rect"] = synth.pack_rect(0, cfg.A - 1, 0, cfg.A - 1)
+        xi_h = np.random.default_rng(700 + rank).random((n, 11), dtype=np.float32)
+        d_xi = torch.from_numpy(xi_h).to(dev)
     d_q = torch.from_numpy(recs.view(np.int32).reshape(-1, 4)).to(dev)
-    d_out = torch.empty(n, dtype=torch.float32, device=dev)
-    for _ in range(args.warmup):
-        store.query_batch(d_q, d_out, 0)
+    d_out = torch.empty((n, 4) if sample else n, dtype=torch.float32, device=dev)
+
+    def step(opts):
+        if sample:
+            store.sample_blocked(d_q, d_xi, d_out, None, opts)
+        else:
+            store.query_batch(d_q, d_out, opts)
         store.sync()
+
+    for _ in range(args.warmup):
+        step(0)
     store.reset_stats()
     clocks = ClockSampler(bus_id_of(dev))
     clocks.start()
@@ -1268,8 +1283,7 @@ def run_blocked_op(args, cfg, rank, world, local_rank):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
     for _ in range(args.steps):
-        store.query_batch(d_q, d_out, pndf.TIMING)
-        store.sync()
+        step(pndf.TIMING)
     e1.record()
     torch.cuda.synchronize()
     if world > 1:
@@ -1281,28 +1295,49 @@ def run_blocked_op(args, cfg, rank, world, local_rank):
     if rank != 0:
         store.free()
         return 0
-    idx = np.unique(np.random.default_rng(6).integers(0, n, min(n, 20000)))
-    t0 = time.perf_counter()
-    ref = oracle.blocked_query_batch(cfg, bs, recs[idx])
-    cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
-    got = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
-    err = np.abs(got - ref)
     nb = cfg.A // 16
+    k_ms = st["query_ms"] / max(1, st["timed_batches"])
+    if sample:
+        idx = np.unique(np.random.default_rng(6).integers(0, n, min(n, 4000)))
+        t0 = time.perf_counter()
+        ref = oracle.blocked_sample_batch(cfg, bs, recs[idx], xi_h[idx])
+        cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
+        o = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy()
+        pix = o[:, 3].view(np.uint32)
+        firm = (ref["pixel"][:, 0] >= 0) & (ref["margin"] > 1e-4)
+        passed = bool(np.array_equal((pix[firm] & 0xffff).astype(np.int64), ref["pixel"][firm, 0]) and
+                      np.array_equal((pix[firm] >> 16).astype(np.int64), ref["pixel"][firm, 1]) and
+                      np.allclose(o[firm, 2], ref["prob"][firm] * cfg.A * cfg.A / 4.0, rtol=1e-4))
+        levels = int(round(math.log2(16)))
+        # per sample: nb^2 block weights + 4 quads per descent level, each 8 neighbours x 9 flop per rank
+        roof = alu_roof((nb * nb + 4 * levels) * 8 * 9 * cfg.R, n, k_ms, "pndf::blocked_sample_kernel", "sample")
+        parity = {"checked": int(idx.shape[0]), "firm": int(firm.sum()), "pass": passed}
+    else:
+        idx = np.unique(np.random.default_rng(6).integers(0, n, min(n, 20000)))
+        t0 = time.perf_counter()
+        ref = oracle.blocked_query_batch(cfg, bs, recs[idx])
+        cpu_rate = idx.shape[0] / (time.perf_counter() - t0)
+        got = d_out[torch.from_numpy(idx).to(dev)].cpu().numpy().astype(np.float64)
+        err = np.abs(got - ref)
+        roof = blocked_roofline(cfg, n, k_ms)
+        parity = {"checked": int(idx.shape[0]), "pass": bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())}
     raw = cfg.P * cfg.A * cfg.A * 4
     comp = st["zc_bytes"] + st["prefix_bytes"] + cfg.P * nb * nb * 4 + bs.group_set.size * 4
-    line = {"metric": BLOCKED_METRIC, "value": n_total / (ms_step * 1e-3), "unit": "queries/s", "n_gpus": world,
+    unit = "samples/s" if sample else "queries/s"
+    line = {"metric": BLOCKED_SAMPLE_METRIC if sample else BLOCKED_METRIC, "value": n_total / (ms_step * 1e-3),
+            "unit": unit, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": workload_name(cfg) + "; blocked store t=16, 8-texel regions",
+            "config": {"workload": workload_name(cfg) + "; blocked store t=16, 8-texel regions" +
+                                   ("; whole-image sampling domain" if sample else ""),
                        "queries_total": n_total, "slabs": bs.info["n_slabs"], "groups": bs.info["n_groups"],
                        "blank_block_fraction": bs.info["blank_fraction"],
                        "storage_vs_raw_pyramid": comp / raw},
-            "roofline": blocked_roofline(cfg, n, st["query_ms"] / max(1, st["timed_batches"])),
-            "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
-                             "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
+            "roofline": roof,
+            "cpu_baseline": {"value": cpu_rate, "unit": unit, "cores": oracle.max_threads(),
+                             "kind": "oracle", "sample": f"{idx.shape[0]} records of the timed batch"},
             "gpu_launches": args.steps, "clocks": clk,
-            "parity_sample": {"checked": int(idx.shape[0]),
-                              "pass": bool(((err <= 1e-4 * np.abs(ref)) | (err <= 1e-7)).all())},
+            "parity_sample": parity,
             "e2e": None}
     print(json.dumps(line), flush=True)
     store.free()
@@ -1349,7 +1384,7 @@ def main():
             return run_sg_op(args, cfg, rank, world, local_rank)
         if args.op in ("wang", "wang_sample"):
             return run_wang_op(args, cfg, rank, world, local_rank)
-        if args.op == "blocked":
+        if args.op in ("blocked", "blocked_sample"):
             return run_blocked_op(args, cfg, rank, world, local_rank)
         if args.op == "sweep":
             return run_sweep_op(args, synth.CONFIGS[3], rank, world, local_rank)

@@ -299,6 +299,21 @@ pndf_status pndf_load_blocked(const pndf_block_desc* desc, const float* C, const
                               const int32_t* group_set, const int64_t* slab_ptr, const float* Z, int device,
                               void* cuda_stream, pndf_store* out);
 
+/* Importance sampling on a blocked / clustered store (pndf_load_blocked; Sec. 5.2; SURVEY §8(f)
+ * rows 1 x 2): "we first choose an image block to start, again according to their averaged NDF values"
+ * -- each t x t angular block of the record's rectangle is weighted by its Eq. 6 SUM over the part
+ * of the rectangle inside it, blended over the footprint's 8 neighbours with their own groups' factors;
+ * xi[i][10] picks the first block whose cumulative weight exceeds xi x total -- then the quad descent of
+ * pndf_sample_batch runs inside that block (xi[i][0..], jitter xi[i][8], xi[i][9]).  pdf = the pixel's
+ * share of the rectangle's mass / pixel area (block pmf x descent pmf).  Choice rules: DESIGN.md reading 26.
+ *   d_xi    DEVICE [n][11] fp32 in [0,1)
+ *   d_out   DEVICE [n] pndf_sample (NaN + sticky PNDF_EQUERY for invalid records; pixel 0xffffffff and
+ *           pdf 0 when the rectangle holds no mass)
+ *   d_block DEVICE [n] int32 chosen block by * nb + bx (-1 = none), or NULL
+ * opts: PNDF_TIMING.  Enqueued on cuda_stream; complete with pndf_sync.  EINVAL on other store kinds. */
+pndf_status pndf_sample_blocked(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
+                                pndf_sample* d_out, int32_t* d_block, uint32_t opts, void* cuda_stream);
+
 /* Test support: run only the binning pass (row a1) on n device records and copy
  * the permutation (query indices in binned order) to d_perm [n] and, if not
  * NULL, the sorted bin keys to d_keys [n] (device memory).  Synchronous. */

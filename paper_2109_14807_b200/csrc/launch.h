@@ -54,6 +54,10 @@ cudaError_t launch_level_sort(const QParams& p, const pndf_query* q, int64_t n, 
 // Blocked / clustered store (blocks.cu).
 cudaError_t launch_blocked_query(const QParams& p, const BlockParams& bp, int G, int NV, const pndf_query* q,
                                  int64_t n, float* out, int num_sms, cudaStream_t st);
+// Importance sampling on the blocked store (blocks.cu): xi [n][11], blk [n] chosen block (may be NULL).
+cudaError_t launch_blocked_sample(const QParams& p, const BlockParams& bp, int G, int NV, const pndf_query* q,
+                                  const float* xi, int64_t n, pndf_sample* out, int32_t* blk, int num_sms,
+                                  cudaStream_t st);
 cudaError_t launch_block_build(const float* X, const float* Y, int sets, int t, int R, int Rp, float* pool,
                                const float* Z, int64_t slabs, const float* C, const int32_t* slab_set, float* Zc,
                                uint32_t* flags, int num_sms, cudaStream_t st);

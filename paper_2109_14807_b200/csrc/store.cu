@@ -819,6 +819,30 @@ pndf_status pndf_sample_batch(pndf_store s, const pndf_query* d_queries, const f
     return PNDF_OK;
 }
 
+pndf_status pndf_sample_blocked(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
+                                pndf_sample* d_out, int32_t* d_block, uint32_t opts, void* cuda_stream) {
+    if (!s || n < 0 || (n > 0 && (!d_queries || !d_xi || !d_out))) return PNDF_EINVAL;
+    if (opts & ~PNDF_TIMING) return PNDF_EINVAL;
+    if (!s->blocked) return PNDF_EINVAL;
+    if (n == 0) return PNDF_OK;
+    if ((uintptr_t)d_queries % 16 != 0 || (uintptr_t)d_out % 16 != 0 || (uintptr_t)d_xi % 4 != 0 ||
+        (uintptr_t)d_block % 4 != 0)
+        return PNDF_EINVAL;
+    std::lock_guard<std::mutex> lk(s->mu);
+    DeviceGuard g(s->device);
+    cudaStream_t st = (cudaStream_t)cuda_stream;
+    const bool timing = (opts & PNDF_TIMING) != 0;
+    if (timing) CK(cudaEventRecord(s->ev[0], st));
+    if (timing) CK(cudaEventRecord(s->ev[1], st));
+    QParams p = s->qp;
+    CK(launch_blocked_sample(p, s->bp, s->G, s->NV, d_queries, d_xi, n, d_out, d_block, s->num_sms, st));
+    if (timing) CK(cudaEventRecord(s->ev[2], st));
+    s->stats.kernel_launches += 1;
+    s->stats.last_binned = 0;
+    s->timing_pending = timing;
+    return PNDF_OK;
+}
+
 pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const float* d_xi, int64_t n,
                               pndf_sample* d_out, int32_t* d_tile, uint32_t opts, void* cuda_stream) {
     if (!s || n < 0 || (n > 0 && (!d_queries || !d_xi || !d_out))) return PNDF_EINVAL;

@@ -73,7 +73,8 @@ EXPORTS = ("pndf_load_factors", "pndf_query_batch", "pndf_sample_batch", "pndf_s
            "pndf_error_string", "pndf_last_cuda_error", "pndf_abi_version", "pndf_store_stats_get",
            "pndf_store_stats_reset", "pndf_store_image", "pndf_set_lanes", "pndf_bin_permutation",
            "pndf_sg_queries", "pndf_load_tiles", "pndf_load_blocked", "pndf_hist_tensor", "pndf_cp_als",
-           "pndf_mttkrp", "pndf_rows_touched", "pndf_cp_als_map", "pndf_mttkrp_map")
+           "pndf_mttkrp", "pndf_rows_touched", "pndf_cp_als_map", "pndf_mttkrp_map",
+           "pndf_sample_blocked")
 
 ALS_NORMALISE = 1
 
@@ -105,6 +106,8 @@ def lib():
         L.pndf_sample_batch.argtypes = [P, P, P, i64, P, u32, P]
         L.pndf_sample_tiles.restype = i32
         L.pndf_sample_tiles.argtypes = [P, P, P, i64, P, P, u32, P]
+        L.pndf_sample_blocked.restype = i32
+        L.pndf_sample_blocked.argtypes = [P, P, P, i64, P, P, u32, P]
         L.pndf_sync.restype = i32
         L.pndf_sync.argtypes = [P, P]
         L.pndf_query_batch_host.restype = i32
@@ -239,6 +242,12 @@ class Store:
         n = xi.shape[0] if n is None else n
         _check(lib().pndf_sample_tiles(self.handle, _ptr(queries), _ptr(xi), n, _ptr(out), _ptr(tile), opts,
                                        _stream(stream)), "pndf_sample_tiles")
+
+    def sample_blocked(self, queries, xi, out, block=None, opts: int = 0, stream=None, n: int | None = None):
+        """pndf_sample_blocked: block choice + quad descent on a blocked store; xi [n, 11] fp32 (device)."""
+        n = queries.shape[0] if n is None else n
+        _check(lib().pndf_sample_blocked(self.handle, _ptr(queries), _ptr(xi), n, _ptr(out), _ptr(block), opts,
+                                         _stream(stream)), "pndf_sample_blocked")
 
     def sync(self, stream=None, raise_on_query_error: bool = True) -> int:
         st = lib().pndf_sync(self.handle, _stream(stream))
