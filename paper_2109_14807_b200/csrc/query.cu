@@ -191,6 +191,9 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(uint32_t* inou
         if (base + k < nb) inout[base + k] = v[k] + off;
 }
 
+#ifndef PNDF_RS_ATOMIC
+#define PNDF_RS_ATOMIC 1  // radix scatter ranking: 1 = leader atomics (pipelined rounds), 0 = load/store counters
+#endif
 constexpr int kRsThreads = 256;
 constexpr int kRsItems = 16;
 constexpr int kRsTile = kRsThreads * kRsItems;  // 4096 keys per tile
@@ -318,6 +321,23 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)
     // warp-private stable ranking: r[i] = items of the same digit earlier in this warp's segment
     uint32_t r[ITEMS / 2];  // two 16-bit ranks per register (a rank is < IPW)
     const uint32_t lt_mask = (1u << lane) - 1u;
+#if PNDF_RS_ATOMIC
+    // each round's group leader claims its group's run with a shared-memory atomicAdd that returns the
+    // digit's running count; one warp's atomics on an address are performed in program order, so runs are
+    // claimed round by round (stable), and no round waits for the previous round's counter store
+#pragma unroll
+    for (int i = 0; i < ITEMS; ++i) {
+        const bool ok = seg + i * 32 < nt;
+        const uint32_t d = (k[i] >> shift) & (RADIX - 1);
+        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : 0xffffffffu);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0u;
+        if (ok && lane == leader) base = atomicAdd(&s_cnt[warp][d], (uint32_t)__popc(peers));
+        base = __shfl_sync(0xffffffffu, base, leader);
+        const uint32_t ri = base + __popc(peers & lt_mask);
+        r[i >> 1] = (i & 1) ? (r[i >> 1] | (ri << 16)) : ri;
+    }
+#else
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         const bool ok = seg + i * 32 < nt;
@@ -331,6 +351,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)
         if (ok && lt == 0) s_cnt[warp][d] = base + __popc(peers);
         __syncwarp();
     }
+#endif
     if (LATE_V) {  // values are needed only for placement: their loads overlap the scans below
 #pragma unroll
         for (int i = 0; i < ITEMS; ++i) {

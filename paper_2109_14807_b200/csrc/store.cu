@@ -954,7 +954,12 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
     else
         chunk = std::max<int64_t>(int64_t(1) << 20, std::min<int64_t>(int64_t(1) << 26, (n + 7) / 8));
     chunk = std::min(chunk, n);
-    {  // fit kSlots x (records + results + binning scratch) in free device memory
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    const int used = (int)std::min<int64_t>(kSlots, nchunks);  // slot streams this call uses
+    bool fits = true;  // buffers of earlier calls already hold this call's chunks: no memory query
+    for (int k = 0; k < used; ++k)
+        fits = fits && s->slots[k].cap >= chunk && (!bin_all || s->slots[k].scratch.cap >= chunk);
+    if (!fits) {  // fit kSlots x (records + results + binning scratch) in free device memory
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
             int64_t have = 0;
@@ -967,7 +972,9 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
     }
     const bool binned = (opts & PNDF_BIN_ON) ? true : (bin_all && chunk >= kMinQ * s->P);
     const uint32_t chunk_opts = (opts & PNDF_SUM) | (binned ? PNDF_BIN_ON : PNDF_BIN_OFF);
-    for (auto& sl : s->slots) {
+    const int nuse = (int)std::min<int64_t>(kSlots, (n + chunk - 1) / chunk);  // chunk may have shrunk
+    for (int k = 0; k < nuse; ++k) {
+        Slot& sl = s->slots[k];
         if (!sl.st) CK(cudaStreamCreateWithFlags(&sl.st, cudaStreamNonBlocking));
         if (sl.cap < chunk) {
             cudaFree(sl.d_rec);
@@ -993,7 +1000,7 @@ pndf_status pndf_query_batch_host(pndf_store s, const pndf_query* h_queries, int
         if (r != PNDF_OK) return r;
         CK(cudaMemcpyAsync(h_out + a, sl.d_out, sizeof(float) * m, cudaMemcpyDeviceToHost, sl.st));
     }
-    for (auto& sl : s->slots) CK(cudaStreamSynchronize(sl.st));
+    for (int k = 0; k < nuse; ++k) CK(cudaStreamSynchronize(s->slots[k].st));
     return read_sticky(s);
 }
 
