@@ -74,8 +74,16 @@ __device__ __forceinline__ void quad_reduce(float& q0, float& q1, float& q2, flo
     }
 }
 
+#ifndef PNDF_SRELOAD
+#define PNDF_SRELOAD 1  // 1: re-read the range corners each level (fewer registers, no corner moves)
+#endif
+
+#ifndef PNDF_SMINB
+#define PNDF_SMINB 2  // resident CTAs per SM the register budget targets
+#endif
+
 template <int G, int NV, bool WRAP, bool BINNED, bool U32>
-__global__ void __launch_bounds__(256) sample_kernel(const QParams p, const pndf_query* __restrict__ q,
+__global__ void __launch_bounds__(256, PNDF_SMINB) sample_kernel(const QParams p, const pndf_query* __restrict__ q,
                                                      const float* __restrict__ xi, const uint32_t* __restrict__ idx,
                                                      int64_t n, pndf_sample* __restrict__ out) {
     constexpr int QPW = 32 / G;
@@ -166,6 +174,14 @@ __global__ void __launch_bounds__(256) sample_kernel(const QParams p, const pndf
 #pragma unroll
             for (int v = 0; v < NV; ++v) {
                 const int c = (gl + v * G) * 4;
+#if PNDF_SRELOAD
+                // the current range's corners are re-read with the midpoints (L1-resident rows, issued
+                // together, so no extra round trip) instead of being carried across levels in registers
+                sxa[v].load(PX + (size_t)xa * PSTRIDE, c, RP);
+                sxb[v].load(PX + (size_t)xb * PSTRIDE, c, RP);
+                sya[v].load(PY + (size_t)ya * PSTRIDE, c, RP);
+                syb[v].load(PY + (size_t)yb * PSTRIDE, c, RP);
+#endif
                 sxm[v].load(PX + (size_t)xm * PSTRIDE, c, RP);
                 sym[v].load(PY + (size_t)ym * PSTRIDE, c, RP);
             }
@@ -208,21 +224,29 @@ __global__ void __launch_bounds__(256) sample_kernel(const QParams p, const pndf
                 if (k < 0) k = qs[3] > 0.f ? 3 : (qs[2] > 0.f ? 2 : (qs[1] > 0.f ? 1 : 0));
                 if (k & 1) {
                     xa = xm;
+#if !PNDF_SRELOAD
 #pragma unroll
                     for (int v = 0; v < NV; ++v) sxa[v] = sxm[v];
+#endif
                 } else {
                     xb = xm;
+#if !PNDF_SRELOAD
 #pragma unroll
                     for (int v = 0; v < NV; ++v) sxb[v] = sxm[v];
+#endif
                 }
                 if (k & 2) {
                     ya = ym;
+#if !PNDF_SRELOAD
 #pragma unroll
                     for (int v = 0; v < NV; ++v) sya[v] = sym[v];
+#endif
                 } else {
                     yb = ym;
+#if !PNDF_SRELOAD
 #pragma unroll
                     for (int v = 0; v < NV; ++v) syb[v] = sym[v];
+#endif
                 }
                 last = qs[k];
                 ++lvl;
