@@ -10,6 +10,7 @@
 //   or  [2][A+1][Rp]   uint32 U32: round(S 2^e_r), see build.cu
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -40,6 +41,8 @@ struct QParams {
     const float* DT;               // range table [2][A][W][Rp]: DT[axis][x1][w-1] = the SAT difference of
                                    // [x1, x1+w) exactly as the query kernel computes it (NULL = none)
     int32_t dt_w;                  // W: widest range served by DT (0 = none)
+    const CUtensorMap* dt_tmap;    // HOST pointer: 2-D tensor map of DT ([rows][Rp], box {Rp, 1}) for the
+                                   // gather4 bulk copies of query_g4_kernel (NULL = none); not read on device
 };
 
 // Implicit Wang tiling (tiles.cu).

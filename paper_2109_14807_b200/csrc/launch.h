@@ -10,6 +10,10 @@ namespace pndf {
 
 bool lanes_supported(int G, int NV);
 
+// PNDF_NOG4=1 in the environment: G == 32 launches use query_kernel instead of query_g4_kernel (A/B runs;
+// results are bitwise identical either way).
+bool g4_disabled();
+
 // Query kernel over n records; idx != nullptr means the records are binned
 // and idx[i] is record i's position in the caller's output.
 cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,

@@ -26,6 +26,14 @@ bool lanes_supported(int G, int NV) {
     return g && v;
 }
 
+bool g4_disabled() {
+    static const int v = [] {
+        const char* e = getenv("PNDF_NOG4");
+        return (e && atoi(e) != 0) ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 cudaError_t launch_query(const QParams& p, int G, int NV, const pndf_query* q, const uint32_t* idx, int64_t n,
                          float* out, int num_sms, cudaStream_t st) {
     if (4 * G * NV != p.Rp) return cudaErrorInvalidValue;

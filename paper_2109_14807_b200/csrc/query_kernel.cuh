@@ -556,10 +556,272 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB) query_kernel(const QParam
     }
 }
 
+// --------------------------------------- gather4-staged query kernel (G == 32) --
+// query_kernel with a5's range-table rows staged by the bulk-copy engine: each warp owns PNDF_G4D slots
+// of shared memory, each holding the dx and dy rows of two consecutive queries; lane 0 fills a slot with
+// ONE cp.async.bulk.tensor ... tile::gather4 (4 arbitrary rows of the DT tensor map), completion on the
+// slot's mbarrier, 2 PNDF_G4D queries ahead.  The consumer's loads no longer sit on its scoreboards, so
+// the FFMA2 / FMUL2 chain of step s waits only for step s's own Zc rows.  Same arithmetic and order as
+// query_kernel: results are bitwise identical.
+#ifndef PNDF_G4D
+#define PNDF_G4D 2  // pair slots per warp (0: off)
+#endif
+
+template <int NV>
+struct G4Layout {
+    static constexpr int RP = 128 * NV;
+    static constexpr int D2 = PNDF_G4D > 0 ? PNDF_G4D : 1;
+    static constexpr int SLOT_F = 4 * RP;  // [q0 dx | q0 dy | q1 dx | q1 dy]
+    static constexpr size_t DESC = sizeof(QDesc) * kWarpsPerBlock * 32;
+    static constexpr size_t REUSE = 128;
+    static constexpr size_t ROWS = (size_t)kWarpsPerBlock * 32 * 2 * 4;  // per query: its dx, dy table rows
+    static constexpr size_t BARS = 128 * ((kWarpsPerBlock * D2 * 8 + 127) / 128);
+    static constexpr size_t RING = (size_t)kWarpsPerBlock * D2 * SLOT_F * 4;
+    static constexpr size_t BYTES = DESC + REUSE + ROWS + BARS + RING;
+};
+
+template <int NV, bool WRAP, bool BINNED, bool U32>
+__global__ void __launch_bounds__(kThreads, PNDF_MINB)
+    query_g4_kernel(const __grid_constant__ CUtensorMap tm, const QParams p, const pndf_query* __restrict__ q,
+                    const uint32_t* __restrict__ idx, int64_t n, int64_t chunk, float* __restrict__ out) {
+    using LY = G4Layout<NV>;
+    constexpr int G = 32;
+    constexpr int RP = LY::RP;
+    constexpr int D2 = LY::D2;
+    constexpr int SB = kSteps;
+    static_assert(SB % 2 == 0 && (SB / 2) % D2 == 0, "pair slots must tile a reduction batch");
+    constexpr int PSTRIDE = U32 ? RP : 2 * RP;
+    extern __shared__ __align__(128) unsigned char qsmem[];
+    QDesc(*sdesc)[32] = reinterpret_cast<QDesc(*)[32]>(qsmem);
+    uint32_t* sreuse = reinterpret_cast<uint32_t*>(qsmem + LY::DESC);
+    int2* srows = reinterpret_cast<int2*>(qsmem + LY::DESC + LY::REUSE);
+    uint64_t* sbar = reinterpret_cast<uint64_t*>(qsmem + LY::DESC + LY::REUSE + LY::ROWS);
+    float* sring = reinterpret_cast<float*>(qsmem + LY::DESC + LY::REUSE + LY::ROWS + LY::BARS);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    QDesc* wd = sdesc[warp];
+    int2* wrows = srows + warp * 32;  // gather4 row coordinates of the batch (decoded once per query)
+    uint64_t* wbar = sbar + warp * D2;
+    float* wring = sring + (size_t)warp * D2 * LY::SLOT_F;
+    const float* __restrict__ Zc = p.Zc;
+    const float* __restrict__ PXl = p.PXY + lane * 4;
+    if (lane == 0)
+        for (int k = 0; k < D2; ++k) mbar_init(wbar + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t phase = 0;
+    // lane 0: one gather4 of the dx / dy rows of queries 2 pr, 2 pr + 1 into slot pr % D2 (row 0 stands in
+    // for an axis whose range is wider than the table: its SAT rows are read at its step)
+    auto issue_pair = [&](int pr) {
+        if (lane == 0) {
+            const int4 rr = *reinterpret_cast<const int4*>(wrows + 2 * pr);
+            const int r0 = rr.x, r1 = rr.y, r2 = rr.z, r3 = rr.w;
+            const int k = pr % D2;
+            // (the slot's previous contents were consumed by every lane's FFMA2s before the __syncwarp that
+            // precedes this issue, so the bulk copy cannot overwrite a pending read)
+            mbar_arrive_expect_tx(wbar + k, 4 * RP * 4);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(wring + k * LY::SLOT_F)),
+                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+                "r"(smem_u32(wbar + k))
+                : "memory");
+        }
+    };
+
+    const int64_t c0 = (int64_t)blockIdx.x * chunk;
+    const int64_t c1 = min(n, c0 + chunk);
+    float4 zc[NV][8];
+    for (int64_t base = c0 + (int64_t)warp * 32; base < c1; base += (int64_t)kWarpsPerBlock * 32) {
+        {
+            const int64_t qi = base + lane;
+            bool valid = false;
+            QDesc& d = wd[lane];
+            if (qi < c1) {
+                const int64_t src = BINNED ? (int64_t)__ldg(idx + qi) : qi;
+                const pndf_query rec = ldg_query(q + src);
+                valid = decode<WRAP, true>(p, rec, (int32_t)src, d);
+            } else {
+                d.out = -1;
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    d.row[k] = 0;
+                    d.w[k] = 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) d.sat[k] = 0;
+                d.mode = 0;
+                d.div = 1.f;
+            }
+            uint32_t same_lo, same_hi;
+            int32_t mine[4];
+            reuse_masks<WRAP>(d, valid, lane > 0, -1, -1, -1, -1, &same_lo, &same_hi, mine);
+            if (lane == 0) {
+                sreuse[2 * warp] = same_lo;
+                sreuse[2 * warp + 1] = same_hi;
+            }
+            wrows[lane] = make_int2((d.mode & 1) ? d.sat[0] : 0, (d.mode & 2) ? d.sat[2] : 0);
+        }
+        __syncwarp();
+        const uint32_t reuse_lo = sreuse[2 * warp];
+        const uint32_t reuse_hi = sreuse[2 * warp + 1];
+#pragma unroll
+        for (int pr = 0; pr < D2; ++pr) issue_pair(pr);
+        float res = 0.f;
+#pragma unroll 1
+        for (int s0 = 0; s0 < 32; s0 += SB) {
+            float part[SB];
+#pragma unroll
+            for (int j = 0; j < SB; ++j) {
+                const int s = s0 + j;
+                const int k = (j / 2) % D2;  // == (s / 2) % D2: SB / 2 is a multiple of D2
+                if ((j & 1) == 0) {
+                    while (!mbar_try_wait(wbar + k, (phase >> k) & 1u)) {
+                    }
+                    phase ^= 1u << k;
+                }
+                const QDesc& d = wd[s];
+                const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
+                const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
+                const int dmode = d.mode;
+                const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
+                const bool reuse0 = s > 0 && ((reuse_lo >> s) & 1u);
+                const bool reuse1 = s > 0 && ((reuse_hi >> s) & 1u);
+                if (__builtin_expect(!(reuse0 && reuse1), 0)) {
+                    if (!reuse0) {
+                        const uint4 r03 = *reinterpret_cast<const uint4*>(&d.row[0]);
+                        const int row[4] = {(int)r03.x, (int)r03.y, (int)r03.z, (int)r03.w};
+#pragma unroll
+                        for (int v = 0; v < NV; ++v)
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                zc[v][kk] = ldg4_stream(Zc + (size_t)row[kk] * RP + (lane + v * G) * 4);
+                    }
+                    if (!reuse1) {
+                        const uint4 r47 = *reinterpret_cast<const uint4*>(&d.row[4]);
+                        const int row[4] = {(int)r47.x, (int)r47.y, (int)r47.z, (int)r47.w};
+#pragma unroll
+                        for (int v = 0; v < NV; ++v)
+#pragma unroll
+                            for (int kk = 0; kk < 4; ++kk)
+                                zc[v][4 + kk] = ldg4_stream(Zc + (size_t)row[kk] * RP + (lane + v * G) * 4);
+                    }
+                }
+                const float* sl = wring + k * LY::SLOT_F + (j & 1) * 2 * RP + lane * 4;
+                float4 dxv[NV], dyv[NV];
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    dxv[v] = *reinterpret_cast<const float4*>(sl + v * G * 4);
+                    dyv[v] = *reinterpret_cast<const float4*>(sl + RP + v * G * 4);
+                }
+                if (__builtin_expect(dmode != 3, 0)) {  // a wide range: its two SAT rows, read directly
+                    const int4 so = *reinterpret_cast<const int4*>(&d.sat[0]);
+#pragma unroll
+                    for (int v = 0; v < NV; ++v) {
+                        const int cv = v * G * 4;
+                        if (!(dmode & 1)) {
+                            const float* px0 = PXl + (int64_t)so.x * PSTRIDE;
+                            const float* px1 = PXl + (int64_t)so.y * PSTRIDE;
+                            if (U32) {
+                                const uint4 qx1 = ldg_sat(px1 + cv), qx0 = ldg_sat(px0 + cv);
+                                dxv[v] = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                                     __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                            } else {
+                                const float4 xh1 = ldg4(px1 + cv), xh0 = ldg4(px0 + cv);
+                                const float4 xl1 = ldg4(px1 + RP + cv), xl0 = ldg4(px0 + RP + cv);
+                                dxv[v] = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                                     (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                            }
+                        }
+                        if (!(dmode & 2)) {
+                            const float* py0 = PXl + (int64_t)so.z * PSTRIDE;
+                            const float* py1 = PXl + (int64_t)so.w * PSTRIDE;
+                            if (U32) {
+                                const uint4 qy1 = ldg_sat(py1 + cv), qy0 = ldg_sat(py0 + cv);
+                                dyv[v] = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                                     __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                            } else {
+                                const float4 yh1 = ldg4(py1 + cv), yh0 = ldg4(py0 + cv);
+                                const float4 yl1 = ldg4(py1 + RP + cv), yl0 = ldg4(py0 + RP + cv);
+                                dyv[v] = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                                     (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                            }
+                        }
+                    }
+                }
+                float2 acc2 = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const float4 dx = dxv[v], dy = dyv[v];
+                    float2 zxy = make_float2(0.f, 0.f), zzw = make_float2(0.f, 0.f);
+#pragma unroll
+                    for (int kk = 0; kk < 8; ++kk) {
+                        const float2 wk = make_float2(w[kk], w[kk]);
+                        zxy = __ffma2_rn(wk, make_float2(zc[v][kk].x, zc[v][kk].y), zxy);
+                        zzw = __ffma2_rn(wk, make_float2(zc[v][kk].z, zc[v][kk].w), zzw);
+                    }
+                    acc2 = __ffma2_rn(__fmul2_rn(make_float2(dx.x, dx.y), make_float2(dy.x, dy.y)), zxy, acc2);
+                    acc2 = __ffma2_rn(__fmul2_rn(make_float2(dx.z, dx.w), make_float2(dy.z, dy.w)), zzw, acc2);
+                }
+                part[j] = acc2.x + acc2.y;
+                if (j & 1) {  // both queries of the pair are done with the slot: refill it D2 pairs ahead
+                    __syncwarp();
+                    if (s / 2 + D2 < 16) issue_pair(s / 2 + D2);
+                }
+            }
+            group_reduce<G, SB>(part, lane);
+            const int jj = lane - s0;
+            int src_gl = 0;
+            {
+                int nv = SB, o = G / 2, rem = jj;
+                while (nv > 1 && o > 0) {
+                    nv >>= 1;
+                    if (rem >= nv) {
+                        src_gl |= o;
+                        rem -= nv;
+                    }
+                    o >>= 1;
+                }
+            }
+            const float got = __shfl_sync(0xffffffffu, part[0], src_gl & 31);
+            if (jj >= 0 && jj < SB) res = got;
+        }
+        const QDesc& mine = wd[lane];
+        const int32_t oi = mine.out;
+        const float div = mine.div;
+        __syncwarp();
+        if (oi >= 0) out[oi] = res / div;
+    }
+}
+
+template <int NV, bool W, bool B, bool U>
+static cudaError_t launch_g4(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
+                             int num_sms, cudaStream_t st) {
+    constexpr size_t smem = G4Layout<NV>::BYTES;
+    auto* kfn = query_g4_kernel<NV, W, B, U>;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kThreads, smem) != cudaSuccess || occ < 1)
+            occ = 1;
+    }
+    int64_t grid = (int64_t)num_sms * occ;
+    const int64_t need = (n + kThreads - 1) / kThreads;
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    int64_t chunk = (n + grid - 1) / grid;
+    chunk = (chunk + 31) / 32 * 32;
+    grid = (n + chunk - 1) / chunk;
+    kfn<<<(unsigned)grid, kThreads, smem, st>>>(*p.dt_tmap, p, q, idx, n, chunk, out);
+    return cudaGetLastError();
+}
+
 // ----------------------------------------------------------- launchers --
 template <int G, int NV, bool W, bool B, bool U>
 static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
                             int num_sms, cudaStream_t st) {
+    if constexpr (G == 32 && PNDF_G4D > 0 && NV <= 2) {
+        if (p.dt_tmap && p.dt_w > 0 && !g4_disabled()) return launch_g4<NV, W, B, U>(p, q, idx, n, out, num_sms, st);
+    }
     constexpr size_t smem = QLayout<G, NV, U>::BYTES;
     cudaFuncSetAttribute(query_kernel<G, NV, W, B, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     static int occ = -1;

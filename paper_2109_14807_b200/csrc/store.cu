@@ -2,6 +2,7 @@
 // enqueue (a1-a6 via query.cu), sync/errors (a7) and the end-to-end host
 // pipeline.  Declarations and argument contracts: include/pndf.h.
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include <stdint.h>
 #include <stdio.h>
 #include <string.h>
@@ -110,6 +111,7 @@ struct pndf_store_s {
     float* Zc = nullptr;
     float* PXY = nullptr;
     float* DT = nullptr;
+    CUtensorMap dt_tmap;  // DT as a 2-D tensor [rows][Rp] for query_g4_kernel's gather4 copies
     uint32_t* err = nullptr;
     Scratch main;
     Slot slots[kSlots];
@@ -151,6 +153,27 @@ void choose_lanes(int R, int* G, int* NV) {
     if (nv > 4) nv = 8;
     *G = g;
     *NV = nv;
+}
+
+// DT [rows][Rp] fp32 as a 2-D tensor map with a one-row box of the whole row (gather4 fetches 4 such rows);
+// false when the driver entry point is unavailable or the shape is outside TMA's limits (Rp > 256)
+bool encode_dt_map(const float* DT, int64_t rows, int Rp, CUtensorMap* out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    if (!fn || Rp > 256 || rows < 1) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)Rp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)Rp * sizeof(float)};
+    cuuint32_t box[2] = {(cuuint32_t)Rp, 1};
+    cuuint32_t es[2] = {1, 1};
+    return fn(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(DT), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 bool capturing(cudaStream_t st) {
@@ -720,6 +743,7 @@ static pndf_status load_impl(const pndf_desc* desc, int64_t P_override, const fl
     p.mean = 1;
     p.DT = nullptr;
     p.dt_w = 0;
+    p.dt_tmap = nullptr;
 #if PNDF_DTAB
     {  // range table for rectangles of side <= W (2 A W Rp floats; 8.4 MB for config 5)
         const int W = std::min(PNDF_DTW, A);
@@ -728,6 +752,7 @@ static pndf_status load_impl(const pndf_desc* desc, int64_t P_override, const fl
             cudaStreamSynchronize(st) == cudaSuccess) {
             p.DT = s->DT;
             p.dt_w = W;
+            p.dt_tmap = encode_dt_map(s->DT, (int64_t)2 * A * W, Rp, &s->dt_tmap) ? &s->dt_tmap : nullptr;
             s->stats.kernel_launches += 1;
             s->stats.range_table_bytes = (int64_t)sizeof(float) * 2 * A * W * Rp;
             s->stats.range_table_width = W;
