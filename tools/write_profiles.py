@@ -122,7 +122,8 @@ def main():
     traffic = {}
     q = os.path.join(GP, "prof_query_full.ncu-rep")
     if os.path.exists(q):
-        txt, dpq = summarize(q, nq, "pndf::query_kernel, config 5, binned, U32 SATs")
+        txt, dpq = summarize(q, nq, "pndf::query_g4_kernel (query kernel with gather4-staged range-table rows), "
+                                    "config 5, binned, U32 SATs")
         open(os.path.join(OUT, f"{rnd}_query_kernel_ncu.txt"), "w").write(txt)
         traffic["config5"] = {"dram_bytes_per_query": dpq["dram"], "l2_read_bytes_per_query": dpq["l2_read"],
                               "warp_instructions_per_query": dpq["inst"],
@@ -148,7 +149,8 @@ def main():
     if os.path.exists(la):
         open(os.path.join(OUT, f"{rnd}_launches_default.txt"), "w").write(launches(la))
     for name in ("bench_default", "bench_c1", "bench_c2", "bench_c3", "bench_c4", "bench_sample", "bench_sg",
-                 "bench_wang", "bench_wang_sample", "bench_blocked", "bench_als", "bench_sweep", "bench_c3_s04"):
+                 "bench_wang", "bench_wang_sample", "bench_blocked", "bench_blocked_sample", "bench_als",
+                 "bench_als_map", "bench_sweep", "bench_c3_s04"):
         b = os.path.join(GP, name + ".log")
         if os.path.exists(b):
             lines = [l for l in open(b).read().splitlines() if l.startswith("{")]
@@ -164,6 +166,10 @@ def main():
         txt1, _ = summarize(al, n_el, "pndf::als::mttkrp_gemm_kernel<32, 1> (mode X: [(P A) x A] . [A x 32], "
                                       "z-reducing epilogue), config 2", 1, "D element")
         open(os.path.join(OUT, f"{rnd}_als_gemm_ncu.txt"), "w").write(txt0 + "\n" + txt1)
+    la3 = os.path.join(GP, "launches_als_map.csv")
+    if os.path.exists(la3):
+        open(os.path.join(OUT, f"{rnd}_launches_als_map.txt"), "w").write(launches(la3).replace(
+            "`python bench.py` (default run)", "`python bench.py --op als_map --config 3 --steps 2 --warmup 3`"))
     la2 = os.path.join(GP, "launches_als.csv")
     if os.path.exists(la2):
         open(os.path.join(OUT, f"{rnd}_launches_als.txt"), "w").write(launches(la2).replace(
