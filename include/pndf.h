@@ -280,7 +280,8 @@ pndf_status pndf_sample_tiles(pndf_store s, const pndf_query* d_queries, const f
  *   slab_ptr  [P][nb^2] int64               Z row of (positional row, block), -1 = blank
  *   Z [num_slabs][R]                          per-slab positional factors
  * SATs are stored in the HILO format.  pndf_query_batch answers queries on it
- * (never binned); pndf_sample_batch returns PNDF_EINVAL. */
+ * (never binned); pndf_sample_blocked samples it (block choice + descent);
+ * pndf_sample_batch returns PNDF_EINVAL. */
 typedef struct {
     uint32_t abi_version; /* = PNDF_ABI_VERSION                                   */
     int32_t map_size;     /* N                                                    */
