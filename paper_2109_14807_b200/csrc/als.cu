@@ -721,15 +721,6 @@ struct MapLevel {
     double inv_tot;   // 1 / (sum w)^2
 };
 
-// copy the level table and the footprint weights into shared memory (every tap reads a weight and every
-// row its level: from global memory those were dependent loads on each warp's critical path)
-__device__ __forceinline__ void stage_tables(const MapLevel* __restrict__ lv, int L, const uint32_t* __restrict__ wtab,
-                                             int nw, MapLevel* slv, uint32_t* sw) {
-    for (int e = threadIdx.x; e < L; e += blockDim.x) slv[e] = lv[e];
-    for (int e = threadIdx.x; e < nw; e += blockDim.x) sw[e] = wtab[e];
-    __syncthreads();
-}
-
 // level of row g among levels [l0, l1) (pass-buffer rows when by_hoff, else Zc rows)
 __device__ __forceinline__ int map_level(const MapLevel* lv, int l0, int l1, int64_t g, bool by_hoff) {
     int l = l0;
@@ -739,20 +730,18 @@ __device__ __forceinline__ int map_level(const MapLevel* lv, int l0, int l1, int
 
 // H[hoff + v n + i][r] = sum_p w_p X[bx][r] Y[by][r] over texels (v, (i s + qmin + p) mod N), levels [l0, l1)
 __global__ void __launch_bounds__(256) mz_h_kernel(const uint16_t* __restrict__ bins, int N, int A, int ash,
-                                                   const MapLevel* __restrict__ glv, int L, int l0, int l1,
-                                                   const uint32_t* __restrict__ gw, int nw, const double* __restrict__ X,
+                                                   const MapLevel* __restrict__ lv, int l0, int l1,
+                                                   const uint32_t* __restrict__ wtab, const double* __restrict__ X,
                                                    const double* __restrict__ Y, int R, double* __restrict__ H) {
-    extern __shared__ double xs[];  // [2][A][32]: X, Y columns of this rank chunk, then the level tables
+    extern __shared__ double xs[];  // [2][A][32]: X, Y columns of this rank chunk
     double* ys = xs + A * 32;
-    MapLevel* lv = reinterpret_cast<MapLevel*>(ys + A * 32);
-    uint32_t* wtab = reinterpret_cast<uint32_t*>(lv + L);
     const int c0 = blockIdx.y * 32, lane = threadIdx.x & 31;
     for (int e = threadIdx.x; e < A * 32; e += blockDim.x) {
         const int r = c0 + (e & 31);
         xs[e] = r < R ? X[(e >> 5) * R + r] : 0.0;
         ys[e] = r < R ? Y[(e >> 5) * R + r] : 0.0;
     }
-    stage_tables(glv, L, gw, nw, lv, wtab);
+    __syncthreads();
     const int64_t g0 = lv[l0].hoff, g1 = lv[l1 - 1].hoff + (int64_t)N * lv[l1 - 1].n;
     const int r = c0 + lane;
     for (int64_t g = g0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); g < g1;
@@ -767,7 +756,7 @@ __global__ void __launch_bounds__(256) mz_h_kernel(const uint16_t* __restrict__ 
 #pragma unroll 4
         for (int p = 0; p < h.wf; ++p) {
             const int b = __ldg(brow + u);
-            acc = fma((double)w[p], xs[(b & (A - 1)) * 32 + lane] * ys[(b >> ash) * 32 + lane], acc);
+            acc = fma((double)__ldg(w + p), xs[(b & (A - 1)) * 32 + lane] * ys[(b >> ash) * 32 + lane], acc);
             if (++u == N) u = 0;
         }
         if (r < R) H[g * R + r] = acc;
@@ -775,13 +764,9 @@ __global__ void __launch_bounds__(256) mz_h_kernel(const uint16_t* __restrict__ 
 }
 
 // M[z][r] = inv_tot sum_q w_q H[hoff + ((j s + qmin + q) mod N) n + i][r], rows z of levels [l0, l1)
-__global__ void __launch_bounds__(256) mz_v_kernel(int N, const MapLevel* __restrict__ glv, int L, int l0, int l1,
-                                                   const uint32_t* __restrict__ gw, int nw, const double* __restrict__ H,
+__global__ void __launch_bounds__(256) mz_v_kernel(int N, const MapLevel* __restrict__ lv, int l0, int l1,
+                                                   const uint32_t* __restrict__ wtab, const double* __restrict__ H,
                                                    int R, double* __restrict__ M) {
-    extern __shared__ double tabs[];
-    MapLevel* lv = reinterpret_cast<MapLevel*>(tabs);
-    uint32_t* wtab = reinterpret_cast<uint32_t*>(lv + L);
-    stage_tables(glv, L, gw, nw, lv, wtab);
     const int r = blockIdx.y * 32 + (threadIdx.x & 31);
     const int64_t z0 = lv[l0].off, z1 = lv[l1 - 1].off + (int64_t)lv[l1 - 1].n * lv[l1 - 1].n;
     for (int64_t z = z0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); z < z1;
@@ -795,7 +780,7 @@ __global__ void __launch_bounds__(256) mz_v_kernel(int N, const MapLevel* __rest
         if (r < R)
 #pragma unroll 4
             for (int q = 0; q < h.wf; ++q) {
-                acc = fma((double)w[q], H[(h.hoff + (int64_t)v * h.n + i) * R + r], acc);
+                acc = fma((double)__ldg(w + q), H[(h.hoff + (int64_t)v * h.n + i) * R + r], acc);
                 if (++v == N) v = 0;
             }
         if (r < R) M[z * R + r] = acc * h.inv_tot;
@@ -804,13 +789,9 @@ __global__ void __launch_bounds__(256) mz_v_kernel(int N, const MapLevel* __rest
 
 // adjoint along v: G[hoff + v n + i][r] = inv_tot sum_j sum_q [(j s + qmin + q) = v mod N] w_q Z[off + j n + i][r]
 // (for d = (v - qmin) mod N the terms are q = d mod s + k s, j = d div s - k mod n, k = 0, 1, ... while q < wf)
-__global__ void __launch_bounds__(256) u_g_kernel(int N, const MapLevel* __restrict__ glv, int L, int l0, int l1,
-                                                  const uint32_t* __restrict__ gw, int nw, const double* __restrict__ Z,
+__global__ void __launch_bounds__(256) u_g_kernel(int N, const MapLevel* __restrict__ lv, int l0, int l1,
+                                                  const uint32_t* __restrict__ wtab, const double* __restrict__ Z,
                                                   int R, double* __restrict__ G) {
-    extern __shared__ double tabs[];
-    MapLevel* lv = reinterpret_cast<MapLevel*>(tabs);
-    uint32_t* wtab = reinterpret_cast<uint32_t*>(lv + L);
-    stage_tables(glv, L, gw, nw, lv, wtab);
     const int r = blockIdx.y * 32 + (threadIdx.x & 31);
     const int64_t g0 = lv[l0].hoff, g1 = lv[l1 - 1].hoff + (int64_t)N * lv[l1 - 1].n;
     for (int64_t g = g0 + (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5); g < g1;
@@ -825,7 +806,7 @@ __global__ void __launch_bounds__(256) u_g_kernel(int N, const MapLevel* __restr
         if (r < R)
 #pragma unroll 4
             for (int q = d % h.s; q < h.wf; q += h.s) {
-                acc = fma((double)w[q], Z[(h.off + (int64_t)j * h.n + i) * R + r], acc);
+                acc = fma((double)__ldg(w + q), Z[(h.off + (int64_t)j * h.n + i) * R + r], acc);
                 if (--j < 0) j = h.n - 1;
             }
         if (r < R) G[g * R + r] = acc * h.inv_tot;
@@ -833,13 +814,9 @@ __global__ void __launch_bounds__(256) u_g_kernel(int N, const MapLevel* __restr
 }
 
 // adjoint along u, summed over levels [l0, l1): U[v N + u][r] (+)= sum_l sum_k w_{p0 + k s} G_l[v][i0 - k mod n][r]
-__global__ void __launch_bounds__(256) u_h_kernel(int N, const MapLevel* __restrict__ glv, int L, int l0, int l1,
-                                                  const uint32_t* __restrict__ gw, int nw, const double* __restrict__ G,
+__global__ void __launch_bounds__(256) u_h_kernel(int N, const MapLevel* __restrict__ lv, int l0, int l1,
+                                                  const uint32_t* __restrict__ wtab, const double* __restrict__ G,
                                                   int R, int accumulate, double* __restrict__ U) {
-    extern __shared__ double tabs[];
-    MapLevel* lv = reinterpret_cast<MapLevel*>(tabs);
-    uint32_t* wtab = reinterpret_cast<uint32_t*>(lv + L);
-    stage_tables(glv, L, gw, nw, lv, wtab);
     const int r = blockIdx.y * 32 + (threadIdx.x & 31);
     const int64_t nt = (int64_t)N * N;
     for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt;
@@ -855,7 +832,7 @@ __global__ void __launch_bounds__(256) u_h_kernel(int N, const MapLevel* __restr
             const double* Gv = G + (h.hoff + (int64_t)v * h.n) * R + r;
 #pragma unroll 4
             for (int p = d % h.s; p < h.wf; p += h.s) {
-                acc = fma((double)w[p], Gv[(int64_t)i * R], acc);
+                acc = fma((double)__ldg(w + p), Gv[(int64_t)i * R], acc);
                 if (--i < 0) i = h.n - 1;
             }
         }
@@ -1445,8 +1422,6 @@ struct MapOps {
     double *HG = nullptr, *U = nullptr, *part = nullptr;
     int pgrid = 0;
     std::vector<MapLevel> lv;
-    int nw = 0;           // footprint weights in the table
-    size_t tab_bytes = 0; // level table + weights, staged in shared memory by the pass kernels
 
     MapOps(const Geometry& geo, cudaStream_t s, int nsm, Buffers& buf, const uint16_t* b)
         : g(geo), st(s), sms(nsm), bins(b) {
@@ -1465,8 +1440,6 @@ struct MapOps {
         }
         const int64_t n0 = g.N / g.s0;
         const int64_t rows = std::max<int64_t>((int64_t)g.N * n0, hb);
-        nw = (int)w.size();
-        tab_bytes = lv.size() * sizeof(MapLevel) + ((w.size() * sizeof(uint32_t) + 15) / 16) * 16;
         d_lv = buf.alloc<MapLevel>(lv.size());
         d_w = buf.alloc<uint32_t>(w.size());
         ACK(cudaMemcpyAsync(d_lv, lv.data(), lv.size() * sizeof(MapLevel), cudaMemcpyHostToDevice, st));
@@ -1481,9 +1454,8 @@ struct MapOps {
     }
     // M [P][R] = D_(z) (X kr Y), fp64
     void mz(const double* X, const double* Y, double* M) {
-        const size_t sm = (size_t)2 * g.A * 32 * sizeof(double) + tab_bytes;
+        const size_t sm = (size_t)2 * g.A * 32 * sizeof(double);
         ACK(cudaFuncSetAttribute(mz_h_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-        ACK(cudaFuncSetAttribute(mz_v_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_bytes));
         for (int grp = 0; grp < 2; ++grp) {
             const int l0 = grp ? 1 : 0, l1 = grp ? g.L : 1;
             int64_t hrows = 0, zrows = 0;
@@ -1491,23 +1463,19 @@ struct MapOps {
                 hrows += (int64_t)g.N * lv[l].n;
                 zrows += (int64_t)lv[l].n * lv[l].n;
             }
-            mz_h_kernel<<<grid(hrows), 256, sm, st>>>(bins, g.N, g.A, g.a_shift, d_lv, g.L, l0, l1, d_w, nw, X, Y,
-                                                       g.R, HG);
-            mz_v_kernel<<<grid(zrows), 256, tab_bytes, st>>>(g.N, d_lv, g.L, l0, l1, d_w, nw, HG, g.R, M);
+            mz_h_kernel<<<grid(hrows), 256, sm, st>>>(bins, g.N, g.A, g.a_shift, d_lv, l0, l1, d_w, X, Y, g.R, HG);
+            mz_v_kernel<<<grid(zrows), 256, 0, st>>>(g.N, d_lv, l0, l1, d_w, HG, g.R, M);
             ACK(cudaGetLastError());
         }
     }
     // U [N^2][R] = the adjoint blur of Z
     void u(const double* Z) {
-        ACK(cudaFuncSetAttribute(u_g_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_bytes));
-        ACK(cudaFuncSetAttribute(u_h_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tab_bytes));
         for (int grp = 0; grp < 2; ++grp) {
             const int l0 = grp ? 1 : 0, l1 = grp ? g.L : 1;
             int64_t hrows = 0;
             for (int l = l0; l < l1; ++l) hrows += (int64_t)g.N * lv[l].n;
-            u_g_kernel<<<grid(hrows), 256, tab_bytes, st>>>(g.N, d_lv, g.L, l0, l1, d_w, nw, Z, g.R, HG);
-            u_h_kernel<<<grid((int64_t)g.N * g.N), 256, tab_bytes, st>>>(g.N, d_lv, g.L, l0, l1, d_w, nw, HG, g.R,
-                                                                         grp, U);
+            u_g_kernel<<<grid(hrows), 256, 0, st>>>(g.N, d_lv, l0, l1, d_w, Z, g.R, HG);
+            u_h_kernel<<<grid((int64_t)g.N * g.N), 256, 0, st>>>(g.N, d_lv, l0, l1, d_w, HG, g.R, grp, U);
             ACK(cudaGetLastError());
         }
     }
