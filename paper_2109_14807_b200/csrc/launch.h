@@ -13,6 +13,9 @@ bool lanes_supported(int G, int NV);
 // PNDF_NOG4=1 in the environment: G == 32 launches use query_kernel instead of query_g4_kernel (A/B runs;
 // results are bitwise identical either way).
 bool g4_disabled();
+// PNDF_NOG5=1: G == 32 launches with a range table use query_g4_kernel instead of query_g5_kernel (A/B runs;
+// the two differ only in the order of the final rank sum).
+bool g5_disabled();
 
 // Query kernel over n records; idx != nullptr means the records are binned
 // and idx[i] is record i's position in the caller's output.

@@ -26,6 +26,14 @@ bool lanes_supported(int G, int NV) {
     return g && v;
 }
 
+bool g5_disabled() {
+    static const int v = [] {
+        const char* e = getenv("PNDF_NOG5");
+        return (e && atoi(e) != 0) ? 1 : 0;
+    }();
+    return v != 0;
+}
+
 bool g4_disabled() {
     static const int v = [] {
         const char* e = getenv("PNDF_NOG4");

@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #include "device.cuh"
 #include "launch.h"
 
@@ -815,10 +817,347 @@ static cudaError_t launch_g4(const QParams& p, const pndf_query* q, const uint32
     return cudaGetLastError();
 }
 
+// ------------------------------------------- lean gather4 query kernel (G == 32) --
+// query_g4_kernel's data path (range-table rows staged by tile::gather4, Zc rows reused in registers)
+// with a leaner step, the per-step control and reduction work cut down:
+//   * one warp-uniform reload branch per step (either level changed); the two levels' row loads inside it
+//     are predicated, not branched;
+//   * batches whose 32 records all take both ranges from the range table (every BJ config) run a step
+//     with no wide-range path at all (ballot at decode);
+//   * no shuffle reduction: each pair of steps stores its 32 per-lane partials over its own (consumed)
+//     descriptor slots, and at the end of the batch lane q sums query q's 32 partials in a fixed order.  A query's result still does not depend on where it sits in the batch
+//     (binned == unbinned bitwise), but it is not bitwise query_g4_kernel's (different summation order).
+#ifndef PNDF_G5D
+#define PNDF_G5D 2  // pair slots per warp
+#endif
+
+// a query's descriptor, then (after its step) its 32 per-lane partials.  144 B = 9 16-byte bank groups: the
+// decode's per-lane 16-byte stores to 32 consecutive slots and the end-of-batch per-lane reads of them are
+// bank-conflict free (a 128 B stride puts every lane on the same banks)
+struct __align__(16) QSlot {
+    QDesc d;
+    int32_t pad[12];
+};
+static_assert(sizeof(QSlot) == 144, "QSlot layout");
+
+template <int NV>
+struct G5Layout {
+    static constexpr int RP = 128 * NV;
+    static constexpr int D2 = PNDF_G5D;
+    static constexpr int SLOT_F = 4 * RP;  // [q0 dx | q0 dy | q1 dx | q1 dy]
+    static constexpr size_t SLOTS = sizeof(QSlot) * kWarpsPerBlock * 32;
+    static constexpr size_t ROWS = (size_t)kWarpsPerBlock * 32 * 4 * 4;  // per query: dx row, dy row, out, div
+    static constexpr size_t BARS = 128 * ((kWarpsPerBlock * D2 * 8 + 127) / 128);
+    static constexpr size_t RING = (size_t)kWarpsPerBlock * D2 * SLOT_F * 4;
+    static constexpr size_t RECS = (size_t)kWarpsPerBlock * 32 * 20;  // next batch: records (16 B), idx (4 B)
+    static constexpr size_t BYTES = SLOTS + ROWS + BARS + RING + RECS;
+};
+
+__device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit_wait_all() {
+    asm volatile("cp.async.commit_group;\n\tcp.async.wait_all;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+template <int NV, bool WRAP, bool BINNED, bool U32>
+__global__ void __launch_bounds__(kThreads, PNDF_MINB)
+    query_g5_kernel(const __grid_constant__ CUtensorMap tm, const QParams p, const pndf_query* __restrict__ q,
+                    const uint32_t* __restrict__ idx, int64_t n, int64_t chunk, float* __restrict__ out) {
+    using LY = G5Layout<NV>;
+    constexpr int G = 32;
+    constexpr int RP = LY::RP;
+    constexpr int D2 = LY::D2;
+    constexpr int SB = 8;  // steps per unrolled block
+    static_assert((SB / 2) % D2 == 0, "pair slots must tile an unrolled block");
+    constexpr int PSTRIDE = U32 ? RP : 2 * RP;
+    extern __shared__ __align__(128) unsigned char qsmem[];
+    QSlot* wslot = reinterpret_cast<QSlot*>(qsmem) + (threadIdx.x >> 5) * 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int4* wrows = reinterpret_cast<int4*>(qsmem + LY::SLOTS) + warp * 32;
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(qsmem + LY::SLOTS + LY::ROWS) + warp * D2;
+    float* wring = reinterpret_cast<float*>(qsmem + LY::SLOTS + LY::ROWS + LY::BARS) + (size_t)warp * D2 * LY::SLOT_F;
+    // the next batch's records (and, binned, their idx entries) arrive by cp.async while this batch runs
+    uint4* srec = reinterpret_cast<uint4*>(qsmem + LY::SLOTS + LY::ROWS + LY::BARS + LY::RING) + warp * 32;
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(qsmem + LY::SLOTS + LY::ROWS + LY::BARS + LY::RING +
+                                                 (size_t)kWarpsPerBlock * 32 * 16) + warp * 32;
+    const float* __restrict__ Zc = p.Zc + lane * 4;
+    if (lane == 0)
+        for (int k = 0; k < D2; ++k) mbar_init(wbar + k, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    __syncwarp();
+    uint32_t phase = 0;
+    auto issue_pair = [&](int pr) {
+        if (lane == 0) {
+            const int4 ra = wrows[2 * pr], rb = wrows[2 * pr + 1];
+            const int4 rr = make_int4(ra.x, ra.y, rb.x, rb.y);
+            const int k = pr % D2;
+            mbar_arrive_expect_tx(wbar + k, 4 * RP * 4);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(wring + k * LY::SLOT_F)),
+                "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(rr.x), "r"(rr.y), "r"(rr.z), "r"(rr.w),
+                "r"(smem_u32(wbar + k))
+                : "memory");
+        }
+    };
+
+    // one step of query s = s0 + j; NARROW: every query of the batch reads both ranges from the table
+    float4 zc[NV][8];
+    float pe = 0.f;  // the even step's partial, stored with the odd step's
+    auto step = [&](auto narrow_tag, int s0, int j, uint32_t nb, uint32_t lob, uint32_t hib) {
+        constexpr bool NARROW = decltype(narrow_tag)::value;
+        const int s = s0 + j;
+        const int k = (j / 2) % D2;
+        if ((j & 1) == 0) {
+            while (!mbar_try_wait(wbar + k, (phase >> k) & 1u)) {
+            }
+            phase ^= 1u << k;
+        }
+        const QDesc& d = wslot[s].d;
+        const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
+        const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
+        const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
+        if ((nb >> j) & 1u) {  // warp-uniform: a level's rows differ from the previous query's
+            const bool rl = !((lob >> j) & 1u), rh = !((hib >> j) & 1u);
+            const int4 r03 = *reinterpret_cast<const int4*>(&d.row[0]);
+            const int4 r47 = *reinterpret_cast<const int4*>(&d.row[4]);
+            const int row[8] = {r03.x, r03.y, r03.z, r03.w, r47.x, r47.y, r47.z, r47.w};
+#pragma unroll
+            for (int v = 0; v < NV; ++v)
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) {
+                    if (rl) zc[v][kk] = ldg4_stream(Zc + (size_t)row[kk] * RP + v * G * 4);
+                    if (rh) zc[v][4 + kk] = ldg4_stream(Zc + (size_t)row[4 + kk] * RP + v * G * 4);
+                }
+        }
+        const float* sl = wring + k * LY::SLOT_F + (j & 1) * 2 * RP + lane * 4;
+        float4 dxv[NV], dyv[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            dxv[v] = *reinterpret_cast<const float4*>(sl + v * G * 4);
+            dyv[v] = *reinterpret_cast<const float4*>(sl + RP + v * G * 4);
+        }
+        if constexpr (!NARROW) {
+            const int dmode = d.mode;
+            if (dmode != 3) {  // a wide range: its two SAT rows, read directly
+                const int4 so = *reinterpret_cast<const int4*>(&d.sat[0]);
+                const float* __restrict__ PXl = p.PXY + lane * 4;
+#pragma unroll
+                for (int v = 0; v < NV; ++v) {
+                    const int cv = v * G * 4;
+                    if (!(dmode & 1)) {
+                        const float* px0 = PXl + (int64_t)so.x * PSTRIDE;
+                        const float* px1 = PXl + (int64_t)so.y * PSTRIDE;
+                        if (U32) {
+                            const uint4 qx1 = ldg_sat(px1 + cv), qx0 = ldg_sat(px0 + cv);
+                            dxv[v] = make_float4(__uint2float_rn(qx1.x - qx0.x), __uint2float_rn(qx1.y - qx0.y),
+                                                 __uint2float_rn(qx1.z - qx0.z), __uint2float_rn(qx1.w - qx0.w));
+                        } else {
+                            const float4 xh1 = ldg4(px1 + cv), xh0 = ldg4(px0 + cv);
+                            const float4 xl1 = ldg4(px1 + RP + cv), xl0 = ldg4(px0 + RP + cv);
+                            dxv[v] = make_float4((xh1.x - xh0.x) + (xl1.x - xl0.x), (xh1.y - xh0.y) + (xl1.y - xl0.y),
+                                                 (xh1.z - xh0.z) + (xl1.z - xl0.z), (xh1.w - xh0.w) + (xl1.w - xl0.w));
+                        }
+                    }
+                    if (!(dmode & 2)) {
+                        const float* py0 = PXl + (int64_t)so.z * PSTRIDE;
+                        const float* py1 = PXl + (int64_t)so.w * PSTRIDE;
+                        if (U32) {
+                            const uint4 qy1 = ldg_sat(py1 + cv), qy0 = ldg_sat(py0 + cv);
+                            dyv[v] = make_float4(__uint2float_rn(qy1.x - qy0.x), __uint2float_rn(qy1.y - qy0.y),
+                                                 __uint2float_rn(qy1.z - qy0.z), __uint2float_rn(qy1.w - qy0.w));
+                        } else {
+                            const float4 yh1 = ldg4(py1 + cv), yh0 = ldg4(py0 + cv);
+                            const float4 yl1 = ldg4(py1 + RP + cv), yl0 = ldg4(py0 + RP + cv);
+                            dyv[v] = make_float4((yh1.x - yh0.x) + (yl1.x - yl0.x), (yh1.y - yh0.y) + (yl1.y - yl0.y),
+                                                 (yh1.z - yh0.z) + (yl1.z - yl0.z), (yh1.w - yh0.w) + (yl1.w - yl0.w));
+                        }
+                    }
+                }
+            }
+        }
+        // a6: (Xbar Ybar) . (sum_k w_k Zc_k) over this lane's 4 NV ranks; two accumulators (xy / zw lanes of
+        // the packed pairs) keep the product chain two deep
+        float2 exy[NV], ezw[NV];
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            exy[v] = __fmul2_rn(make_float2(dxv[v].x, dxv[v].y), make_float2(dyv[v].x, dyv[v].y));
+            ezw[v] = __fmul2_rn(make_float2(dxv[v].z, dxv[v].w), make_float2(dyv[v].z, dyv[v].w));
+        }
+        float2 a0 = make_float2(0.f, 0.f), a1 = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            float2 zxy = __fmul2_rn(make_float2(w[0], w[0]), make_float2(zc[v][0].x, zc[v][0].y));
+            float2 zzw = __fmul2_rn(make_float2(w[0], w[0]), make_float2(zc[v][0].z, zc[v][0].w));
+#pragma unroll
+            for (int kk = 1; kk < 8; ++kk) {
+                const float2 wk = make_float2(w[kk], w[kk]);
+                zxy = __ffma2_rn(wk, make_float2(zc[v][kk].x, zc[v][kk].y), zxy);
+                zzw = __ffma2_rn(wk, make_float2(zc[v][kk].z, zc[v][kk].w), zzw);
+            }
+            a0 = __ffma2_rn(exy[v], zxy, a0);
+            a1 = __ffma2_rn(ezw[v], zzw, a1);
+        }
+        const float2 a = __fadd2_rn(a0, a1);
+        const float part = a.x + a.y;
+        if ((j & 1) == 0) {
+            pe = part;
+        } else {
+            // both queries of the pair are done with their descriptors and the ring slot: the descriptor
+            // slots take the pair's partials, and the ring slot is refilled D2 pairs ahead
+            __syncwarp();
+            reinterpret_cast<float*>(wslot + s - 1)[lane] = pe;
+            reinterpret_cast<float*>(wslot + s)[lane] = part;
+            if (s / 2 + D2 < 16) issue_pair(s / 2 + D2);
+        }
+    };
+
+    const int64_t c0 = (int64_t)blockIdx.x * chunk;
+    const int nloc = (int)(min(n, c0 + chunk) - c0);  // this CTA's queries (chunk < 2^31)
+    // each lane fetches its own record of the next batch (no cross-lane hand-off, so no warp sync)
+    auto fetch_idx = [&](int blq) {
+        if (BINNED && blq + lane < nloc) cp_async_4(sidx + lane, idx + c0 + blq + lane);
+    };
+    auto fetch_rec = [&](int blq) {
+        if (blq + lane < nloc)
+            cp_async_16(srec + lane, q + (BINNED ? (int64_t)sidx[lane] : c0 + blq + lane));
+        cp_async_commit();
+    };
+    fetch_idx(warp * 32);
+    cp_async_commit_wait_all();
+    fetch_rec(warp * 32);
+    for (int bl = warp * 32; bl < nloc; bl += kWarpsPerBlock * 32) {
+        cp_async_commit_wait_all();
+        uint32_t same_lo, same_hi;
+        bool narrow_ok;
+        {
+            const int ql = bl + lane;
+            bool valid = false;
+            QDesc& d = wslot[lane].d;
+            d.out = -1;
+            d.div = 1.f;
+            if (ql < nloc) {
+                const int64_t src = BINNED ? (int64_t)sidx[lane] : c0 + ql;
+                const uint4 rv = srec[lane];
+                pndf_query rec;
+                rec.u = __uint_as_float(rv.x);
+                rec.v = __uint_as_float(rv.y);
+                rec.size = __uint_as_float(rv.z);
+                rec.rect = rv.w;
+                valid = decode<WRAP, true>(p, rec, (int32_t)src, d);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) {
+                    d.row[k] = 0;
+                    d.w[k] = 0.f;
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k) d.sat[k] = 0;
+                d.mode = 0;
+            }
+            int32_t mine[4];
+            reuse_masks<WRAP>(d, valid, lane > 0, -1, -1, -1, -1, &same_lo, &same_hi, mine);
+            // invalid / absent records (mode 0, zero weights, NaN or no output) may take the narrow step:
+            // it reads range-table row 0, finite, and their result is discarded or NaN anyway
+            narrow_ok = __all_sync(0xffffffffu, d.mode == 3 || !valid);
+            wrows[lane] = make_int4((d.mode & 1) ? d.sat[0] : 0, (d.mode & 2) ? d.sat[2] : 0, d.out,
+                                    __float_as_int(d.div));
+        }
+        __syncwarp();
+#pragma unroll
+        for (int pr = 0; pr < D2; ++pr) issue_pair(pr);
+        const int bn = bl + kWarpsPerBlock * 32;  // this warp's next batch
+        fetch_idx(bn);
+        cp_async_commit();
+        uint32_t nb = ~(same_lo & same_hi);  // bit j: step j reloads (shifted down a block at a time)
+        if (narrow_ok) {
+#pragma unroll 1
+            for (int s0 = 0; s0 < 32; s0 += SB) {
+#pragma unroll
+                for (int j = 0; j < SB; ++j) step(std::true_type{}, s0, j, nb, same_lo, same_hi);
+                nb >>= SB;
+                same_lo >>= SB;
+                same_hi >>= SB;
+                if (s0 == 0) {  // the next batch's idx entries have landed: fetch its records
+                    cp_async_commit_wait_all();
+                    fetch_rec(bn);
+                }
+            }
+        } else {
+#pragma unroll 1
+            for (int s0 = 0; s0 < 32; s0 += SB) {
+#pragma unroll
+                for (int j = 0; j < SB; ++j) step(std::false_type{}, s0, j, nb, same_lo, same_hi);
+                nb >>= SB;
+                same_lo >>= SB;
+                same_hi >>= SB;
+                if (s0 == 0) {
+                    cp_async_commit_wait_all();
+                    fetch_rec(bn);
+                }
+            }
+        }
+        __syncwarp();
+        // lane q: query q's 32 partials (chunk c = lanes 4c..4c+3)
+        const float4* pr4 = reinterpret_cast<const float4*>(wslot + lane);
+        float4 t[8];
+#pragma unroll
+        for (int c = 0; c < 8; ++c) t[c] = pr4[c];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            t[c].x += t[c + 4].x;
+            t[c].y += t[c + 4].y;
+            t[c].z += t[c + 4].z;
+            t[c].w += t[c + 4].w;
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            t[c].x += t[c + 2].x;
+            t[c].y += t[c + 2].y;
+            t[c].z += t[c + 2].z;
+            t[c].w += t[c + 2].w;
+        }
+        const float res = ((t[0].x + t[1].x) + (t[0].y + t[1].y)) + ((t[0].z + t[1].z) + (t[0].w + t[1].w));
+        const int4 mo = wrows[lane];
+        __syncwarp();  // the slots are rewritten by the next batch's decode
+        if (mo.z >= 0) out[mo.z] = res / __int_as_float(mo.w);  // a6: Eq. 6 mean (div = area) or sum (div = 1)
+    }
+}
+
+template <int NV, bool W, bool B, bool U>
+static cudaError_t launch_g5(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
+                             int num_sms, cudaStream_t st) {
+    constexpr size_t smem = G5Layout<NV>::BYTES;
+    auto* kfn = query_g5_kernel<NV, W, B, U>;
+    static int occ = -1;
+    if (occ < 0) {
+        cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kfn, kThreads, smem) != cudaSuccess || occ < 1)
+            occ = 1;
+    }
+    int64_t grid = (int64_t)num_sms * occ;
+    const int64_t need = (n + kThreads - 1) / kThreads;
+    if (grid > need) grid = need;
+    if (grid < 1) grid = 1;
+    int64_t chunk = (n + grid - 1) / grid;
+    chunk = (chunk + 31) / 32 * 32;
+    grid = (n + chunk - 1) / chunk;
+    kfn<<<(unsigned)grid, kThreads, smem, st>>>(*p.dt_tmap, p, q, idx, n, chunk, out);
+    return cudaGetLastError();
+}
+
 // ----------------------------------------------------------- launchers --
 template <int G, int NV, bool W, bool B, bool U>
 static cudaError_t launch_q(const QParams& p, const pndf_query* q, const uint32_t* idx, int64_t n, float* out,
                             int num_sms, cudaStream_t st) {
+    if constexpr (G == 32 && NV <= 2) {
+        if (p.dt_tmap && p.dt_w > 0 && !g5_disabled()) return launch_g5<NV, W, B, U>(p, q, idx, n, out, num_sms, st);
+    }
     if constexpr (G == 32 && PNDF_G4D > 0 && NV <= 2) {
         if (p.dt_tmap && p.dt_w > 0 && !g4_disabled()) return launch_g4<NV, W, B, U>(p, q, idx, n, out, num_sms, st);
     }
