@@ -830,13 +830,20 @@ static cudaError_t launch_g4(const QParams& p, const pndf_query* q, const uint32
 #ifndef PNDF_G5D
 #define PNDF_G5D 2  // pair slots per warp
 #endif
+#ifndef PNDF_G5SB
+#define PNDF_G5SB 4  // steps per unrolled block (8: 197.8 ms, 4: 194.9 ms on config 5 -- half the code, fewer instruction-cache misses)
+#endif
+#ifndef PNDF_G5ELECT
+#define PNDF_G5ELECT 1  // 1: the pair copies are issued by an elect.sync lane with predicated instructions (no branch)
+#endif
 
 // a query's descriptor, then (after its step) its 32 per-lane partials.  144 B = 9 16-byte bank groups: the
 // decode's per-lane 16-byte stores to 32 consecutive slots and the end-of-batch per-lane reads of them are
 // bank-conflict free (a 128 B stride puts every lane on the same banks)
 struct __align__(16) QSlot {
     QDesc d;
-    int32_t pad[12];
+    int32_t pad[8];
+    int4 fin;  // dx row, dy row of the range table, out index, div: past the 128 B the partials overwrite
 };
 static_assert(sizeof(QSlot) == 144, "QSlot layout");
 
@@ -846,11 +853,10 @@ struct G5Layout {
     static constexpr int D2 = PNDF_G5D;
     static constexpr int SLOT_F = 4 * RP;  // [q0 dx | q0 dy | q1 dx | q1 dy]
     static constexpr size_t SLOTS = sizeof(QSlot) * kWarpsPerBlock * 32;
-    static constexpr size_t ROWS = (size_t)kWarpsPerBlock * 32 * 4 * 4;  // per query: dx row, dy row, out, div
     static constexpr size_t BARS = 128 * ((kWarpsPerBlock * D2 * 8 + 127) / 128);
     static constexpr size_t RING = (size_t)kWarpsPerBlock * D2 * SLOT_F * 4;
     static constexpr size_t RECS = (size_t)kWarpsPerBlock * 32 * 20;  // next batch: records (16 B), idx (4 B)
-    static constexpr size_t BYTES = SLOTS + ROWS + BARS + RING + RECS;
+    static constexpr size_t BYTES = SLOTS + BARS + RING + RECS;
 };
 
 __device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
@@ -872,18 +878,17 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
     constexpr int G = 32;
     constexpr int RP = LY::RP;
     constexpr int D2 = LY::D2;
-    constexpr int SB = 8;  // steps per unrolled block
+    constexpr int SB = PNDF_G5SB;  // steps per unrolled block
     static_assert((SB / 2) % D2 == 0, "pair slots must tile an unrolled block");
     constexpr int PSTRIDE = U32 ? RP : 2 * RP;
     extern __shared__ __align__(128) unsigned char qsmem[];
     QSlot* wslot = reinterpret_cast<QSlot*>(qsmem) + (threadIdx.x >> 5) * 32;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int4* wrows = reinterpret_cast<int4*>(qsmem + LY::SLOTS) + warp * 32;
-    uint64_t* wbar = reinterpret_cast<uint64_t*>(qsmem + LY::SLOTS + LY::ROWS) + warp * D2;
-    float* wring = reinterpret_cast<float*>(qsmem + LY::SLOTS + LY::ROWS + LY::BARS) + (size_t)warp * D2 * LY::SLOT_F;
+    uint64_t* wbar = reinterpret_cast<uint64_t*>(qsmem + LY::SLOTS) + warp * D2;
+    float* wring = reinterpret_cast<float*>(qsmem + LY::SLOTS + LY::BARS) + (size_t)warp * D2 * LY::SLOT_F;
     // the next batch's records (and, binned, their idx entries) arrive by cp.async while this batch runs
-    uint4* srec = reinterpret_cast<uint4*>(qsmem + LY::SLOTS + LY::ROWS + LY::BARS + LY::RING) + warp * 32;
-    uint32_t* sidx = reinterpret_cast<uint32_t*>(qsmem + LY::SLOTS + LY::ROWS + LY::BARS + LY::RING +
+    uint4* srec = reinterpret_cast<uint4*>(qsmem + LY::SLOTS + LY::BARS + LY::RING) + warp * 32;
+    uint32_t* sidx = reinterpret_cast<uint32_t*>(qsmem + LY::SLOTS + LY::BARS + LY::RING +
                                                  (size_t)kWarpsPerBlock * 32 * 16) + warp * 32;
     const float* __restrict__ Zc = p.Zc + lane * 4;
     if (lane == 0)
@@ -892,8 +897,21 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
     __syncwarp();
     uint32_t phase = 0;
     auto issue_pair = [&](int pr) {
+#if PNDF_G5ELECT
+        // every lane reads the (warp-uniform) coordinates; one elected lane arrives and issues the copy
+        const int4 ra = wslot[2 * pr].fin, rb = wslot[2 * pr + 1].fin;
+        const int k = pr % D2;
+        asm volatile(
+            "{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n"
+            " @p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%7], %8;\n"
+            " @p cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];\n}" ::"r"(smem_u32(wring + k * LY::SLOT_F)),
+            "l"(reinterpret_cast<uint64_t>(&tm)), "r"(0), "r"(ra.x), "r"(ra.y), "r"(rb.x), "r"(rb.y),
+            "r"(smem_u32(wbar + k)), "r"(4 * RP * 4)
+            : "memory");
+#else
         if (lane == 0) {
-            const int4 ra = wrows[2 * pr], rb = wrows[2 * pr + 1];
+            const int4 ra = wslot[2 * pr].fin, rb = wslot[2 * pr + 1].fin;
             const int4 rr = make_int4(ra.x, ra.y, rb.x, rb.y);
             const int k = pr % D2;
             mbar_arrive_expect_tx(wbar + k, 4 * RP * 4);
@@ -904,6 +922,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
                 "r"(smem_u32(wbar + k))
                 : "memory");
         }
+#endif
     };
 
     // one step of query s = s0 + j; NARROW: every query of the batch reads both ranges from the table
@@ -1065,7 +1084,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
             // invalid / absent records (mode 0, zero weights, NaN or no output) may take the narrow step:
             // it reads range-table row 0, finite, and their result is discarded or NaN anyway
             narrow_ok = __all_sync(0xffffffffu, d.mode == 3 || !valid);
-            wrows[lane] = make_int4((d.mode & 1) ? d.sat[0] : 0, (d.mode & 2) ? d.sat[2] : 0, d.out,
+            wslot[lane].fin = make_int4((d.mode & 1) ? d.sat[0] : 0, (d.mode & 2) ? d.sat[2] : 0, d.out,
                                     __float_as_int(d.div));
         }
         __syncwarp();
@@ -1123,7 +1142,7 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
             t[c].w += t[c + 2].w;
         }
         const float res = ((t[0].x + t[1].x) + (t[0].y + t[1].y)) + ((t[0].z + t[1].z) + (t[0].w + t[1].w));
-        const int4 mo = wrows[lane];
+        const int4 mo = wslot[lane].fin;
         __syncwarp();  // the slots are rewritten by the next batch's decode
         if (mo.z >= 0) out[mo.z] = res / __int_as_float(mo.w);  // a6: Eq. 6 mean (div = area) or sum (div = 1)
     }
