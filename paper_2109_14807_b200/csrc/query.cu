@@ -337,16 +337,7 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)
     // warp-private stable ranking: r[i] = items of the same digit earlier in this warp's segment
     uint32_t r[ITEMS / 2];  // two 16-bit ranks per register (a rank is < IPW)
     const uint32_t lt_mask = (1u << lane) - 1u;
-#if PNDF_RS_ATOMIC == 3
-    // experiment: every lane claims its own slot (ranks unique, order within a round's equal digits arbitrary)
-#pragma unroll
-    for (int i = 0; i < ITEMS; ++i) {
-        const bool ok = seg + i * 32 < nt;
-        const uint32_t d = (k[i] >> shift) & (RADIX - 1);
-        const uint32_t ri = ok ? atomicAdd(&s_cnt[warp][d], 1u) : 0u;
-        r[i >> 1] = (i & 1) ? (r[i >> 1] | (ri << 16)) : ri;
-    }
-#elif PNDF_RS_ATOMIC
+#if PNDF_RS_ATOMIC
     // each round's group leader claims its group's run with a shared-memory atomicAdd that returns the
     // digit's running count; one warp's atomics on an address are performed in program order, so runs are
     // claimed round by round (stable), and no round waits for the previous round's counter store
@@ -356,19 +347,10 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)
         const uint32_t d = (k[i] >> shift) & (RADIX - 1);
         const uint32_t peers = __match_any_sync(0xffffffffu, ok ? d : 0xffffffffu);
         const int leader = __ffs(peers) - 1;
-        const uint32_t lt = peers & lt_mask;
         uint32_t base = 0u;
-#if PNDF_RS_ATOMIC == 2
-        // predicated, not branched: the 16 rounds' match / atomic / shuffle chains can overlap
-        asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %3, 0;\n @p atom.shared.add.u32 %0, [%1], %2;\n}"
-                     : "+r"(base)
-                     : "r"(smem_u32(&s_cnt[warp][d])), "r"((uint32_t)__popc(peers)), "r"((uint32_t)(ok && lt == 0u))
-                     : "memory");
-#else
         if (ok && lane == leader) base = atomicAdd(&s_cnt[warp][d], (uint32_t)__popc(peers));
-#endif
         base = __shfl_sync(0xffffffffu, base, leader);
-        const uint32_t ri = base + __popc(lt);
+        const uint32_t ri = base + __popc(peers & lt_mask);
         r[i >> 1] = (i & 1) ? (r[i >> 1] | (ri << 16)) : ri;
     }
 #else

@@ -16,7 +16,7 @@ timeout 1500 ncu --metrics gpu__time_duration.sum --clock-control none --csv --l
 echo launches_rc=$? >> gpurun_out/ncu_launches.log
 CMD="python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline --no-parity"
 timeout 600 $CMD > gpurun_out/plain_full.log 2>&1 && \
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:query_g4 -c 1 -o gpurun_out/prof_query_full -f $CMD > gpurun_out/ncu_full.log 2>&1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:query_g5 -c 1 -o gpurun_out/prof_query_full -f $CMD > gpurun_out/ncu_full.log 2>&1
 echo full_rc=$? >> gpurun_out/ncu_full.log
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:rs_scatter -c 1 -o gpurun_out/prof_scatter_full -f $CMD > gpurun_out/ncu_scatter.log 2>&1
 echo scatter_rc=$? >> gpurun_out/ncu_scatter.log

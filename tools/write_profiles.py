@@ -47,6 +47,18 @@ def summarize(rep, nq, title, idx=0, unit="query"):
             i = hdr.index(m)
             vals[m] = (v[i], units[i])
             lines.append(f"{m:60s} {v[i]:>24s} {units[i]}")
+    stalls = []
+    for i, hname in enumerate(hdr):
+        if hname.startswith("smsp__average_warps_issue_stalled_") and hname.endswith("_per_issue_active.ratio"):
+            try:
+                stalls.append((float(v[i].replace(",", "")), hname[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")]))
+            except ValueError:
+                pass
+    if stalls:
+        lines.append("")
+        lines.append("warp stall cycles per issued instruction (top reasons):")
+        for val, name in sorted(stalls, reverse=True)[:8]:
+            lines.append(f"  {name:28s} {val:8.3f}")
     lines.append("")
 
     def num(m):
@@ -122,7 +134,7 @@ def main():
     traffic = {}
     q = os.path.join(GP, "prof_query_full.ncu-rep")
     if os.path.exists(q):
-        txt, dpq = summarize(q, nq, "pndf::query_g4_kernel (query kernel with gather4-staged range-table rows), "
+        txt, dpq = summarize(q, nq, "pndf::query_g5_kernel (lean query kernel, gather4-staged range-table rows), "
                                     "config 5, binned, U32 SATs")
         open(os.path.join(OUT, f"{rnd}_query_kernel_ncu.txt"), "w").write(txt)
         traffic["config5"] = {"dram_bytes_per_query": dpq["dram"], "l2_read_bytes_per_query": dpq["l2_read"],
