@@ -833,6 +833,9 @@ static cudaError_t launch_g4(const QParams& p, const pndf_query* q, const uint32
 #ifndef PNDF_G5SB
 #define PNDF_G5SB 4  // steps per unrolled block (8: 197.8 ms, 4: 194.9 ms on config 5 -- half the code, fewer instruction-cache misses)
 #endif
+#ifndef PNDF_G5EARLY
+#define PNDF_G5EARLY 1  // 1: a step's Zc reload is issued at the end of the previous step (0: at its own start)
+#endif
 #ifndef PNDF_G5ELECT
 #define PNDF_G5ELECT 1  // 1: the pair copies are issued by an elect.sync lane with predicated instructions (no branch)
 #endif
@@ -928,6 +931,19 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
     // one step of query s = s0 + j; NARROW: every query of the batch reads both ranges from the table
     float4 zc[NV][8];
     float pe = 0.f;  // the even step's partial, stored with the odd step's
+    // (re)load the Zc rows of the levels that differ from the previous query's (rl: level l0, rh: l0 + 1)
+    auto reload = [&](const QDesc& d, bool rl, bool rh) {
+        const int4 r03 = *reinterpret_cast<const int4*>(&d.row[0]);
+        const int4 r47 = *reinterpret_cast<const int4*>(&d.row[4]);
+        const int row[8] = {r03.x, r03.y, r03.z, r03.w, r47.x, r47.y, r47.z, r47.w};
+#pragma unroll
+        for (int v = 0; v < NV; ++v)
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk) {
+                if (rl) zc[v][kk] = ldg4_stream(Zc + (size_t)row[kk] * RP + v * G * 4);
+                if (rh) zc[v][4 + kk] = ldg4_stream(Zc + (size_t)row[4 + kk] * RP + v * G * 4);
+            }
+    };
     auto step = [&](auto narrow_tag, int s0, int j, uint32_t nb, uint32_t lob, uint32_t hib) {
         constexpr bool NARROW = decltype(narrow_tag)::value;
         const int s = s0 + j;
@@ -941,19 +957,9 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
         const float4 w03 = *reinterpret_cast<const float4*>(&d.w[0]);
         const float4 w47 = *reinterpret_cast<const float4*>(&d.w[4]);
         const float w[8] = {w03.x, w03.y, w03.z, w03.w, w47.x, w47.y, w47.z, w47.w};
-        if ((nb >> j) & 1u) {  // warp-uniform: a level's rows differ from the previous query's
-            const bool rl = !((lob >> j) & 1u), rh = !((hib >> j) & 1u);
-            const int4 r03 = *reinterpret_cast<const int4*>(&d.row[0]);
-            const int4 r47 = *reinterpret_cast<const int4*>(&d.row[4]);
-            const int row[8] = {r03.x, r03.y, r03.z, r03.w, r47.x, r47.y, r47.z, r47.w};
-#pragma unroll
-            for (int v = 0; v < NV; ++v)
-#pragma unroll
-                for (int kk = 0; kk < 4; ++kk) {
-                    if (rl) zc[v][kk] = ldg4_stream(Zc + (size_t)row[kk] * RP + v * G * 4);
-                    if (rh) zc[v][4 + kk] = ldg4_stream(Zc + (size_t)row[4 + kk] * RP + v * G * 4);
-                }
-        }
+#if !PNDF_G5EARLY
+        if ((nb >> j) & 1u) reload(d, !((lob >> j) & 1u), !((hib >> j) & 1u));
+#endif
         const float* sl = wring + k * LY::SLOT_F + (j & 1) * 2 * RP + lane * 4;
         float4 dxv[NV], dyv[NV];
 #pragma unroll
@@ -1022,6 +1028,12 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
             a0 = __ffma2_rn(exy[v], zxy, a0);
             a1 = __ffma2_rn(ezw[v], zzw, a1);
         }
+#if PNDF_G5EARLY
+        // the Zc registers are free again: the next query's reload (warp-uniform) is issued here, so its
+        // latency overlaps this step's tail, the pair copy and the next step's shared-memory loads
+        if ((nb >> (j + 1)) & 1u)
+            reload(wslot[s + 1].d, !((lob >> (j + 1)) & 1u), !((hib >> (j + 1)) & 1u));
+#endif
         const float2 a = __fadd2_rn(a0, a1);
         const float part = a.x + a.y;
         if ((j & 1) == 0) {
@@ -1094,6 +1106,9 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
         fetch_idx(bn);
         cp_async_commit();
         uint32_t nb = ~(same_lo & same_hi);  // bit j: step j reloads (shifted down a block at a time)
+#if PNDF_G5EARLY
+        reload(wslot[0].d, true, true);  // query 0 never repeats a previous query's rows
+#endif
         if (narrow_ok) {
 #pragma unroll 1
             for (int s0 = 0; s0 < 32; s0 += SB) {
