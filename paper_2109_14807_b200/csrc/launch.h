@@ -44,24 +44,6 @@ cudaError_t launch_query_hilo_clamp(int G, int NV, const QParams& p, const pndf_
 cudaError_t launch_sample_hilo_clamp(int G, int NV, const QParams& p, const pndf_query* q, const float* xi,
                                   const uint32_t* idx, int64_t n, pndf_sample* out, int num_sms, cudaStream_t st);
 
-// Tensor-core run kernel (query_tc.cuh): the eligible 128-query blocks of a binned batch (Rp == 256).
-// launch_tc_classify (query.cu) lists the aligned blocks of the sorted keys that hold one valid key:
-// list[0 .. *count) block ids (device), count zeroed by the call.
-cudaError_t launch_tc_classify(const uint32_t* sorted_keys, int64_t n, int64_t P, uint32_t* list, uint32_t* count,
-                               cudaStream_t st);
-cudaError_t launch_query_tc(const QParams& p, const pndf_query* q, const uint32_t* perm, const uint32_t* list,
-                            const uint32_t* count, float* out, int num_sms, cudaStream_t st);
-cudaError_t launch_tc_u32_wrap(const QParams& p, const pndf_query* q, const uint32_t* perm, const uint32_t* list,
-                               const uint32_t* count, float* out, int num_sms, cudaStream_t st);
-cudaError_t launch_tc_u32_clamp(const QParams& p, const pndf_query* q, const uint32_t* perm, const uint32_t* list,
-                                const uint32_t* count, float* out, int num_sms, cudaStream_t st);
-cudaError_t launch_tc_hilo_wrap(const QParams& p, const pndf_query* q, const uint32_t* perm, const uint32_t* list,
-                                const uint32_t* count, float* out, int num_sms, cudaStream_t st);
-cudaError_t launch_tc_hilo_clamp(const QParams& p, const pndf_query* q, const uint32_t* perm, const uint32_t* list,
-                                 const uint32_t* count, float* out, int num_sms, cudaStream_t st);
-// PNDF_TC=1 in the environment: binned batches of Rp == 256 stores run their one-key blocks on the tensor cores.
-bool tc_enabled();
-
 // Wang-tiled query (tiles.cu).
 cudaError_t launch_tiled_query(const QParams& p, const TileParams& tp, int G, int NV, const pndf_query* q,
                                const uint32_t* idx, int64_t n, float* out, int num_sms, cudaStream_t st);

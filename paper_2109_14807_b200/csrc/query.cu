@@ -34,14 +34,6 @@ bool g5_disabled() {
     return v != 0;
 }
 
-bool tc_enabled() {
-    static const int v = [] {
-        const char* e = getenv("PNDF_TC");
-        return (e && atoi(e) != 0) ? 1 : 0;
-    }();
-    return v != 0;
-}
-
 bool g4_disabled() {
     static const int v = [] {
         const char* e = getenv("PNDF_NOG4");
@@ -534,52 +526,10 @@ cudaError_t launch_level_sort(const QParams& p, const pndf_query* q, int64_t n, 
     return cudaGetLastError();
 }
 
-// Blocks of 128 consecutive entries of the sorted keys that hold one valid key (first == last: the keys
-// are sorted): their queries share all 8 Zc rows.  Appended warp by warp, so the list stays in key order up
-// to the order of the warps' atomics.
-__global__ void __launch_bounds__(256) tc_classify_kernel(const uint32_t* __restrict__ keys, int64_t nblocks,
-                                                          uint32_t invalid_key, uint32_t* list, uint32_t* count) {
-    const int64_t b = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    bool ok = false;
-    if (b < nblocks) {
-        const uint32_t k0 = __ldg(keys + b * 128), k1 = __ldg(keys + b * 128 + 127);
-        ok = k0 == k1 && k0 != invalid_key;
-    }
-    const uint32_t m = __ballot_sync(0xffffffffu, ok);
-    const int lane = threadIdx.x & 31;
-    uint32_t base = 0;
-    if (lane == 0 && m) base = atomicAdd(count, (uint32_t)__popc(m));
-    base = __shfl_sync(0xffffffffu, base, 0);
-    if (ok) list[base + __popc(m & ((1u << lane) - 1u))] = (uint32_t)b;
-}
-
 int64_t bin_key_space(int64_t P, int* half) {
     // half-cell keys (4 per cell) when they fit in 32 bits, else cell keys
     *half = (4 * P + 1 < (int64_t)0xffffffffLL) ? 1 : 0;
     return (*half ? 4 * P : P) + 1;
-}
-
-cudaError_t launch_tc_classify(const uint32_t* sorted_keys, int64_t n, int64_t P, uint32_t* list, uint32_t* count,
-                               cudaStream_t st) {
-    int half;
-    const int64_t nkeys = bin_key_space(P, &half);
-    cudaError_t e = cudaMemsetAsync(count, 0, sizeof(uint32_t), st);
-    if (e != cudaSuccess) return e;
-    const int64_t nblocks = n / 128;
-    if (nblocks > 0)
-        tc_classify_kernel<<<(unsigned)((nblocks + 255) / 256), 256, 0, st>>>(sorted_keys, nblocks,
-                                                                              (uint32_t)(nkeys - 1), list, count);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_query_tc(const QParams& p, const pndf_query* q, const uint32_t* perm, const uint32_t* list,
-                            const uint32_t* count, float* out, int num_sms, cudaStream_t st) {
-    if (p.Rp != 256) return cudaErrorInvalidValue;
-    if (p.prefix_u32)
-        return p.wrap ? launch_tc_u32_wrap(p, q, perm, list, count, out, num_sms, st)
-                      : launch_tc_u32_clamp(p, q, perm, list, count, out, num_sms, st);
-    return p.wrap ? launch_tc_hilo_wrap(p, q, perm, list, count, out, num_sms, st)
-                  : launch_tc_hilo_clamp(p, q, perm, list, count, out, num_sms, st);
 }
 
 cudaError_t launch_binning(const QParams& p, const pndf_query* q, int64_t n, int64_t P, BinScratch& sc,

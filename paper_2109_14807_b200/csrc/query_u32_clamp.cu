@@ -1,7 +1,6 @@
 // query_u32_clamp.cu -- query kernel instantiations: uint32 fixed-point SATs,
 // clamped neighbours (one translation unit per variant so they compile in parallel).
 #include "query_kernel.cuh"
-#include "query_tc.cuh"
 
 namespace pndf {
 
@@ -9,11 +8,6 @@ cudaError_t launch_query_u32_clamp(int G, int NV, const QParams& p, const pndf_q
                                  int64_t n, float* out, int num_sms, cudaStream_t st) {
     if (idx) return dispatch_g<false, true, true>(G, NV, p, q, idx, n, out, num_sms, st);
     return dispatch_g<false, false, true>(G, NV, p, q, idx, n, out, num_sms, st);
-}
-
-cudaError_t launch_tc_u32_clamp(const QParams& p, const pndf_query* q, const uint32_t* perm, const uint32_t* list,
-                               const uint32_t* count, float* out, int num_sms, cudaStream_t st) {
-    return launch_tc<false, true>(p, q, perm, list, count, out, num_sms, st);
 }
 
 }  // namespace pndf

@@ -259,18 +259,9 @@ pndf_status enqueue(pndf_store_s* s, Scratch& sc, const pndf_query* q, int64_t n
         const int64_t m = std::min(step, n - a);
         if (binned) {
             const uint32_t* perm = nullptr;
-            const uint32_t* keys = nullptr;
-            const bool tc = tc_enabled() && p.Rp == 256 && s->G == 32;
-            CK(launch_binning(p, q + a, m, s->P, sc, s->num_sms, st, &launches, &perm, tc ? &keys : nullptr));
+            CK(launch_binning(p, q + a, m, s->P, sc, s->num_sms, st, &launches, &perm));
             if (timing && first) CK(cudaEventRecord(s->ev[1], st));
             CK(launch_query(p, s->G, s->NV, q + a, perm, m, out + a, s->num_sms, st));
-            if (tc) {  // stage A: the one-key blocks are recomputed on the tensor cores (counts = free scratch now)
-                uint32_t* cnt = sc.counts;
-                uint32_t* list = sc.counts + 16;
-                CK(launch_tc_classify(keys, m, s->P, list, cnt, st));
-                CK(launch_query_tc(p, q + a, perm, list, cnt, out + a, s->num_sms, st));
-                launches += 3;
-            }
         } else {
             if (timing && first) CK(cudaEventRecord(s->ev[1], st));
             CK(launch_query(p, s->G, s->NV, q + a, nullptr, m, out + a, s->num_sms, st));
