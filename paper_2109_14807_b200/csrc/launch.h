@@ -16,6 +16,10 @@ bool g4_disabled();
 // PNDF_NOG5=1: G == 32 launches with a range table use query_g4_kernel instead of query_g5_kernel (A/B runs;
 // the two differ only in the order of the final rank sum).
 bool g5_disabled();
+// queries per interleaved chunk of query_g5_kernel (PNDF_G5CHUNK, default 16384, a multiple of 256)
+int64_t g5_chunk();
+// PNDF_G5ROT=0: every CTA walks its chunks in batch order (default 1: rotated start per CTA)
+bool g5_rot();
 
 // Query kernel over n records; idx != nullptr means the records are binned
 // and idx[i] is record i's position in the caller's output.

@@ -34,6 +34,24 @@ bool g5_disabled() {
     return v != 0;
 }
 
+int64_t g5_chunk() {
+    static const int64_t v = [] {
+        const char* e = getenv("PNDF_G5CHUNK");
+        int64_t c = e ? atoll(e) : 16384;
+        if (c < 256) c = 256;
+        return c / 256 * 256;
+    }();
+    return v;
+}
+
+bool g5_rot() {
+    static const int v = [] {
+        const char* e = getenv("PNDF_G5ROT");
+        return (e && atoi(e) == 0) ? 0 : 1;
+    }();
+    return v != 0;
+}
+
 bool g4_disabled() {
     static const int v = [] {
         const char* e = getenv("PNDF_NOG4");

@@ -876,7 +876,7 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int NV, bool WRAP, bool BINNED, bool U32>
 __global__ void __launch_bounds__(kThreads, PNDF_MINB)
     query_g5_kernel(const __grid_constant__ CUtensorMap tm, const QParams p, const pndf_query* __restrict__ q,
-                    const uint32_t* __restrict__ idx, int64_t n, int64_t chunk, float* __restrict__ out) {
+                    const uint32_t* __restrict__ idx, int64_t n, int64_t chunk, int rot, float* __restrict__ out) {
     using LY = G5Layout<NV>;
     constexpr int G = 32;
     constexpr int RP = LY::RP;
@@ -1048,8 +1048,17 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
         }
     };
 
-    const int64_t c0 = (int64_t)blockIdx.x * chunk;
-    const int nloc = (int)(min(n, c0 + chunk) - c0);  // this CTA's queries (chunk < 2^31)
+    // CTA b takes the chunks b, b + gridDim.x, ... of the batch: a binned batch is ordered by level, and a
+    // level-0 query (nearly every one reloads its rows) costs several coarse-level ones, so contiguous
+    // per-CTA ranges leave most SMs idle while the level-0 CTAs finish; interleaved chunks give every CTA
+    // the same level mix (and all CTAs work on one region of the map at a time: better L2 locality)
+    // rot: each CTA starts its round at a different point of the batch, so at any time the CTAs are spread
+    // over all levels and the reload-heavy level-0 phase does not hit DRAM from every SM at once
+    const int64_t nch = (n + chunk - 1) / chunk;
+    const int64_t cnt = (nch - blockIdx.x + gridDim.x - 1) / gridDim.x;  // chunks of this CTA
+    const int64_t r0 = rot ? ((int64_t)blockIdx.x * cnt) / gridDim.x : 0;
+    int64_t c0 = 0;
+    int nloc = 0;  // the current chunk's queries (chunk < 2^31)
     // each lane fetches its own record of the next batch (no cross-lane hand-off, so no warp sync)
     auto fetch_idx = [&](int blq) {
         if (BINNED && blq + lane < nloc) cp_async_4(sidx + lane, idx + c0 + blq + lane);
@@ -1059,6 +1068,10 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
             cp_async_16(srec + lane, q + (BINNED ? (int64_t)sidx[lane] : c0 + blq + lane));
         cp_async_commit();
     };
+    for (int64_t kq = 0; kq < cnt; ++kq) {
+    const int64_t kk = kq + r0 < cnt ? kq + r0 : kq + r0 - cnt;
+    c0 = ((int64_t)blockIdx.x + kk * gridDim.x) * chunk;
+    nloc = (int)(min(n, c0 + chunk) - c0);
     fetch_idx(warp * 32);
     cp_async_commit_wait_all();
     fetch_rec(warp * 32);
@@ -1161,6 +1174,8 @@ __global__ void __launch_bounds__(kThreads, PNDF_MINB)
         __syncwarp();  // the slots are rewritten by the next batch's decode
         if (mo.z >= 0) out[mo.z] = res / __int_as_float(mo.w);  // a6: Eq. 6 mean (div = area) or sum (div = 1)
     }
+    cp_async_commit_wait_all();  // nothing of this chunk's last (empty) prefetch is left in flight
+    }
 }
 
 template <int NV, bool W, bool B, bool U>
@@ -1180,8 +1195,10 @@ static cudaError_t launch_g5(const QParams& p, const pndf_query* q, const uint32
     if (grid < 1) grid = 1;
     int64_t chunk = (n + grid - 1) / grid;
     chunk = (chunk + 31) / 32 * 32;
-    grid = (n + chunk - 1) / chunk;
-    kfn<<<(unsigned)grid, kThreads, smem, st>>>(*p.dt_tmap, p, q, idx, n, chunk, out);
+    if (chunk > g5_chunk()) chunk = g5_chunk();  // large batches: interleaved chunks (see the kernel)
+    const int64_t nchunks = (n + chunk - 1) / chunk;
+    if (grid > nchunks) grid = nchunks;
+    kfn<<<(unsigned)grid, kThreads, smem, st>>>(*p.dt_tmap, p, q, idx, n, chunk, g5_rot() ? 1 : 0, out);
     return cudaGetLastError();
 }
 
