@@ -111,6 +111,17 @@ def issue_ceiling(inst_per_unit):
     return sms * 4 * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / inst_per_unit if inst_per_unit else None
 
 
+def query_kernel_name(st):
+    """The query kernel a store's batches launch (csrc/query_kernel.cuh launch_q): 32 lanes per query, at most
+    2 float4 per lane and a range table -> query_g5_kernel (unless PNDF_NOG5 / PNDF_NOG4), else query_kernel."""
+    g32 = st["lanes_per_query"] == 32 and st["rank_padded"] <= 256 and st.get("range_table_width", 0) > 0
+    if g32 and not int(os.environ.get("PNDF_NOG5", "0") or 0):
+        return "pndf::query_g5_kernel"
+    if g32 and not int(os.environ.get("PNDF_NOG4", "0") or 0):
+        return "pndf::query_g4_kernel"
+    return "pndf::query_kernel"
+
+
 def alu_roof(flop_per_unit, units, k_ms, kernel, unit_name, **extra):
     """`roofline` object against the FP32 ALU ceiling (the binding roof of these gather-and-reduce kernels
     once binning keeps the Zc rows on chip: DESIGN.md §5)."""
@@ -518,7 +529,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             "l2_angular_rows": (l2_gbs * 1e9 / (ang_rows * 4 * Rp)) if l2_gbs else None,
             "hbm_compulsory": hbm * 1e9 / (comp / n),
             "issue": issue_ceiling(tr.get("warp_instructions_per_query")) if tr else None}
-    roof = alu_roof(FLOP_RANK_QUERY * cfg.R, n, q_ms, "pndf::query_kernel", "query",
+    roof = alu_roof(FLOP_RANK_QUERY * cfg.R, n, q_ms, query_kernel_name(st), "query",
                     traffic=traffic, traffic_source=None if tr is None else tr.get("source"),
                     ceilings_queries_per_s=ceil, achieved_queries_per_s=n / (q_ms * 1e-3),
                     hbm_compulsory={"bytes": comp, "distinct_zc_rows": rows_u, "gbs": comp / (q_ms * 1e-3) / 1e9,
@@ -827,7 +838,7 @@ def run_sg_op(args, cfg, rank, world, local_rank):
             "config": {"workload": workload_name(cfg) + "; SG lights: lambda log-U[10,1000], A U[0.5,2], "
                                                          "half vector Beckmann 0.3, eps 0.3",
                        "queries_total": n_total, "binned": bool(st["last_binned"])},
-            "roofline": alu_roof(FLOP_RANK_QUERY * cfg.R, n, q_ms, "pndf::query_kernel (after sg_rect_kernel)",
+            "roofline": alu_roof(FLOP_RANK_QUERY * cfg.R, n, q_ms, query_kernel_name(st) + " (after sg_rect_kernel)",
                                  "query", touched_bytes_per_query=Bq, step_ms=ms_rank),
             "cpu_baseline": {"value": cpu_rate, "unit": "queries/s", "cores": oracle.max_threads(),
                              "kind": "oracle", "sample": f"{idx.shape[0]} queries of the timed batch"},
