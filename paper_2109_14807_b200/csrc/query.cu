@@ -339,6 +339,14 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)
     const int nt = (int)((n - t0) < (int64_t)kRsTile ? (n - t0) : (int64_t)kRsTile);
     const int seg = warp * IPW + lane;  // tile-local index of item 0 of this lane
 
+    // this tile's global run starts (one strided 4-byte load per digit): fetched now by every thread so
+    // their latency hides behind the key loads instead of sitting in warp 0's scan between two barriers
+    uint32_t goff_r[(RADIX + THREADS - 1) / THREADS];
+#pragma unroll
+    for (int j = 0; j < (RADIX + THREADS - 1) / THREADS; ++j) {
+        const int d = t + j * THREADS;
+        goff_r[j] = d < RADIX ? __ldg(offsets + (int64_t)d * ntiles + blockIdx.x) : 0u;
+    }
     uint32_t k[ITEMS], v[ITEMS];
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
@@ -424,11 +432,15 @@ __global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)
         for (int j = 0; j < DPL; ++j) {
             const int d = lane * DPL + j;
             s_start[d] = acc;
-            s_goff[d] = offsets[(int64_t)d * ntiles + blockIdx.x] - acc;
             acc += c[j];
         }
     }
     __syncthreads();
+#pragma unroll
+    for (int j = 0; j < (RADIX + THREADS - 1) / THREADS; ++j) {
+        const int d = t + j * THREADS;
+        if (d < RADIX) s_goff[d] = goff_r[j] - s_start[d];
+    }
 #pragma unroll
     for (int i = 0; i < ITEMS; ++i) {
         if (seg + i * 32 < nt) {
