@@ -459,3 +459,47 @@ def test_rows_touched_counts_distinct_neighbour_rows(k, wrap):
     want = np.unique(rows[valid].reshape(-1)).shape[0]
     assert int(d_rows.item()) == want
     st.free()
+
+
+_CHUNK_SCRIPT = r"""
+import sys
+import numpy as np
+import oracle, synth
+from tests._util import assert_parity, run_gpu
+N, s0, L, A, R, wrap = 64, 1, 7, 32, 256, {wrap}
+P = sum((N // (s0 << l)) ** 2 for l in range(L))
+f = synth.random_factors(A, R, P, seed=11, sparsity=0.4)
+rng = np.random.default_rng(12)
+n = 100003
+x1 = rng.integers(0, A, n)
+y1 = rng.integers(0, A, n)
+x2 = np.minimum(A - 1, x1 + rng.integers(0, 9, n))
+y2 = np.minimum(A - 1, y1 + rng.integers(0, 9, n))
+recs = synth.make_records(rng.uniform(-N, 2 * N, n), rng.uniform(-N, 2 * N, n),
+                          np.exp2(rng.uniform(-1.0, L + 1.0, n)), x1, x2, y1, y2)
+ref = oracle.query_batch(oracle.make_desc(N, s0, L, A, R, wrap), f.C, f.X, f.Y, f.Z, recs, mean=True)
+outs = []
+for opts in (0, 2):
+    got, st = run_gpu(dict(N=N, s0=s0, L=L, A=A, R=R, wrap=wrap), f, recs, opts)
+    assert st == 0
+    assert_parity(got, ref, "chunked g5 opts=%d" % opts)
+    outs.append(np.asarray(got, np.float32).tobytes())
+assert outs[0] == outs[1], "binned and unbinned results differ in bits"
+print("ok")
+"""
+
+
+@pytest.mark.parametrize("wrap", [True, False])
+def test_g5_interleaved_chunks_small_chunk(wrap):
+    """query_g5_kernel walks the batch in interleaved chunks.  With PNDF_G5CHUNK=256
+    (read once at library load, hence the subprocess) a 100,003-query batch is 391 chunks over at most 296
+    CTAs: several chunks per CTA, a rotated start, a ragged last chunk -- against the oracle, binned and
+    unbinned, bitwise equal to each other."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PNDF_G5CHUNK="256", PYTHONPATH=root + os.pathsep + os.environ.get("PYTHONPATH", ""))
+    r = subprocess.run([sys.executable, "-c", _CHUNK_SCRIPT.format(wrap=wrap)], cwd=root, env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and r.stdout.strip().endswith("ok"), r.stdout[-2000:] + r.stderr[-4000:]
