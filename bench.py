@@ -528,7 +528,11 @@ def run_ours(args, cfg, rank, world, local_rank):
     ceil = {"fp32_alu": fp32_peak_tflops() * 1e12 / (FLOP_RANK_QUERY * cfg.R),
             "l2_angular_rows": (l2_gbs * 1e9 / (ang_rows * 4 * Rp)) if l2_gbs else None,
             "hbm_compulsory": hbm * 1e9 / (comp / n),
-            "issue": issue_ceiling(tr.get("warp_instructions_per_query")) if tr else None}
+            "issue": issue_ceiling(tr.get("warp_instructions_per_query")) if tr else None,
+            # query_g5_kernel: both range rows cross the SM's shared-memory path twice (gather4 in, LDS.128
+            # out) at 128 B per cycle, + ~6 wavefronts of descriptors, weights and partials
+            "smem_path": (issue_ceiling(4.0 * (2 * ang_rows * 4 * Rp / 128 + 6)))
+            if query_kernel_name(st) == "pndf::query_g5_kernel" else None}
     roof = alu_roof(FLOP_RANK_QUERY * cfg.R, n, q_ms, query_kernel_name(st), "query",
                     traffic=traffic, traffic_source=None if tr is None else tr.get("source"),
                     ceilings_queries_per_s=ceil, achieved_queries_per_s=n / (q_ms * 1e-3),
@@ -543,6 +547,10 @@ def run_ours(args, cfg, rank, world, local_rank):
                          "beside it; touched_bytes_per_query (20 + 48R, the method's 12 look-ups) is not a roof: "
                          "binned queries reuse Zc rows from registers",
                     binning_ms=b_ms, query_share_of_step=q_ms / ms_rank if ms_rank else None)
+    # the ceiling the kernel sits closest to (frac above stays the FP32 one the contract names)
+    fr = {k: (n / (q_ms * 1e-3)) / v for k, v in ceil.items() if v}
+    near = max(fr, key=fr.get)
+    roof["closest_ceiling"] = {"name": near, "frac": fr[near]}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, f, bins, i0, args.cpu_seconds)
