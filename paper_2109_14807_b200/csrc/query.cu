@@ -229,8 +229,14 @@ __global__ void __launch_bounds__(kScanThreads) scan_apply_kernel(uint32_t* inou
 #define PNDF_RS_ATOMIC 1  // radix scatter ranking: 1 = leader atomics (pipelined rounds), 0 = load/store counters
 #endif
 constexpr int kRsThreads = 256;
-constexpr int kRsItems = 16;
-constexpr int kRsTile = kRsThreads * kRsItems;  // 4096 keys per tile
+#ifndef PNDF_RS_ITEMS
+#define PNDF_RS_ITEMS 28  // keys per thread of a radix tile (256 threads): 7168-key tiles, 2 CTAs per SM (config 5 binning: 16 -> 28.9 ms, 24 -> 28.3, 28 -> 26.5, 32 -> 27.0, 36 -> 31.7)
+#endif
+#ifndef PNDF_RS_MINB
+#define PNDF_RS_MINB 2
+#endif
+constexpr int kRsItems = PNDF_RS_ITEMS;
+constexpr int kRsTile = kRsThreads * kRsItems;  // 7168 keys per tile
 constexpr int kRsWarps = kRsThreads / 32;
 
 // counts[d * ntiles + tile] = #keys of the tile whose digit is d (digits of BITS bits).
@@ -317,7 +323,7 @@ __global__ void __launch_bounds__(kRsThreads) bin_keys_kernel(const QParams p, c
 // order, then written out so that consecutive items of a digit run go to
 // consecutive global addresses.
 template <int BITS, int THREADS, bool LATE_V>
-__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : 3)) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : PNDF_RS_MINB)) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in, int64_t n,
                                                                 int shift, const uint32_t* __restrict__ offsets,
                                                                 int64_t ntiles, uint32_t* keys_out,
@@ -495,7 +501,7 @@ static bool scatter_late_v() {
     return v;
 }
 
-// scatter CTA size: 256 (default) or 512 threads per 4096-key tile (PNDF_SCATTER_THREADS, for A/B runs)
+// scatter CTA size: 256 (default) or 512 threads per tile (PNDF_SCATTER_THREADS, for A/B runs)
 static int scatter_threads() {
     static int v = [] {
         const char* e = getenv("PNDF_SCATTER_THREADS");
