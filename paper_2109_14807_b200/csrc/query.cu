@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(kRsThreads) bin_keys_kernel(const QParams p, c
 // order, then written out so that consecutive items of a digit run go to
 // consecutive global addresses.
 template <int BITS, int THREADS, bool LATE_V>
-__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 2 : (LATE_V ? 4 : PNDF_RS_MINB)) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
+__global__ void __launch_bounds__(THREADS, THREADS >= 512 ? 1 : PNDF_RS_MINB) rs_scatter_kernel(const uint32_t* __restrict__ keys_in,
                                                                 const uint32_t* __restrict__ vals_in, int64_t n,
                                                                 int shift, const uint32_t* __restrict__ offsets,
                                                                 int64_t ntiles, uint32_t* keys_out,
